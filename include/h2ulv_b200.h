@@ -1,0 +1,277 @@
+/*
+ * h2ulv_b200.h — C ABI of the B200-native H²-ULV factorize/solve path.
+ *
+ * The reference (`h2ulv`, /root/reference/pkg) is pure Python and has no
+ * FFI; its dense engine is `dense_core.run_plan` driving LAPACK/BLAS one
+ * block at a time (dense_core.py:229-284, called from ulv_factor._run,
+ * ulv_factor.py:145-151).  This library replaces that engine: every entry
+ * point below executes ONE batched phase of a level (all boxes / all pairs
+ * at once) on the GPU.  The Python mirror of the reference API
+ * (paper_2502_02395_b200/ulv_factor.py, ulv_solve.py, h2_build.py) binds
+ * these symbols through ctypes.
+ *
+ * Conventions
+ *   - all matrices are FP64, row-major (numpy C order): element (r, c) of
+ *     a matrix X with leading dimension ld is X[r*ld + c];
+ *   - every descriptor array and tile/CTA map passed as `d_*` lives in
+ *     device memory; scalars are host values;
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     asynchronous on that stream;
+ *   - every function returns 0 on success or a nonzero H2G_E* code; the
+ *     message is available from h2g_last_error().  No exception crosses the
+ *     ABI.  Numerical breakdown (non-positive pivot) is reported through
+ *     the device array `d_npd`, see h2g_panel_potrf.
+ */
+#ifndef H2ULV_B200_H
+#define H2ULV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2G_ABI_VERSION 1
+
+enum {
+  H2G_OK = 0,
+  H2G_EINVAL = 1,   /* bad argument (null pointer, negative size, ...)   */
+  H2G_ECUDA = 2,    /* a CUDA runtime call or launch failed               */
+  H2G_ESTEP = 3     /* unknown step kind in a program                     */
+};
+
+/* ---- grouped GEMM ---------------------------------------------------------
+ * C = alpha * op(A) * op(B) + beta * C  for every problem of the group.
+ * op(A) is M x K, op(B) is K x N.  trans_a / trans_b are uniform for the
+ * launch.  flags bit 0 (H2G_GEMM_LOWER, requires M == N) computes only the
+ * 64x64 output tiles on or below the diagonal (SYRK-style Schur updates).
+ * `tile_start` is the problem's first tile in the launch; d_tile_map[t] is
+ * the problem index of tile t (t < total_tiles).
+ * Replaces: dense_core.multiply (dense_core.py:84-93) for the phases
+ * diag_mul1/2, off_mul1/2 and diag_schur (ulv_factor.py:189-200, 236-259).
+ */
+#define H2G_GEMM_LOWER 1
+typedef struct h2g_gemm_problem {
+  const double* A;
+  const double* B;
+  double* C;
+  int32_t M, N, K;
+  int32_t lda, ldb, ldc;
+  int32_t tile_start;
+  int32_t flags;
+  double alpha, beta;
+} h2g_gemm_problem;
+
+int h2g_gemm_tiles(int M, int N, int flags); /* tiles one problem needs */
+int h2g_gemm_grouped(int trans_a, int trans_b, const h2g_gemm_problem* d_probs,
+                     const int32_t* d_tile_map, int total_tiles, void* stream);
+
+/* ---- panel of the partial (ULV) Cholesky ----------------------------------
+ * For one box: factor the b x b diagonal block H[p:p+b, p:p+b] (b <= 64) in
+ * place (lower Cholesky) and overwrite every row x of
+ *   H[p+b : n, p : p+b]   and   R[0 : nr, p : p+b]
+ * with x * L^-T.  Together with the trailing update (h2g_gemm_grouped, NT,
+ * alpha=-1, beta=1) this is the right-looking partial Cholesky of the
+ * sparsified diagonal block that yields L(r)_ii, L(s)_ii, V_i and the single
+ * Schur update of SS_ii in ONE pass (ulv_factor.py:217-241 =
+ * factor_diag, ulv_factor.py:78-84).  The descriptor's CTAs split the rows;
+ * d_cta_map[c] is the descriptor of CTA c.  A pivot that is not > 0 (or
+ * NaN) at column p+j records atomicMin(&d_npd[npd_slot], p+j) — the same
+ * pivot index dpotrf's info-1 reports (dense_core.py:60-63).
+ */
+typedef struct h2g_panel_desc {
+  double* H;
+  double* R;          /* may be NULL when nr == 0 */
+  int32_t ldh, ldr;
+  int32_t n;          /* rows of H (trailing rows p+b..n-1 get the TRSM) */
+  int32_t nr;         /* rows of R */
+  int32_t p, b;       /* panel start column and width (1..64) */
+  int32_t npd_slot;   /* index into d_npd */
+  int32_t cta_start;  /* first CTA of this descriptor */
+  int32_t rows_per_cta;
+  int32_t pad_;
+} h2g_panel_desc;
+
+int h2g_panel_potrf(const h2g_panel_desc* d_descs, const int32_t* d_cta_map,
+                    int total_ctas, int32_t* d_npd, void* stream);
+
+/* ---- block copy / gather ----------------------------------------------------
+ * dst[r, c] = src(r, c) for an rows x cols block, where src(r, c) is
+ *   mode 0: src[r*lds + c]            (copy)
+ *   mode 1: src[c*lds + r]            (transpose)
+ *   mode 2: src[max(r,c)*lds + min(r,c)]  (symmetric from the lower half)
+ *   mode 3: (r == c) ? 1 : 0              (identity fill; src unused)
+ * 32x32 tiles; d_tile_map[t] = descriptor of tile t.
+ * Replaces: merge_level / inject_couplings (ulv_factor.py:108-132, 289-303)
+ * — the 2x2 assembly of child SS blocks (and far couplings) into the parent
+ * near blocks.
+ */
+typedef struct h2g_copy_desc {
+  const double* src;
+  double* dst;
+  int32_t rows, cols;
+  int32_t lds, ldd;
+  int32_t mode;
+  int32_t tile_start;
+} h2g_copy_desc;
+
+int h2g_copy_tiles(int rows, int cols);
+int h2g_block_copy(const h2g_copy_desc* d_descs, const int32_t* d_tile_map,
+                   int total_tiles, void* stream);
+
+/* ---- substitution ------------------------------------------------------------
+ * Vectors are blocks of `w` columns, row-major with leading dimension w.
+ *
+ * h2g_gemv_grouped: for every output segment o (one CTA each)
+ *   y_o = init_o - sum_t op(A_t) x_t           (init_o may alias y_o or be NULL = 0)
+ * or, with H2G_GEMV_SPLIT, y = op(A) x written as rows [0, split) -> y and
+ * rows [split, m) -> y2 (the basis transform of _transform_in,
+ * ulv_solve.py:33-41, split = r).  Terms of output o are
+ * d_terms[term_begin .. term_end).  With H2G_GEMV_PLUS the sum is added.
+ * Replaces the per-box numpy products of _forward/_backward
+ * (ulv_solve.py:98-113, 144-181).
+ */
+#define H2G_GEMV_PLUS 1
+#define H2G_GEMV_SPLIT 2
+typedef struct h2g_gemv_term {
+  const double* A;
+  const double* x;
+  int32_t lda;
+  int32_t trans;   /* 0: A is m x K ; 1: A is K x m (use A^T) */
+  int32_t K;
+  int32_t pad_;
+} h2g_gemv_term;
+
+typedef struct h2g_gemv_out {
+  double* y;
+  double* y2;        /* SPLIT only */
+  const double* init;
+  int32_t m;         /* rows of y (before split) */
+  int32_t split;     /* SPLIT only */
+  int32_t term_begin, term_end;
+  int32_t flags;
+  int32_t pad_;
+} h2g_gemv_out;
+
+int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
+                     int w, void* stream);
+
+/* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
+ * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
+ * leading dimension ldl (dense_core.tri_solve, dense_core.py:69-81).
+ */
+typedef struct h2g_trsv_desc {
+  const double* L;
+  double* x;
+  int32_t n;
+  int32_t ldl;
+} h2g_trsv_desc;
+
+int h2g_trsv_batched(const h2g_trsv_desc* d_descs, int count, int trans, int w, void* stream);
+
+/* ---- complementary basis: batched Householder QR ----------------------------
+ * Blocked Householder QR of Z_i (n_i x k_i, in place) in panels of <= 32
+ * columns, LAPACK conventions (dgeqrf/dlarfg).  h2g_qr_panel factors the
+ * panel Z[p:n, p:p+b] of every box in place (R on/above the diagonal,
+ * reflectors below with implicit unit diagonal), copies the reflectors with
+ * their unit diagonal into V[p:n, p:p+b], writes tau[p..p+b) and the b x b
+ * upper-triangular block factor T (H_p...H_{p+b-1} = I - V T V^T), so that
+ * the trailing update (C -= V T^T V^T C) and the explicit formation of Q
+ * (Q <- Q - V T V^T Q, last panel first) are h2g_gemm_grouped calls.
+ * Replaces: np.linalg.qr(z, mode="complete") in id_basis
+ * (dense_core.py:136-144), i.e. the ① complementary basis.
+ */
+typedef struct h2g_qr_panel_desc {
+  double* Z;         /* n x k, ld ldz */
+  double* V;         /* explicit reflectors, same layout as Z (zero-initialised) */
+  double* tau;       /* length >= k */
+  double* T;         /* 32 x 32 block factor for this panel, ld 32 */
+  int32_t n, ldz;
+  int32_t p, b;
+} h2g_qr_panel_desc;
+
+int h2g_qr_panel(const h2g_qr_panel_desc* d_descs, int count, void* stream);
+
+/* h2g_basis_finish: given Q (n x n, explicit) and the factored Z (R in the
+ * upper triangle), apply the sign convention of id_basis
+ * (dense_core.py:140-144): s = sign(diag R[:k,:k]) (0 -> +1),
+ * Q[:, :k] *= s, and frame = s[:,None] * R[:k, :] (k x k).  Then reorder the
+ * columns of Q into q_full = [q_red | q_skel] in place order.
+ */
+typedef struct h2g_basis_desc {
+  const double* Q;   /* n x n explicit Householder product (input) */
+  const double* Z;   /* factored Z (R upper), ld ldz */
+  double* qfull;     /* n x n output = [q_red | q_skel] */
+  double* frame;     /* k x k output */
+  int32_t n, k, ldz;
+  int32_t pad_;
+} h2g_basis_desc;
+
+int h2g_basis_finish(const h2g_basis_desc* d_descs, int count, void* stream);
+
+/* ---- kernel matrix blocks ------------------------------------------------------
+ * out[a, b] = K(|x_rows[a] - x_cols[b]|) with K = 1/r (laplace) or
+ * exp(-decay r)/r (yukawa); out = shift where the two global point ids are
+ * equal (kernels.gen_block, kernels.py:46-64).  Coincident distinct points
+ * set d_coincident[0] = 1 (the host then locates the pair and raises
+ * CoincidentPointsError like kernels.py:55-57).
+ */
+typedef struct h2g_kblock_desc {
+  const int64_t* rows;
+  const int64_t* cols;
+  double* out;
+  int32_t m, n, ldo;
+  int32_t tile_start;
+} h2g_kblock_desc;
+
+int h2g_kernel_blocks(const h2g_kblock_desc* d_descs, const int32_t* d_tile_map, int total_tiles,
+                      const double* d_points, int family, double shift, double decay,
+                      int64_t* d_coincident, void* stream);
+
+/* ---- native executor ---------------------------------------------------------
+ * A factorization is a static list of steps (one batched phase each); the
+ * executor issues them back to back on `stream` without returning to
+ * Python, optionally captured once into a CUDA graph and replayed.
+ */
+enum {
+  H2G_STEP_GEMM_NN = 0,
+  H2G_STEP_GEMM_NT = 1,
+  H2G_STEP_GEMM_TN = 2,
+  H2G_STEP_GEMM_TT = 3,
+  H2G_STEP_PANEL = 4,
+  H2G_STEP_COPY = 5,
+  H2G_STEP_MEMCPY = 6,   /* descs = dst, map = src (bytes in count) */
+  H2G_STEP_QR_PANEL = 7,
+  H2G_STEP_BASIS = 8,
+  H2G_STEP_GEMV = 9,     /* descs = outs, map = terms, grid = w            */
+  H2G_STEP_TRSV = 10,    /* descs = trsv descs, grid = w, arg = trans      */
+  H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
+                            npd = coincident flag; arg = family; shift/decay
+                            in the two doubles                              */
+};
+
+typedef struct h2g_step {
+  int32_t kind;
+  int32_t count;      /* problems / descriptors (bytes for MEMCPY) */
+  int32_t grid;       /* tiles or CTAs (w for GEMV/TRSV) */
+  int32_t arg;        /* TRSV: trans; KBLOCK: family */
+  const void* descs;  /* device descriptor array */
+  const int32_t* map; /* device tile / CTA map */
+  int32_t* npd;       /* PANEL: device pivot-status array */
+  const void* aux;    /* KBLOCK: device points (N x 3) */
+  double d0, d1;      /* KBLOCK: shift, decay */
+} h2g_step;
+
+int h2g_run_program(const h2g_step* steps, int nsteps, void* stream);
+int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out);
+int h2g_graph_launch(void* exec, void* stream);
+int h2g_graph_destroy(void* exec);
+
+int h2g_abi_version(void);
+const char* h2g_last_error(void);
+int h2g_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2ULV_B200_H */

@@ -1,0 +1,122 @@
+"""ctypes binding of libh2ulv_b200.so (the C ABI in include/h2ulv_b200.h).
+
+There is deliberately no fallback: if the library cannot be loaded or no
+CUDA device is present, `lib()` raises NativeUnavailableError.  Descriptor
+arrays are numpy structured arrays whose layout mirrors the C structs
+byte for byte (checked against the struct sizes at import).
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import NativeUnavailableError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libh2ulv_b200.so")
+
+# --- descriptor layouts (must match include/h2ulv_b200.h) -------------------------------
+GEMM_DT = np.dtype([("A", "<u8"), ("B", "<u8"), ("C", "<u8"), ("M", "<i4"), ("N", "<i4"), ("K", "<i4"),
+                    ("lda", "<i4"), ("ldb", "<i4"), ("ldc", "<i4"), ("tile_start", "<i4"), ("flags", "<i4"),
+                    ("alpha", "<f8"), ("beta", "<f8")])
+PANEL_DT = np.dtype([("H", "<u8"), ("R", "<u8"), ("ldh", "<i4"), ("ldr", "<i4"), ("n", "<i4"), ("nr", "<i4"),
+                     ("p", "<i4"), ("b", "<i4"), ("npd_slot", "<i4"), ("cta_start", "<i4"),
+                     ("rows_per_cta", "<i4"), ("pad_", "<i4")])
+COPY_DT = np.dtype([("src", "<u8"), ("dst", "<u8"), ("rows", "<i4"), ("cols", "<i4"), ("lds", "<i4"),
+                    ("ldd", "<i4"), ("mode", "<i4"), ("tile_start", "<i4")])
+GEMV_TERM_DT = np.dtype([("A", "<u8"), ("x", "<u8"), ("lda", "<i4"), ("trans", "<i4"), ("K", "<i4"),
+                         ("pad_", "<i4")])
+GEMV_OUT_DT = np.dtype([("y", "<u8"), ("y2", "<u8"), ("init", "<u8"), ("m", "<i4"), ("split", "<i4"),
+                        ("term_begin", "<i4"), ("term_end", "<i4"), ("flags", "<i4"), ("pad_", "<i4")])
+TRSV_DT = np.dtype([("L", "<u8"), ("x", "<u8"), ("n", "<i4"), ("ldl", "<i4")])
+QRP_DT = np.dtype([("Z", "<u8"), ("V", "<u8"), ("tau", "<u8"), ("T", "<u8"), ("n", "<i4"), ("ldz", "<i4"),
+                   ("p", "<i4"), ("b", "<i4")])
+BASIS_DT = np.dtype([("Q", "<u8"), ("Z", "<u8"), ("qfull", "<u8"), ("frame", "<u8"), ("n", "<i4"), ("k", "<i4"),
+                     ("ldz", "<i4"), ("pad_", "<i4")])
+KBLOCK_DT = np.dtype([("rows", "<u8"), ("cols", "<u8"), ("out", "<u8"), ("m", "<i4"), ("n", "<i4"),
+                      ("ldo", "<i4"), ("tile_start", "<i4")])
+STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", "<i4"), ("descs", "<u8"),
+                    ("map", "<u8"), ("npd", "<u8"), ("aux", "<u8"), ("d0", "<f8"), ("d1", "<f8")])
+
+assert GEMM_DT.itemsize == 72 and PANEL_DT.itemsize == 56 and COPY_DT.itemsize == 40
+assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 24
+assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 64
+
+STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "PANEL": 4, "COPY": 5, "MEMCPY": 6,
+        "QR_PANEL": 7, "BASIS": 8, "GEMV": 9, "TRSV": 10, "KBLOCK": 11}
+GEMM_LOWER = 1
+GEMV_PLUS = 1
+GEMV_SPLIT = 2
+GEMM_TILE = 64
+COPY_TILE = 32
+PANEL_WIDTH = 64
+QR_PANEL_WIDTH = 32
+
+EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_panel_potrf", "h2g_copy_tiles", "h2g_block_copy",
+           "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
+           "h2g_run_program", "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
+           "h2g_last_error", "h2g_device_sm_count"]
+
+_LIB = None
+
+
+def load_library(path=LIB_PATH):
+    """Load the shared library without touching the GPU (CPU-safe)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise NativeUnavailableError(
+            f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i32 = ctypes.c_void_p, ctypes.c_int
+    sig = {
+        "h2g_gemm_tiles": (i32, [i32, i32, i32]),
+        "h2g_gemm_grouped": (i32, [i32, i32, vp, vp, i32, vp]),
+        "h2g_panel_potrf": (i32, [vp, vp, i32, vp, vp]),
+        "h2g_copy_tiles": (i32, [i32, i32]),
+        "h2g_block_copy": (i32, [vp, vp, i32, vp]),
+        "h2g_gemv_grouped": (i32, [vp, i32, vp, i32, vp]),
+        "h2g_trsv_batched": (i32, [vp, i32, i32, i32, vp]),
+        "h2g_qr_panel": (i32, [vp, i32, vp]),
+        "h2g_basis_finish": (i32, [vp, i32, vp]),
+        "h2g_kernel_blocks": (i32, [vp, vp, i32, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp]),
+        "h2g_run_program": (i32, [vp, i32, vp]),
+        "h2g_graph_capture": (i32, [vp, i32, vp, ctypes.POINTER(vp)]),
+        "h2g_graph_launch": (i32, [vp, vp]),
+        "h2g_graph_destroy": (i32, [vp]),
+        "h2g_abi_version": (i32, []),
+        "h2g_last_error": (ctypes.c_char_p, []),
+        "h2g_device_sm_count": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.h2g_abi_version() != 1:
+        raise NativeUnavailableError("libh2ulv_b200.so ABI version mismatch")
+    _LIB = lib
+    return lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is usable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the H2-ULV path runs only on the GPU (no CPU fallback)")
+    return load_library()
+
+
+def check(rc, what="h2g call"):
+    if rc != 0:
+        msg = load_library().h2g_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

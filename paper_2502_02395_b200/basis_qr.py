@@ -1,0 +1,132 @@
+"""① Complementary basis on the GPU: batched blocked Householder QR.
+
+For every box of a level, Z_i (n_i x k_i) is factored Z = Q R with the
+LAPACK conventions of `np.linalg.qr(z, mode="complete")` (dgeqrf + dorgqr)
+that the reference calls in id_basis (dense_core.py:136-144); then the sign
+fix s = sign(diag R) (0 -> +1), q_skel = Q[:, :k] s, frame = s R[:k, :],
+q_red = Q[:, k:] (dense_core.py:140-144) and q_full = [q_red | q_skel].
+
+Program per level (all boxes in every launch), panels of 32 columns:
+  factor:  QR_PANEL(p); W = V_p^T C; W2 = T_p^T W; C -= V_p W2   (C = Z[p:, p+b:])
+  form Q:  Q = I; for p = last..0:  W = V_p^T Q_s; W2 = T_p W; Q_s -= V_p W2
+           (Q_s = Q[p:, p:], backward accumulation as in dorgqr)
+  finish:  BASIS (sign fix, [q_red | q_skel], frame)
+"""
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .program import Program
+
+F64 = torch.float64
+QB = nat.QR_PANEL_WIDTH
+
+
+class LevelQR:
+    """Device buffers + program of the complete QR of one level's Z_i."""
+
+    def __init__(self, device, n, k, z_ptrs=None):
+        self.device = device
+        self.n = np.asarray(n, dtype=np.int64)
+        self.k = np.asarray(k, dtype=np.int64)
+        nb = len(self.n)
+        self.zoff = np.concatenate([[0], np.cumsum(self.n * self.k)[:-1]]).astype(np.int64)
+        self.qoff = np.concatenate([[0], np.cumsum(self.n * self.n)[:-1]]).astype(np.int64)
+        self.foff = np.concatenate([[0], np.cumsum(self.k * self.k)[:-1]]).astype(np.int64)
+        zs = max(int((self.n * self.k).sum()), 1)
+        self.Z = torch.zeros(zs, dtype=F64, device=device)
+        self.V = torch.zeros(zs, dtype=F64, device=device)
+        self.Q = torch.empty(max(int((self.n * self.n).sum()), 1), dtype=F64, device=device)
+        self.qfull = torch.empty_like(self.Q)
+        self.frame = torch.empty(max(int((self.k * self.k).sum()), 1), dtype=F64, device=device)
+        npan = -(-self.k // QB)
+        self.toff = np.concatenate([[0], np.cumsum(npan * QB * QB)[:-1]]).astype(np.int64)
+        self.T = torch.zeros(max(int(npan.sum()) * QB * QB, 1), dtype=F64, device=device)
+        self.tau = torch.zeros(max(int(self.k.sum()), 1), dtype=F64, device=device)
+        self.tauoff = np.concatenate([[0], np.cumsum(self.k)[:-1]]).astype(np.int64)
+        wsz = max(int((QB * np.maximum(self.n, 1)).sum()), 1)
+        self.woff = np.concatenate([[0], np.cumsum(QB * self.n)[:-1]]).astype(np.int64)
+        self.W = torch.empty(wsz, dtype=F64, device=device)
+        self.W2 = torch.empty(wsz, dtype=F64, device=device)
+        self.nb = nb
+
+    def ptr(self, t, off):
+        return t.data_ptr() + 8 * int(off)
+
+    def build(self, prog):
+        n, k, nb = self.n, self.k, self.nb
+        # identity for boxes with k == 0 (q_red = I) and as the start of dorgqr
+        prog.copy([(0, self.ptr(self.Q, self.qoff[i]), int(n[i]), int(n[i]), 0, int(n[i]), 3) for i in range(nb)])
+        kmax = int(k.max()) if nb else 0
+        panels = list(range(0, kmax, QB))
+        for p in panels:
+            descs, g1, g2, g3 = [], [], [], []
+            for i in range(nb):
+                ni, ki = int(n[i]), int(k[i])
+                if ki <= p:
+                    continue
+                b = min(QB, ki - p)
+                zi, vi = self.ptr(self.Z, self.zoff[i]), self.ptr(self.V, self.zoff[i])
+                ti = self.ptr(self.T, self.toff[i] + (p // QB) * QB * QB)
+                descs.append((zi, vi, self.ptr(self.tau, self.tauoff[i]), ti, ni, ki, p, b))
+                m = ki - p - b
+                if m <= 0:
+                    continue
+                wi, w2 = self.ptr(self.W, self.woff[i]), self.ptr(self.W2, self.woff[i])
+                vp = vi + 8 * (p * ki + p)
+                cp = zi + 8 * (p * ki + p + b)
+                g1.append((vp, cp, wi, b, m, ni - p, ki, ki, m, 0, 1.0, 0.0))          # W = V^T C
+                g2.append((ti, wi, w2, b, m, b, QB, m, m, 0, 1.0, 0.0))                # W2 = T^T W
+                g3.append((vp, w2, cp, ni - p, m, b, ki, m, ki, 0, -1.0, 1.0))          # C -= V W2
+            prog.qr_panel(descs)
+            prog.gemm(1, 0, g1)
+            prog.gemm(1, 0, g2)
+            prog.gemm(0, 0, g3)
+        for p in reversed(panels):
+            g1, g2, g3 = [], [], []
+            for i in range(nb):
+                ni, ki = int(n[i]), int(k[i])
+                if ki <= p:
+                    continue
+                b = min(QB, ki - p)
+                m = ni - p
+                vi = self.ptr(self.V, self.zoff[i])
+                vp = vi + 8 * (p * ki + p)
+                ti = self.ptr(self.T, self.toff[i] + (p // QB) * QB * QB)
+                wi, w2 = self.ptr(self.W, self.woff[i]), self.ptr(self.W2, self.woff[i])
+                qs = self.ptr(self.Q, self.qoff[i]) + 8 * (p * ni + p)
+                g1.append((vp, qs, wi, b, m, m, ki, ni, m, 0, 1.0, 0.0))               # W = V^T Q_s
+                g2.append((ti, wi, w2, b, m, b, QB, m, m, 0, 1.0, 0.0))                # W2 = T W
+                g3.append((vp, w2, qs, m, m, b, ki, m, ni, 0, -1.0, 1.0))              # Q_s -= V W2
+            prog.gemm(1, 0, g1)
+            prog.gemm(0, 0, g2)
+            prog.gemm(0, 0, g3)
+        prog.basis([(self.ptr(self.Q, self.qoff[i]), self.ptr(self.Z, self.zoff[i]),
+                     self.ptr(self.qfull, self.qoff[i]), self.ptr(self.frame, self.foff[i]),
+                     int(n[i]), int(k[i]), int(k[i])) for i in range(nb) if k[i] > 0])
+        # k == 0: q_full = I
+        prog.copy([(0, self.ptr(self.qfull, self.qoff[i]), int(n[i]), int(n[i]), 0, int(n[i]), 3)
+                   for i in range(nb) if k[i] == 0])
+
+
+def complete_qr_host(zs, device=None):
+    """Complete QR of host matrices Z_i on the GPU; returns [(q_full, frame)]."""
+    nat.lib()
+    device = torch.device(device or "cuda")
+    n = [z.shape[0] for z in zs]
+    k = [z.shape[1] for z in zs]
+    lq = LevelQR(device, n, k)
+    host = np.concatenate([np.ascontiguousarray(z, dtype=np.float64).ravel() for z in zs] + [np.zeros(0)])
+    if host.size:
+        lq.Z[:host.size].copy_(torch.from_numpy(host))
+    prog = Program(device)
+    lq.build(prog)
+    prog.finalize().run()
+    out = []
+    qf, fr = lq.qfull.cpu().numpy(), lq.frame.cpu().numpy()
+    for i in range(len(zs)):
+        ni, ki = n[i], k[i]
+        out.append((qf[lq.qoff[i]:lq.qoff[i] + ni * ni].reshape(ni, ni).copy(),
+                    fr[lq.foff[i]:lq.foff[i] + ki * ki].reshape(ki, ki).copy()))
+    return out

@@ -1,0 +1,115 @@
+// C ABI plumbing: error reporting, the native step executor and CUDA-graph
+// capture of a whole factorization program (see include/h2ulv_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+static thread_local char g_err[512] = "";
+
+int h2g_set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int h2g_check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return H2G_OK;
+}
+
+extern "C" const char* h2g_last_error(void) { return g_err; }
+extern "C" int h2g_abi_version(void) { return H2G_ABI_VERSION; }
+
+extern "C" int h2g_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+static int run_step(const h2g_step& s, cudaStream_t st) {
+  switch (s.kind) {
+    case H2G_STEP_GEMM_NN:
+    case H2G_STEP_GEMM_NT:
+    case H2G_STEP_GEMM_TN:
+    case H2G_STEP_GEMM_TT: {
+      int k = s.kind - H2G_STEP_GEMM_NN;
+      return h2g_gemm_grouped(k >> 1, k & 1, (const h2g_gemm_problem*)s.descs, s.map, s.grid, st);
+    }
+    case H2G_STEP_PANEL:
+      return h2g_panel_potrf((const h2g_panel_desc*)s.descs, s.map, s.grid, s.npd, st);
+    case H2G_STEP_COPY:
+      return h2g_block_copy((const h2g_copy_desc*)s.descs, s.map, s.grid, st);
+    case H2G_STEP_MEMCPY: {
+      if (s.count <= 0) return H2G_OK;
+      cudaError_t e = cudaMemcpyAsync((void*)s.descs, (const void*)s.map, (size_t)s.count, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "memcpy step: %s", cudaGetErrorString(e));
+      return H2G_OK;
+    }
+    case H2G_STEP_QR_PANEL:
+      return h2g_qr_panel((const h2g_qr_panel_desc*)s.descs, s.count, st);
+    case H2G_STEP_BASIS:
+      return h2g_basis_finish((const h2g_basis_desc*)s.descs, s.count, st);
+    case H2G_STEP_GEMV:
+      return h2g_gemv_grouped((const h2g_gemv_out*)s.descs, s.count, (const h2g_gemv_term*)s.map, s.grid, st);
+    case H2G_STEP_TRSV:
+      return h2g_trsv_batched((const h2g_trsv_desc*)s.descs, s.count, s.arg, s.grid, st);
+    case H2G_STEP_KBLOCK:
+      return h2g_kernel_blocks((const h2g_kblock_desc*)s.descs, s.map, s.grid, (const double*)s.aux, s.arg,
+                               s.d0, s.d1, (int64_t*)s.npd, st);
+    default:
+      return h2g_set_error(H2G_ESTEP, "unknown step kind %d", s.kind);
+  }
+}
+
+extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream) {
+  if (nsteps < 0 || (nsteps > 0 && !steps)) return h2g_set_error(H2G_EINVAL, "h2g_run_program: bad steps");
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < nsteps; ++i) {
+    int rc = run_step(steps[i], st);
+    if (rc) {
+      char buf[400];
+      snprintf(buf, sizeof(buf), "%.380s", g_err);
+      return h2g_set_error(rc, "step %d (kind %d): %s", i, steps[i].kind, buf);
+    }
+  }
+  return H2G_OK;
+}
+
+extern "C" int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out) {
+  if (!exec_out) return h2g_set_error(H2G_EINVAL, "h2g_graph_capture: null exec_out");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "begin capture: %s", cudaGetErrorString(e));
+  int rc = h2g_run_program(steps, nsteps, stream);
+  e = cudaStreamEndCapture(st, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "end capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "instantiate: %s", cudaGetErrorString(e));
+  *exec_out = (void*)exec;
+  return H2G_OK;
+}
+
+extern "C" int h2g_graph_launch(void* exec, void* stream) {
+  if (!exec) return h2g_set_error(H2G_EINVAL, "h2g_graph_launch: null graph");
+  cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream);
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "graph launch: %s", cudaGetErrorString(e));
+  return H2G_OK;
+}
+
+extern "C" int h2g_graph_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return H2G_OK;
+}

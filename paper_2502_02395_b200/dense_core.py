@@ -1,0 +1,154 @@
+"""Host-side pieces of the dense engine: the basis container, the skeleton
+(interpolative-decomposition) selection and the reference flop model.
+
+What stays on the host and why
+  * `skeleton_selection` is the column-pivoted QR (dgeqp3) of the sample
+    matrix that chooses the skeleton rows and builds the interpolation
+    operator T (dense_core.py:114-134).  The north star requires skeleton
+    indices BIT-IDENTICAL to the reference, so it runs through the same
+    LAPACK routine on identical samples.
+  * `flop_count` / `PhaseFlops` restate the reference's flop model and its
+    pad-to-level-max accounting (dense_core.py:166-181, 229-248), so
+    `factors.flops` equals the reference's dict exactly and GFLOP/s are
+    computed with the same numerator.
+
+Everything numerical on the factorization path (the complete QR of ①,
+every GEMM, the partial Cholesky, the merge, the substitution) runs on
+the GPU through libh2ulv_b200.so.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+
+
+@dataclass
+class BasisDecomposition:
+    """Orthonormal split [q_red | q_skel] of a box's n unknowns (dense_core.py:24-48)."""
+
+    q_skel: np.ndarray
+    q_red: np.ndarray
+    skeleton: np.ndarray
+    rank: int
+    frame: np.ndarray
+
+    @property
+    def n(self):
+        return self.q_skel.shape[0]
+
+    @property
+    def q_full(self):
+        return np.hstack([self.q_red, self.q_skel])
+
+
+@dataclass
+class SkeletonChoice:
+    """Result of the pivoted-QR half of id_basis for one box."""
+
+    skeleton: np.ndarray  # sorted box-local row ids (int64)
+    t: np.ndarray         # n x k interpolation operator, columns follow `skeleton`
+    rank: int
+
+
+def skeleton_selection(samples, rank=None, tol=None):
+    """Column-pivoted QR of samples^T -> (skeleton, T, k).
+
+    k = rank (capped by the shape) or the first index whose pivot ratio
+    |r_kk / r_00| <= tol; exactly-zero pivots are never kept
+    (dense_core.py:114-123).  T[skeleton] = I and the other rows are
+    (R11^-1 R12)^T (dense_core.py:125-134).
+    """
+    if (rank is None) == (tol is None):
+        raise ValueError("exactly one of rank/tol must be given")
+    a = np.asarray(samples, dtype=np.float64)
+    n, m = a.shape
+    if m < 1:
+        raise ValueError("need at least one sample column")
+    _, r, piv = scipy.linalg.qr(a.T, pivoting=True, mode="economic")
+    diag = np.abs(np.diag(r))
+    if diag.size == 0 or diag[0] == 0.0:
+        k = 0
+    elif rank is not None:
+        k = min(rank, n, m)
+    else:
+        below = np.flatnonzero(diag / diag[0] <= tol)
+        k = int(below[0]) if below.size else min(n, m)
+    k = min(k, int(np.count_nonzero(diag > 0)))
+    if k == 0:
+        return SkeletonChoice(skeleton=np.zeros(0, dtype=np.int64), t=np.zeros((n, 0)), rank=0)
+    lead = piv[:k]
+    order = np.argsort(lead)
+    t = np.zeros((n, k))
+    t[lead] = np.eye(k)
+    if n > k:
+        t[piv[k:]] = scipy.linalg.solve_triangular(r[:k, :k], r[:k, k:], lower=False).T
+    return SkeletonChoice(skeleton=lead[order].astype(np.int64), t=t[:, order], rank=k)
+
+
+def id_basis(samples, rank=None, tol=None, row_weight=None):
+    """Drop-in for the reference `id_basis` (dense_core.py:96-150).
+
+    Skeleton selection on the host (bit-exact), complementary basis (①) by
+    the batched GPU Householder QR.
+    """
+    from . import basis_qr
+
+    choice = skeleton_selection(samples, rank=rank, tol=tol)
+    n = np.asarray(samples).shape[0]
+    if choice.rank == 0:
+        return BasisDecomposition(q_skel=np.zeros((n, 0)), q_red=np.eye(n), skeleton=choice.skeleton,
+                                  rank=0, frame=np.zeros((0, 0)))
+    z = choice.t if row_weight is None else np.asarray(row_weight, dtype=np.float64) @ choice.t
+    qfull, frame = basis_qr.complete_qr_host([z])[0]
+    k = choice.rank
+    return BasisDecomposition(q_skel=qfull[:, n - k:], q_red=qfull[:, :n - k], skeleton=choice.skeleton,
+                              rank=k, frame=frame)
+
+
+# --------------------------------------------------------------------------- flop model
+
+def flop_count(kind, dims):
+    """Leading-order flops (dense_core.py:166-181): cholesky n^3/3,
+    tri_solve n^2 m, multiply 2 m n k."""
+    if kind == "cholesky":
+        return dims[0] ** 3 // 3
+    if kind == "tri_solve":
+        return dims[0] * dims[0] * dims[1]
+    if kind == "multiply":
+        return 2 * dims[0] * dims[1] * dims[2]
+    if kind == "diag_fill":
+        return 0
+    raise ValueError(f"unknown op kind '{kind}'")
+
+
+def _pad4(x):
+    return 0 if x <= 0 else max(4, -(-x // 4) * 4)
+
+
+class PhaseFlops:
+    """The reference's per-(level, phase) record: true flops, flops of the
+    dims padded to the per-kind maximum rounded to 4, and the op count
+    (plan_batches + _record, dense_core.py:229-248, ulv_factor.py:135-142)."""
+
+    def __init__(self):
+        self.flops = {"levels": {}, "total_true": 0, "total_padded": 0}
+
+    def record(self, level, phase, ops):
+        """ops: list of (kind, dims) in the order the reference issues them."""
+        by_kind = {}
+        for kind, dims in ops:
+            by_kind.setdefault(kind, []).append(tuple(int(d) for d in dims))
+        true = padded = 0
+        for kind, dl in by_kind.items():
+            width = len(dl[0])
+            mx = tuple(_pad4(max(d[a] for d in dl)) for a in range(width))
+            true += sum(flop_count(kind, d) for d in dl)
+            padded += flop_count(kind, mx) * len(dl)
+        ent = self.flops["levels"].setdefault(level, {}).setdefault(
+            phase, {"true": 0, "padded": 0, "count": 0})
+        ent["true"] += true
+        ent["padded"] += padded
+        ent["count"] += len(ops)
+        self.flops["total_true"] += true
+        self.flops["total_padded"] += padded

@@ -1,0 +1,238 @@
+"""Static GPU programs: lists of batched steps plus their descriptors.
+
+A factorization (or a basis construction) is known in full from the box
+dimensions before any arithmetic runs, so the host builds every descriptor
+once, ships all of them to the device in ONE copy, and the native
+executor (h2g_run_program) issues the steps back to back — optionally as
+a single CUDA graph replay.  This replaces the reference's per-op Python
+planner/executor (dense_core.plan_batches / run_plan, dense_core.py:229-284).
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+
+def gemm_tiles(m, n, flags=0):
+    if m <= 0 or n <= 0:
+        return 0
+    if flags & nat.GEMM_LOWER:
+        t = -(-m // nat.GEMM_TILE)
+        return t * (t + 1) // 2
+    return (-(-m // nat.GEMM_TILE)) * (-(-n // nat.GEMM_TILE))
+
+
+def copy_tiles(rows, cols):
+    if rows <= 0 or cols <= 0:
+        return 0
+    return (-(-rows // nat.COPY_TILE)) * (-(-cols // nat.COPY_TILE))
+
+
+class Program:
+    """Accumulates steps; `finalize()` uploads descriptors and resolves pointers."""
+
+    def __init__(self, device):
+        self.device = device
+        self._blobs = []      # numpy byte arrays (descriptors and maps)
+        self._steps = []      # dicts: kind, count, grid, arg, descs, map, npd, aux, d0, d1
+        self.dev_blob = None
+        self.steps = None
+        self.graph = None
+        self.kernel_launches = 0
+
+    # -- blob bookkeeping -------------------------------------------------------------
+    def _blob(self, arr):
+        if arr is None:
+            return -1
+        self._blobs.append(np.ascontiguousarray(arr).view(np.uint8).reshape(-1))
+        return len(self._blobs) - 1
+
+    def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0):
+        self._steps.append(dict(kind=kind, count=int(count), grid=int(grid), descs=descs, map=map_, npd=npd,
+                                arg=int(arg), aux=aux, d0=float(d0), d1=float(d1)))
+
+    # -- step constructors ------------------------------------------------------------
+    def gemm(self, trans_a, trans_b, problems):
+        """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta)."""
+        rows = [p for p in problems if p[3] > 0 and p[4] > 0]
+        if not rows:
+            return 0
+        arr = np.zeros(len(rows), dtype=nat.GEMM_DT)
+        cols = list(zip(*rows))
+        for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
+            arr[name] = col
+        tiles = np.array([gemm_tiles(m, n, f) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])], dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        arr["tile_start"] = starts
+        total = int(tiles.sum())
+        tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
+        # K == 0 problems still need their beta*C epilogue; keep them (tiles > 0)
+        kind = nat.STEP["GEMM_NN"] + 2 * int(bool(trans_a)) + int(bool(trans_b))
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap))
+        return total
+
+    def panel(self, descs, npd_ptr):
+        """descs: list of (H, R, ldh, ldr, n, nr, p, b, npd_slot, rows_per_cta)."""
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.PANEL_DT)
+        cols = list(zip(*descs))
+        for name, col in zip(("H", "R", "ldh", "ldr", "n", "nr", "p", "b", "npd_slot", "rows_per_cta"), cols):
+            arr[name] = col
+        rows_total = (arr["n"] - arr["p"] - arr["b"]).astype(np.int64) + arr["nr"]
+        ctas = np.maximum(1, -(-rows_total // arr["rows_per_cta"]))
+        arr["cta_start"] = np.concatenate([[0], np.cumsum(ctas)[:-1]])
+        cmap = np.repeat(np.arange(len(descs), dtype=np.int32), ctas)
+        self._add(nat.STEP["PANEL"], len(descs), int(ctas.sum()), self._blob(arr), self._blob(cmap), npd=npd_ptr)
+        return int(ctas.sum())
+
+    def copy(self, descs):
+        """descs: list of (src, dst, rows, cols, lds, ldd, mode)."""
+        rows = [d for d in descs if d[2] > 0 and d[3] > 0]
+        if not rows:
+            return 0
+        arr = np.zeros(len(rows), dtype=nat.COPY_DT)
+        cols = list(zip(*rows))
+        for name, col in zip(("src", "dst", "rows", "cols", "lds", "ldd", "mode"), cols):
+            arr[name] = col
+        tiles = np.array([copy_tiles(r, c) for r, c in zip(arr["rows"], arr["cols"])], dtype=np.int64)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
+        self._add(nat.STEP["COPY"], len(rows), int(tiles.sum()), self._blob(arr), self._blob(tmap))
+        return int(tiles.sum())
+
+    def memcpy(self, dst_ptr, src_ptr, nbytes):
+        if nbytes > 0:
+            self._add(nat.STEP["MEMCPY"], int(nbytes), 0, ("raw", dst_ptr), ("raw", src_ptr))
+
+    def qr_panel(self, descs):
+        """descs: list of (Z, V, tau, T, n, ldz, p, b)."""
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.QRP_DT)
+        for name, col in zip(("Z", "V", "tau", "T", "n", "ldz", "p", "b"), zip(*descs)):
+            arr[name] = col
+        self._add(nat.STEP["QR_PANEL"], len(descs), len(descs), self._blob(arr))
+        return len(descs)
+
+    def basis(self, descs):
+        """descs: list of (Q, Z, qfull, frame, n, k, ldz)."""
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.BASIS_DT)
+        for name, col in zip(("Q", "Z", "qfull", "frame", "n", "k", "ldz"), zip(*descs)):
+            arr[name] = col
+        self._add(nat.STEP["BASIS"], len(descs), len(descs), self._blob(arr))
+        return len(descs)
+
+    def gemv(self, outs, w):
+        """outs: list of (y, y2, init, m, split, flags, [terms...]) with terms (A, x, lda, trans, K)."""
+        outs = [o for o in outs if o[3] > 0]
+        if not outs:
+            return 0
+        oarr = np.zeros(len(outs), dtype=nat.GEMV_OUT_DT)
+        tl = []
+        for q, (y, y2, init, m, split, flags, tms) in enumerate(outs):
+            oarr[q] = (y, y2, init, m, split, len(tl), len(tl) + len(tms), flags, 0)
+            tl.extend(tms)
+        tarr = np.zeros(max(len(tl), 1), dtype=nat.GEMV_TERM_DT)
+        for q, (a, x, lda, trans, k) in enumerate(tl):
+            tarr[q] = (a, x, lda, trans, k, 0)
+        self._add(nat.STEP["GEMV"], len(outs), w, self._blob(oarr), self._blob(tarr))
+        return len(outs)
+
+    def trsv(self, descs, trans, w):
+        """descs: list of (L, x, n, ldl)."""
+        descs = [d for d in descs if d[2] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.TRSV_DT)
+        for q, d in enumerate(descs):
+            arr[q] = d
+        self._add(nat.STEP["TRSV"], len(descs), w, self._blob(arr), arg=trans)
+        return len(descs)
+
+    def kblock(self, descs, points_ptr, family, shift, decay, flag_ptr):
+        """descs: list of (rows_ptr, cols_ptr, out_ptr, m, n, ldo)."""
+        descs = [d for d in descs if d[3] > 0 and d[4] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.KBLOCK_DT)
+        for name, col in zip(("rows", "cols", "out", "m", "n", "ldo"), zip(*descs)):
+            arr[name] = col
+        tiles = (-(-arr["m"].astype(np.int64) // 32)) * (-(-arr["n"].astype(np.int64) // 32))
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        self._add(nat.STEP["KBLOCK"], len(descs), int(tiles.sum()), self._blob(arr), self._blob(tmap),
+                  npd=flag_ptr, arg=family, aux=points_ptr, d0=shift, d1=decay)
+        return int(tiles.sum())
+
+    # -- finalize / run ---------------------------------------------------------------
+    def finalize(self):
+        offs, total = [], 0
+        for b in self._blobs:
+            offs.append(total)
+            total += (b.size + 255) // 256 * 256
+        host = torch.zeros(max(total, 256), dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for o, b in zip(offs, self._blobs):
+            hv[o:o + b.size] = b
+        self.dev_blob = host.to(self.device, non_blocking=True)
+        self._host_blob = host  # keep pinned source alive until the copy completes
+        base = self.dev_blob.data_ptr()
+        steps = np.zeros(len(self._steps), dtype=nat.STEP_DT)
+
+        def resolve(v):
+            if isinstance(v, tuple):
+                return v[1]
+            return base + offs[v] if v >= 0 else 0
+
+        for q, st in enumerate(self._steps):
+            steps[q]["kind"] = st["kind"]
+            steps[q]["count"] = st["count"]
+            steps[q]["grid"] = st["grid"]
+            steps[q]["arg"] = st["arg"]
+            steps[q]["descs"] = resolve(st["descs"])
+            steps[q]["map"] = resolve(st["map"])
+            steps[q]["npd"] = st["npd"]
+            steps[q]["aux"] = st["aux"]
+            steps[q]["d0"] = st["d0"]
+            steps[q]["d1"] = st["d1"]
+        self.steps = steps
+        self.kernel_launches = int(sum(1 for st in self._steps if st["kind"] != nat.STEP["MEMCPY"]))
+        self.step_kinds = [st["kind"] for st in self._steps]
+        self._blobs = []
+        return self
+
+    def run(self, stream=None):
+        lib = nat.lib()
+        rc = lib.h2g_run_program(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps), nat.stream_ptr(stream))
+        nat.check(rc, "h2g_run_program")
+
+    def capture(self, stream=None):
+        """Capture the whole program into one CUDA graph (on a side stream)."""
+        lib = nat.lib()
+        s = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        torch.cuda.current_stream(self.device).synchronize()
+        exe = ctypes.c_void_p()
+        rc = lib.h2g_graph_capture(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps),
+                                   nat.stream_ptr(s), ctypes.byref(exe))
+        nat.check(rc, "h2g_graph_capture")
+        self.graph = exe
+        return self
+
+    def launch(self, stream=None):
+        if self.graph is None:
+            return self.run(stream)
+        rc = nat.lib().h2g_graph_launch(self.graph, nat.stream_ptr(stream))
+        nat.check(rc, "h2g_graph_launch")
+
+    def __del__(self):
+        if getattr(self, "graph", None) is not None:
+            try:
+                nat.load_library().h2g_graph_destroy(self.graph)
+            except Exception:
+                pass

@@ -1,0 +1,407 @@
+"""H²-ULV factorization on the GPU — drop-in for `h2ulv.ulv_factor`.
+
+`factorize(h2, batched=True, retain=False) -> ULVFactors` keeps the
+reference signature and output contract (ulv_factor.py:154-316): per level
+`lr_diag[i]`, `lr_off[(i, j)]`, `ls[(a, b)]`, `v[i]`, `dims[i]`, the root
+factor, `merge_map`, the flop report and the write audit.  The blocks stay
+in HBM; the numpy views materialize lazily on first access.
+
+Per level l (fine to coarse) the whole level is a handful of batched launches
+(one `Program`, optionally one CUDA graph for the entire factorization):
+
+  R <- Q (device copy)                       q_full kept for the solve
+  GEMM NN   M_i = A_ii Q_i                   diag_mul1 (ulv_factor.py:189-194)
+  GEMM TN   H_i = Q_i^T M_i                  diag_mul2 (195-200)
+  for p in 0, 64, ...:                       partial Cholesky of H_i (217-241):
+    PANEL   chol(H[p:p+b,p:p+b]); rows below and R rows <- X L^-T
+    GEMM NT trailing update (lower tiles of H, and R[:, p+b:r])
+            -> H = [[L(r)], [L(s)_ii, SS_ii - L(s) L(s)^T]],  R = [V_i | q_skel_i]
+  GEMM NN   MO_ij = A_ij [V_j | q_skel_j]    off_mul1 (243-253)
+  GEMM TN   T_ij  = Q_i^T MO_ij              off_mul2 (254-259)
+            L(s)_ji = (A_ij q_skel_j)^T V_i  = (L(r)_ii^-1 RS_ij)^T  off_mirror (282-286)
+  COPY      parent near blocks <- 2x2 child SS / couplings           merge (289-303)
+root: the same PANEL/GEMM loop on the merged d x d block (309-314).
+
+`batched` is accepted for signature compatibility: there is only the batched
+GPU path, and it is deterministic (no atomics in any reduction), so repeated
+runs are bitwise identical — the property test_ulv_factor.py:227-241 checks.
+"""
+
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .dense_core import PhaseFlops
+from .errors import NotPositiveDefiniteError, StructureError
+from .h2_device import DeviceH2
+from .program import Program
+
+INT_MAX = 2 ** 31 - 1
+F64 = torch.float64
+PANEL_ROWS_PER_CTA = 128
+
+
+class _LazyBlocks(Mapping):
+    """Read-only dict whose values are downloaded from HBM on first access."""
+
+    def __init__(self, keys, fetch):
+        self._keys = list(keys)
+        self._set = set(self._keys)
+        self._fetch = fetch
+        self._cache = {}
+
+    def __getitem__(self, key):
+        if key not in self._set:
+            raise KeyError(key)
+        if key not in self._cache:
+            self._cache[key] = self._fetch(key)
+        return self._cache[key]
+
+    def __iter__(self):
+        return iter(self._keys)
+
+    def __len__(self):
+        return len(self._keys)
+
+
+@dataclass
+class ULVLevel:
+    lr_diag: Mapping = field(default_factory=dict)
+    lr_off: Mapping = field(default_factory=dict)
+    ls: Mapping = field(default_factory=dict)
+    v: Mapping = field(default_factory=dict)
+    dims: dict = field(default_factory=dict)
+
+
+class ULVFactors:
+    """Factor container with the reference's attributes (ulv_factor.py:34-47)."""
+
+    def __init__(self, h2, plan):
+        self.h2 = h2
+        self._plan = plan
+        self.levels = {}
+        self.merge_map = {}
+        self.flops = plan.flops
+        self.audit = plan.audit
+        self.retained = None
+        self._root = None
+
+    @property
+    def depth(self):
+        return self._plan.depth
+
+    @property
+    def root(self):
+        if self._root is None:
+            self._root = self._plan.download_root()
+        return self._root
+
+    @property
+    def device(self):
+        return self._plan
+
+
+def _mat(t, off, rows, cols, ld, r0=0, c0=0):
+    """Strided view of a row-major block inside flat tensor `t`, as numpy."""
+    if rows == 0 or cols == 0:
+        return np.zeros((rows, cols))
+    base = off + r0 * ld + c0
+    v = t[base: base + (rows - 1) * ld + cols].as_strided((rows, cols), (ld, 1))
+    return v.cpu().numpy().copy()
+
+
+class _LevelBuffers:
+    pass
+
+
+class FactorPlan:
+    """Device buffers + the static step program of one factorization."""
+
+    def __init__(self, dh2: DeviceH2, lists):
+        self.dh2 = dh2
+        self.depth = dh2.depth
+        dev = dh2.device
+        self.device = dev
+        prog = Program(dev)
+        depth = self.depth
+        # pivot status: one slot per box of every level plus the root
+        self.slot_base = {}
+        acc = 0
+        for l in range(depth, 0, -1):
+            self.slot_base[l] = acc
+            acc += 2 ** l
+        self.slot_base[0] = acc
+        self.npd = torch.full((acc + 1,), INT_MAX, dtype=torch.int32, device=dev)
+        self._npd_init = torch.full((acc + 1,), INT_MAX, dtype=torch.int32, device=dev)
+        prog.memcpy(self.npd.data_ptr(), self._npd_init.data_ptr(), 4 * (acc + 1))
+        self.bufs = {}
+        self.merge_pairs = {}
+
+        if depth == 0:
+            d = int(dh2.root_a.shape[0])
+            self.root_buf = torch.empty(d * d, dtype=F64, device=dev)
+            self.root_dim = d
+            prog.memcpy(self.root_buf.data_ptr(), dh2.root_a.data_ptr(), 8 * d * d)
+            self._cholesky_steps(prog, self.root_buf.data_ptr(), d, d, self.slot_base[0])
+        else:
+            a_buf, a_off = dh2.leaf_a, dh2.aoff
+            for l in range(depth, 0, -1):
+                lay = dh2.levels[l]
+                B = _LevelBuffers()
+                self.bufs[l] = B
+                B.lay = lay
+                n, k, r = lay.n, lay.k, lay.r
+                qsz = max(lay.qsize, 1)
+                B.M = torch.empty(qsz, dtype=F64, device=dev)
+                B.H = torch.empty(qsz, dtype=F64, device=dev)
+                B.R = torch.empty(qsz, dtype=F64, device=dev)
+                B.a, B.aoff = a_buf, a_off
+                qp, Hp, Rp, Mp = dh2.q[l].data_ptr(), B.H.data_ptr(), B.R.data_ptr(), B.M.data_ptr()
+                ap = a_buf.data_ptr()
+                qo = lay.qoff
+                for (i, j) in lay.near_pairs:
+                    if (i, j) not in a_off:
+                        raise StructureError(f"missing near block ({l}, {i}, {j})")
+                nb = lay.nb
+                # ---- diagonal phase
+                prog.memcpy(Rp, qp, 8 * lay.qsize)
+                prob = []
+                for i in range(nb):
+                    ni = int(n[i])
+                    prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
+                                 0, 1.0, 0.0))
+                prog.gemm(0, 0, prob)
+                prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
+                         int(n[i]), int(n[i]), int(n[i]), 0, 1.0, 0.0) for i in range(nb)]
+                prog.gemm(1, 0, prob)
+                self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l])
+                # ---- off-diagonal phase
+                offp = lay.off_pairs
+                B.toff, B.lsoff = {}, {}
+                tacc = lacc = 0
+                for (i, j) in offp:
+                    B.toff[(i, j)] = tacc
+                    tacc += int(n[i] * n[j])
+                    B.lsoff[(i, j)] = lacc
+                    lacc += int(k[j] * r[i])
+                B.MO = torch.empty(max(tacc, 1), dtype=F64, device=dev)
+                B.T = torch.empty(max(tacc, 1), dtype=F64, device=dev)
+                B.LSm = torch.empty(max(lacc, 1), dtype=F64, device=dev)
+                MOp, Tp, LSp = B.MO.data_ptr(), B.T.data_ptr(), B.LSm.data_ptr()
+                prob = []
+                for (i, j) in offp:
+                    ni, nj = int(n[i]), int(n[j])
+                    prob.append((ap + 8 * a_off[(i, j)], Rp + 8 * qo[j], MOp + 8 * B.toff[(i, j)], ni, nj, nj,
+                                 nj, nj, nj, 0, 1.0, 0.0))
+                prog.gemm(0, 0, prob)
+                prob = []
+                for (i, j) in offp:
+                    ni, nj, ri, rj, kj = int(n[i]), int(n[j]), int(r[i]), int(r[j]), int(k[j])
+                    mo = MOp + 8 * B.toff[(i, j)]
+                    prob.append((qp + 8 * qo[i], mo, Tp + 8 * B.toff[(i, j)], ni, nj, ni, ni, nj, nj, 0, 1.0, 0.0))
+                    # mirror: L(s)_ji = (A_ij q_skel_j)^T V_i   (k_j x r_i)
+                    prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
+                                 0, 1.0, 0.0))
+                prog.gemm(1, 0, prob)
+                # ---- merge into the parent level (or the root)
+                a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2)
+            d = self._root_d
+            self.root_dim = d
+            self.root_buf = a_buf
+            self._cholesky_steps(prog, a_buf.data_ptr(), d, d, self.slot_base[0])
+
+        self.flops = flop_report({l: (B.lay.n, B.lay.k, B.lay.off_pairs) for l, B in self.bufs.items()},
+                                 self.root_dim)
+        self.audit = self._audit()
+        self.program = prog.finalize()
+
+    # ------------------------------------------------------------------ steps
+    def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0):
+        nb = len(n)
+        rmax = int(r.max()) if nb else 0
+        for p in range(0, rmax, nat.PANEL_WIDTH):
+            descs, prob = [], []
+            for i in range(nb):
+                ri, ni = int(r[i]), int(n[i])
+                if ri <= p:
+                    continue
+                b = min(nat.PANEL_WIDTH, ri - p)
+                h = Hp + 8 * int(qo[i])
+                rr = Rp + 8 * int(qo[i]) if Rp else 0
+                descs.append((h, rr, ni, ni, ni, ni if Rp else 0, p, b, slot0 + i, PANEL_ROWS_PER_CTA))
+                m = ni - p - b
+                pan = h + 8 * ((p + b) * ni + p)
+                if m > 0:
+                    prob.append((pan, pan, h + 8 * ((p + b) * ni + p + b), m, m, b, ni, ni, ni,
+                                 nat.GEMM_LOWER, -1.0, 1.0))
+                if Rp and ri - p - b > 0:
+                    prob.append((rr + 8 * p, pan, rr + 8 * (p + b), ni, ri - p - b, b, ni, ni, ni, 0, -1.0, 1.0))
+            prog.panel(descs, self.npd.data_ptr())
+            prog.gemm(0, 1, prob)
+
+    def _cholesky_steps(self, prog, ptr, d, ld, slot):
+        assert d == ld
+        self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]), np.array([d]), slot)
+
+    def _merge_steps(self, prog, l, B, lists, dh2):
+        lay = B.lay
+        n, k, r = lay.n, lay.k, lay.r
+        parents = sorted((pi, pj) for (pi, pj) in lists.near[l - 1] if pi >= pj)
+        self.merge_pairs[l] = parents
+        pn = {p: int(k[2 * p] + k[2 * p + 1]) for p in range(2 ** (l - 1))}
+        aoff, acc = {}, 0
+        for (pi, pj) in parents:
+            aoff[(pi, pj)] = acc
+            acc += pn[pi] * pn[pj]
+        abuf = torch.empty(max(acc, 1), dtype=F64, device=self.device)
+        if l == 1:
+            self._root_d = pn[0]
+        Hp, Tp, Sp = B.H.data_ptr(), B.T.data_ptr(), dh2.s[l].data_ptr()
+        qo = lay.qoff
+        descs = []
+        for (pi, pj) in parents:
+            dst0 = abuf.data_ptr() + 8 * aoff[(pi, pj)]
+            ldd = pn[pj]
+            for a in (0, 1):
+                ci = 2 * pi + a
+                ro = 0 if a == 0 else int(k[2 * pi])
+                for b in (0, 1):
+                    cj = 2 * pj + b
+                    co = 0 if b == 0 else int(k[2 * pj])
+                    dst = dst0 + 8 * (ro * ldd + co)
+                    kci, kcj = int(k[ci]), int(k[cj])
+                    if ci == cj:
+                        src = Hp + 8 * int(qo[ci] + r[ci] * n[ci] + r[ci])
+                        descs.append((src, dst, kci, kcj, int(n[ci]), ldd, 2))
+                        continue
+                    hi, lo = (ci, cj) if ci > cj else (cj, ci)
+                    mode = 0 if ci > cj else 1
+                    if (hi, lo) in B.toff:
+                        src = Tp + 8 * int(B.toff[(hi, lo)] + r[hi] * n[lo] + r[lo])
+                        lds = int(n[lo])
+                    elif (hi, lo) in lay.soff:
+                        src = Sp + 8 * int(lay.soff[(hi, lo)])
+                        lds = int(k[lo])
+                    else:
+                        raise StructureError(f"missing child SS block ({l}, {ci}, {cj})")
+                    descs.append((src, dst, kci, kcj, lds, ldd, mode))
+        prog.copy(descs)
+        return abuf, aoff
+
+    def _audit(self):
+        """Write audit of the reference's slab store (ulv_factor.py:319-337),
+        derived from the program: off-diagonal SS blocks (T) and the RR/RS/SR
+        slabs are written once by their producing GEMM and never updated; the
+        diagonal SS receives its single Schur update (split into one trailing
+        GEMM per Cholesky panel on the GPU)."""
+        boxes = sum(2 ** l for l in range(1, self.depth + 1))
+        panels = []
+        for l, B in self.bufs.items():
+            panels.extend(int(-(-ri // nat.PANEL_WIDTH)) for ri in B.lay.r)
+        return {"offdiag_ss_post_init_writes": 0, "rr_rs_sr_post_init_writes": 0,
+                "diag_ss_update_counts": [1] if boxes else [], "diag_ss_blocks": boxes,
+                "diag_ss_panel_updates": sorted(set(panels))}
+
+    # ------------------------------------------------------------------ run / check
+    def run(self, stream=None):
+        self.program.launch(stream)
+
+    def check_pivots(self):
+        npd = self.npd.cpu().numpy()
+        if (npd == INT_MAX).all():
+            return
+        for l in list(range(self.depth, 0, -1)) + [0]:
+            base = self.slot_base[l]
+            cnt = 2 ** l if l > 0 else 1
+            seg = npd[base:base + cnt]
+            bad = np.flatnonzero(seg != INT_MAX)
+            if bad.size:
+                box = int(bad[0])
+                raise NotPositiveDefiniteError(int(seg[box]), level=l, box=box)
+
+    # ------------------------------------------------------------------ views
+    def download_root(self):
+        d = self.root_dim
+        return np.tril(_mat(self.root_buf, 0, d, d, d))
+
+    def level_views(self, l):
+        B = self.bufs[l]
+        lay = B.lay
+        n, k, r, qo = lay.n, lay.k, lay.r, lay.qoff
+        nb = lay.nb
+        lvl = ULVLevel()
+        lvl.dims = {i: (int(r[i]), int(k[i])) for i in range(nb)}
+        lvl.lr_diag = _LazyBlocks(range(nb), lambda i: np.tril(_mat(B.H, int(qo[i]), int(r[i]), int(r[i]), int(n[i]))))
+        lvl.v = _LazyBlocks(range(nb), lambda i: _mat(B.R, int(qo[i]), int(n[i]), int(r[i]), int(n[i])))
+        lvl.lr_off = _LazyBlocks(lay.off_pairs, lambda p: _mat(B.T, B.toff[p], int(r[p[0]]), int(r[p[1]]),
+                                                               int(n[p[1]])))
+
+        def ls_fetch(key):
+            a, b = key
+            if a == b:
+                return _mat(B.H, int(qo[a]), int(k[a]), int(r[a]), int(n[a]), r0=int(r[a]))
+            if a > b:
+                return _mat(B.T, B.toff[(a, b)], int(k[a]), int(r[b]), int(n[b]), r0=int(r[a]))
+            return _mat(B.LSm, B.lsoff[(b, a)], int(k[a]), int(r[b]), int(r[b]))
+
+        keys = [(i, i) for i in range(nb)] + list(lay.off_pairs) + [(j, i) for (i, j) in lay.off_pairs]
+        lvl.ls = _LazyBlocks(keys, ls_fetch)
+        return lvl
+
+
+def flop_report(levels, root_dim):
+    """The reference's flop dict from box dimensions alone.
+
+    levels: {l: (n array, k array, sorted near pairs i > j)}.  Phases and op
+    order as issued by ulv_factor.factorize (ulv_factor.py:189-313); padded
+    counts follow plan_batches (dense_core.py:229-248).
+    """
+    fl = PhaseFlops()
+    for l in sorted(levels, reverse=True):
+        n, k, offp = levels[l]
+        r = np.asarray(n) - np.asarray(k)
+        nb = len(n)
+        fl.record(l, "diag_mul1", [("multiply", (n[i], n[i], n[i])) for i in range(nb)])
+        fl.record(l, "diag_mul2", [("multiply", (n[i], n[i], n[i])) for i in range(nb)])
+        fl.record(l, "diag_chol", [("cholesky", (r[i],)) for i in range(nb)])
+        fl.record(l, "diag_trsm", [op for i in range(nb)
+                                   for op in (("tri_solve", (r[i], k[i])), ("tri_solve", (r[i], n[i])))])
+        fl.record(l, "diag_schur", [("multiply", (k[i], k[i], r[i])) for i in range(nb)])
+        fl.record(l, "off_mul1", [("multiply", (n[i], n[j], n[j])) for (i, j) in offp])
+        fl.record(l, "off_mul2", [("multiply", (n[i], n[j], n[i])) for (i, j) in offp])
+        fl.record(l, "off_mirror", [("tri_solve", (r[i], k[j])) for (i, j) in offp])
+    fl.record(0, "root", [("cholesky", (root_dim,))])
+    return fl.flops
+
+
+def factorize(h2, batched=True, retain=False):
+    """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
+    if retain:
+        raise NotImplementedError("retain=True (pre-factorization slab copies) is not supported on the GPU path yet")
+    nat.lib()
+    dh2 = h2_device_of(h2)
+    plan = FactorPlan(dh2, h2.lists)
+    plan.run()
+    plan.check_pivots()
+    return factors_from_plan(h2, plan)
+
+
+def factors_from_plan(h2, plan):
+    f = ULVFactors(h2, plan)
+    for l in range(plan.depth, 0, -1):
+        f.levels[l] = plan.level_views(l)
+    for l, parents in plan.merge_pairs.items():
+        f.merge_map[l] = {(pi, pj): [(2 * pi + a, 2 * pj + b) for a in (0, 1) for b in (0, 1)]
+                          for (pi, pj) in parents}
+    return f
+
+
+def h2_device_of(h2):
+    """The DeviceH2 of `h2`: the cached one (GPU construct) or a fresh upload."""
+    dh2 = getattr(h2, "_device", None)
+    if dh2 is None:
+        dh2 = DeviceH2.from_host(h2)
+    return dh2

@@ -1,0 +1,358 @@
+"""Forward/backward substitution through the GPU ULV factors — drop-in for
+`h2ulv.ulv_solve` (ulv_solve.py:1-207).
+
+`solve(factors, b, mode="parallel")` permutes b into tree order, runs the
+forward sweep (levels fine -> coarse, then the root) and the backward sweep
+(root, then coarse -> fine) and permutes back.  The "parallel" form
+(ulv_solve.py:98-109, 166-176) is what runs: every phase of a level is one
+batched launch over all boxes, so a level costs 5 launches forward and 5
+backward independent of the box count.  "naive" (the sequential Algorithm 3
+of the reference) is executed box by box with the same kernels.
+
+Vectors live in HBM in split layout per level: all redundant segments
+(y_R) back to back, all skeleton segments (b_S) back to back.  The skeleton
+segments of level l, concatenated in box order, are exactly the input
+segments of level l-1 (n_p = k_2p + k_2p+1), so the merge
+`segs[p] = vstack(b_S,2p, b_S,2p+1)` (ulv_solve.py:113) costs nothing.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .program import Program
+
+F64 = torch.float64
+
+
+@dataclass
+class BlockVector:
+    """Per-level redundant segments plus the root segment (ulv_solve.py:18-25)."""
+
+    yr: dict = field(default_factory=dict)
+    root: np.ndarray = None
+    width: int = 1
+    vector: bool = True
+    _plan: object = None
+
+
+def _near_sets(lay):
+    nb = lay.nb
+    below = [[] for _ in range(nb)]
+    above = [[] for _ in range(nb)]
+    for (i, j) in lay.off_pairs:
+        below[i].append(j)
+        above[j].append(i)
+    return [sorted(x) for x in below], [sorted(x) for x in above]
+
+
+class SolvePlan:
+    """Device vectors and the forward / backward programs for RHS width w."""
+
+    def __init__(self, fplan, w, mode="parallel"):
+        self.fp = fplan
+        self.w = w
+        self.mode = mode
+        dev = fplan.device
+        self.device = dev
+        depth = fplan.depth
+        dh2 = fplan.dh2
+        self.count = dh2.count
+        z = lambda m: torch.zeros(max(int(m), 1) * w, dtype=F64, device=dev)
+        self.xin = z(self.count)
+        d = fplan.root_dim
+        self.yroot, self.xroot = z(d), z(d)
+        self.v = {}
+        for l in range(depth, 0, -1):
+            lay = fplan.bufs[l].lay
+            sr, sk, sn = int(lay.r.sum()), int(lay.k.sum()), int(lay.n.sum())
+            self.v[l] = dict(BR=z(sr), BS=z(sk), Z=z(sr), Y=z(sr), YB=z(sr), Z2=z(sr), XR=z(sr), FULL=z(sn),
+                             offR=np.concatenate([[0], np.cumsum(lay.r)[:-1]]).astype(np.int64),
+                             offS=np.concatenate([[0], np.cumsum(lay.k)[:-1]]).astype(np.int64),
+                             offX=np.concatenate([[0], np.cumsum(lay.n)[:-1]]).astype(np.int64))
+        self.fwd = self._build_forward().finalize()
+        self.bwd = self._build_backward().finalize()
+        self.output = self.v[depth]["FULL"] if depth >= 1 else self.xroot
+
+    # -------------------------------------------------------------- pointers
+    def _p(self, t, off_rows=0):
+        return t.data_ptr() + 8 * int(off_rows) * self.w
+
+    def _ls(self, l, a, b):
+        """(pointer, ld) of L(s)_ab at level l."""
+        B = self.fp.bufs[l]
+        lay = B.lay
+        n, r = lay.n, lay.r
+        if a == b:
+            return B.H.data_ptr() + 8 * int(lay.qoff[a] + r[a] * n[a]), int(n[a])
+        if a > b:
+            return B.T.data_ptr() + 8 * int(B.toff[(a, b)] + r[a] * n[b]), int(n[b])
+        return B.LSm.data_ptr() + 8 * int(B.lsoff[(b, a)]), int(r[b])
+
+    def _ls_keys(self, lay):
+        keys = [(i, i) for i in range(lay.nb)] + list(lay.off_pairs) + [(j, i) for (i, j) in lay.off_pairs]
+        return [(a, b) for (a, b) in keys if lay.k[a] > 0 and lay.r[b] > 0]
+
+    def _L(self, l, i):
+        B = self.fp.bufs[l]
+        return B.H.data_ptr() + 8 * int(B.lay.qoff[i]), int(B.lay.n[i])
+
+    # -------------------------------------------------------------- forward
+    def _build_forward(self):
+        fp, w = self.fp, self.w
+        prog = Program(self.device)
+        depth = fp.depth
+        if depth == 0:
+            d = fp.root_dim
+            prog.memcpy(self.yroot.data_ptr(), self.xin.data_ptr(), 8 * d * w)
+            prog.trsv([(fp.root_buf.data_ptr(), self.yroot.data_ptr(), d, d)], 0, w)
+            return prog
+        xin = self.xin
+        for l in range(depth, 0, -1):
+            V = self.v[l]
+            lay = fp.bufs[l].lay
+            n, k, r, nb = lay.n, lay.k, lay.r, lay.nb
+            offR, offS, offX = V["offR"], V["offS"], V["offX"]
+            below, _ = _near_sets(lay)
+            q = fp.dh2.q[l]
+            # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
+            outs = []
+            for i in range(nb):
+                outs.append((self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
+                             nat.GEMV_PLUS | nat.GEMV_SPLIT,
+                             [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))]))
+            prog.gemv(outs, w)
+            if self.mode == "parallel":
+                self._forward_parallel_level(prog, l, V, lay, below)
+            else:
+                self._forward_naive_level(prog, l, V, lay)
+            xin = V["BS"]
+        d = fp.root_dim
+        prog.memcpy(self.yroot.data_ptr(), xin.data_ptr(), 8 * d * w)
+        prog.trsv([(fp.root_buf.data_ptr(), self.yroot.data_ptr(), d, d)], 0, w)
+        return prog
+
+    def _forward_parallel_level(self, prog, l, V, lay, below):
+        w = self.w
+        n, k, r, nb = lay.n, lay.k, lay.r, lay.nb
+        offR, offS = V["offR"], V["offS"]
+        B = self.fp.bufs[l]
+        # P1  z_i = L_ii^-1 b_R,i
+        prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
+        prog.trsv([(*self._L(l, i)[:1], self._p(V["Z"], offR[i]), int(r[i]), self._L(l, i)[1]) for i in range(nb)], 0, w)
+        # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j
+        outs = []
+        for i in range(nb):
+            terms = [(B.T.data_ptr() + 8 * int(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
+                     for j in below[i] if r[j] > 0]
+            outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
+        prog.gemv(outs, w)
+        # P3  y_i = L_ii^-1 t_i
+        prog.trsv([(self._L(l, i)[0], self._p(V["Y"], offR[i]), int(r[i]), self._L(l, i)[1]) for i in range(nb)], 0, w)
+        # P4  b_S,a -= sum_b L(s)_ab y_b
+        self._ls_update_forward(prog, l, V, lay)
+
+    def _ls_update_forward(self, prog, l, V, lay, only_b=None):
+        w = self.w
+        offR, offS = V["offR"], V["offS"]
+        terms = {}
+        for (a, b) in self._ls_keys(lay):
+            if only_b is not None and b != only_b:
+                continue
+            ptr, ld = self._ls(l, a, b)
+            terms.setdefault(a, []).append((ptr, self._p(V["Y"], offR[b]), ld, 0, int(lay.r[b])))
+        outs = [(self._p(V["BS"], offS[a]), 0, self._p(V["BS"], offS[a]), int(lay.k[a]), 0, 0, sorted(t))
+                for a, t in sorted(terms.items())]
+        prog.gemv(outs, w)
+
+    def _forward_naive_level(self, prog, l, V, lay):
+        """Algorithm 3 order (ulv_solve.py:90-97): box by box."""
+        w = self.w
+        offR = V["offR"]
+        B = self.fp.bufs[l]
+        _, above = _near_sets(lay)
+        prog.memcpy(V["Y"].data_ptr(), V["BR"].data_ptr(), 8 * int(lay.r.sum()) * w)
+        for i in range(lay.nb):
+            Lp, ld = self._L(l, i)
+            prog.trsv([(Lp, self._p(V["Y"], offR[i]), int(lay.r[i]), ld)], 0, w)
+            outs = []
+            for j in above[i]:
+                if lay.r[i] == 0 or lay.r[j] == 0:
+                    continue
+                outs.append((self._p(V["Y"], offR[j]), 0, self._p(V["Y"], offR[j]), int(lay.r[j]), 0, 0,
+                             [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Y"], offR[i]), int(lay.n[i]), 0,
+                               int(lay.r[i]))]))
+            prog.gemv(outs, w)
+            self._ls_update_forward(prog, l, V, lay, only_b=i)
+
+    # -------------------------------------------------------------- backward
+    def _build_backward(self):
+        fp, w = self.fp, self.w
+        prog = Program(self.device)
+        depth = fp.depth
+        d = fp.root_dim
+        prog.memcpy(self.xroot.data_ptr(), self.yroot.data_ptr(), 8 * d * w)
+        prog.trsv([(fp.root_buf.data_ptr(), self.xroot.data_ptr(), d, d)], 1, w)
+        xs = self.xroot
+        for l in range(1, depth + 1):
+            V = self.v[l]
+            lay = fp.bufs[l].lay
+            n, k, r, nb = lay.n, lay.k, lay.r, lay.nb
+            offR, offS, offX = V["offR"], V["offS"], V["offX"]
+            B = fp.bufs[l]
+            # B1  y_R,i -= sum_a L(s)_ai^T x_S,a
+            src = {}
+            for (a, b) in self._ls_keys(lay):
+                ptr, ld = self._ls(l, a, b)
+                src.setdefault(b, []).append((ptr, self._p(xs, offS[a]), ld, 1, int(k[a])))
+            outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0, sorted(src.get(i, [])))
+                    for i in range(nb)]
+            prog.gemv(outs, w)
+            if self.mode == "parallel":
+                _, above = _near_sets(lay)
+                prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
+                prog.trsv([(self._L(l, i)[0], self._p(V["Z2"], offR[i]), int(r[i]), self._L(l, i)[1])
+                           for i in range(nb)], 1, w)
+                outs = []
+                for i in range(nb):
+                    terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
+                              int(r[j])) for j in above[i] if r[j] > 0]
+                    outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
+                prog.gemv(outs, w)
+                prog.trsv([(self._L(l, i)[0], self._p(V["XR"], offR[i]), int(r[i]), self._L(l, i)[1])
+                           for i in range(nb)], 1, w)
+            else:
+                self._backward_naive_level(prog, l, V, lay)
+            # B3  full_i = q_red x_R + q_skel x_S
+            q = fp.dh2.q[l]
+            outs = []
+            for i in range(nb):
+                qi = q.data_ptr() + 8 * int(lay.qoff[i])
+                terms = []
+                if r[i] > 0:
+                    terms.append((qi, self._p(V["XR"], offR[i]), int(n[i]), 0, int(r[i])))
+                if k[i] > 0:
+                    terms.append((qi + 8 * int(r[i]), self._p(xs, offS[i]), int(n[i]), 0, int(k[i])))
+                outs.append((self._p(V["FULL"], offX[i]), 0, 0, int(n[i]), 0, nat.GEMV_PLUS, terms))
+            prog.gemv(outs, w)
+            xs = V["FULL"]
+        return prog
+
+    def _backward_naive_level(self, prog, l, V, lay):
+        """ulv_solve.py:157-162: reversed box order."""
+        w = self.w
+        offR = V["offR"]
+        B = self.fp.bufs[l]
+        _, above = _near_sets(lay)
+        prog.memcpy(V["XR"].data_ptr(), V["YB"].data_ptr(), 8 * int(lay.r.sum()) * w)
+        for i in reversed(range(lay.nb)):
+            terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["XR"], offR[j]), int(lay.n[i]), 1,
+                      int(lay.r[j])) for j in above[i] if lay.r[j] > 0]
+            if terms:
+                prog.gemv([(self._p(V["XR"], offR[i]), 0, self._p(V["XR"], offR[i]), int(lay.r[i]), 0, 0, terms)], w)
+            Lp, ld = self._L(l, i)
+            prog.trsv([(Lp, self._p(V["XR"], offR[i]), int(lay.r[i]), ld)], 1, w)
+
+    # -------------------------------------------------------------- run
+    def run_forward(self, stream=None):
+        self.fwd.launch(stream)
+
+    def run_backward(self, stream=None):
+        self.bwd.launch(stream)
+
+    def block_vector(self, vector):
+        bv = BlockVector(width=self.w, vector=vector, _plan=self)
+        for l in range(self.fp.depth, 0, -1):
+            V = self.v[l]
+            lay = self.fp.bufs[l].lay
+            y = V["Y"].view(-1, self.w)
+            for i in range(lay.nb):
+                o = int(V["offR"][i])
+                bv.yr[(l, i)] = y[o:o + int(lay.r[i])].cpu().numpy()
+        bv.root = self.yroot.view(-1, self.w)[:self.fp.root_dim].cpu().numpy()
+        return bv
+
+
+def _plan_for(factors, w, mode):
+    cache = factors.__dict__.setdefault("_solve_plans", {})
+    key = (w, mode)
+    if key not in cache:
+        cache[key] = SolvePlan(factors.device, w, mode)
+    return cache[key]
+
+
+def _to_tree_order(factors, b):
+    bm = np.asarray(b, dtype=np.float64)
+    vector = bm.ndim == 1
+    bm = bm.reshape(factors.h2.count, -1)
+    return bm, vector
+
+
+def forward_parallel(factors, b):
+    return _forward(factors, b, "parallel")
+
+
+def forward_naive(factors, b):
+    return _forward(factors, b, "naive")
+
+
+def _forward(factors, b, mode):
+    """b in TREE order (as the reference's forward_* expect)."""
+    nat.lib()
+    bm, vector = _to_tree_order(factors, b)
+    sp = _plan_for(factors, bm.shape[1], mode)
+    sp.xin.view(-1, sp.w)[:factors.h2.count].copy_(torch.from_numpy(np.ascontiguousarray(bm)))
+    sp.run_forward()
+    return sp.block_vector(vector)
+
+
+def backward_parallel(factors, y):
+    return _backward(factors, y, "parallel")
+
+
+def backward_naive(factors, y):
+    return _backward(factors, y, "naive")
+
+
+def _backward(factors, y, mode):
+    nat.lib()
+    sp = _plan_for(factors, y.width, mode)
+    if y._plan is not sp:  # upload a host BlockVector
+        for l in range(factors.device.depth, 0, -1):
+            V = sp.v[l]
+            lay = factors.device.bufs[l].lay
+            dst = V["Y"].view(-1, sp.w)
+            for i in range(lay.nb):
+                o = int(V["offR"][i])
+                dst[o:o + int(lay.r[i])].copy_(torch.from_numpy(np.asarray(y.yr[(l, i)]).reshape(-1, sp.w)))
+        sp.yroot.view(-1, sp.w)[:factors.device.root_dim].copy_(
+            torch.from_numpy(np.asarray(y.root).reshape(-1, sp.w)))
+    sp.run_backward()
+    x = sp.output.view(-1, sp.w)[:factors.h2.count].cpu().numpy()
+    return x[:, 0] if y.vector else x
+
+
+def solve(factors, b, mode="parallel"):
+    """Solve A x = b with b in the ORIGINAL input order (ulv_solve.py:191-207)."""
+    if mode not in ("naive", "parallel"):
+        raise ValueError(f"unknown mode '{mode}'")
+    nat.lib()
+    bm = np.asarray(b, dtype=np.float64)
+    vector = bm.ndim == 1
+    bm = bm.reshape(factors.h2.count, -1)
+    sp = _plan_for(factors, bm.shape[1], mode)
+    dev = sp.device
+    perm = factors.__dict__.get("_perm_dev")
+    if perm is None:
+        perm = torch.from_numpy(np.asarray(factors.h2.cloud.perm, dtype=np.int64)).to(dev)
+        factors._perm_dev = perm
+    b_dev = torch.from_numpy(np.ascontiguousarray(bm)).to(dev)
+    sp.xin.view(-1, sp.w)[:factors.h2.count] = b_dev.index_select(0, perm)
+    sp.run_forward()
+    sp.run_backward()
+    x_dev = torch.empty_like(b_dev)
+    x_dev[perm] = sp.output.view(-1, sp.w)[:factors.h2.count]
+    x = x_dev.cpu().numpy()
+    return x[:, 0] if vector else x

@@ -1,0 +1,95 @@
+"""GPU parity: the sm_100a factorize/solve against the reference's own
+factors (golden fixtures) and the CPU oracle.  FP64 tolerances are written
+in each test; integer outputs (dims, flop report) must be identical."""
+import numpy as np
+import pytest
+
+from fixtures import H2_FIXTURES, flops_equal, load_h2, meta, reference_factors
+from oracle import h2ulv_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+RTOL_BLOCK = 1e-9     # factor blocks vs reference (same bases, different summation order)
+RTOL_X = 1e-8         # solution vs reference solution
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2502_02395_b200 as p
+    return p
+
+
+@pytest.mark.parametrize("name", H2_FIXTURES)
+def test_factor_blocks_match_reference(pkg, name):
+    h2 = load_h2(name)
+    ref = reference_factors(name)
+    f = pkg.factorize(h2)
+    assert flops_equal(f.flops, meta(name)["flops"])
+    assert f.audit["offdiag_ss_post_init_writes"] == 0 and f.audit["diag_ss_update_counts"] == [1]
+    for (l, i), v in ref["lr_diag"].items():
+        assert _rel(f.levels[l].lr_diag[i], v) < RTOL_BLOCK, (l, i)
+    for (l, i, j), v in ref["lr_off"].items():
+        assert _rel(f.levels[l].lr_off[(i, j)], v) < RTOL_BLOCK, (l, i, j)
+    for (l, a, b), v in ref["ls"].items():
+        assert _rel(f.levels[l].ls[(a, b)], v) < RTOL_BLOCK, (l, a, b)
+    for l in f.levels:
+        for i in f.levels[l].v:
+            lr = f.levels[l].lr_diag[i]
+            qr_ = h2.bases[(l, i)].q_red
+            assert np.allclose(f.levels[l].v[i] @ lr.T, qr_, atol=1e-10)
+    assert _rel(f.root, ref["root"]) < RTOL_BLOCK
+
+
+@pytest.mark.parametrize("name", H2_FIXTURES)
+@pytest.mark.parametrize("mode", ["parallel", "naive"])
+def test_solve_matches_reference(pkg, name, mode):
+    h2 = load_h2(name)
+    ref = reference_factors(name)
+    f = pkg.factorize(h2)
+    x = pkg.solve(f, ref["b"], mode=mode)
+    want = ref["x"] if mode == "parallel" else ref["x_naive"]
+    assert _rel(x, want) < RTOL_X
+    res = orc.residual(h2, x, ref["b"])
+    assert res <= 10 * meta(name)["residual"] + 1e-15
+
+
+def test_solve_multi_rhs_and_zero(pkg):
+    h2 = load_h2("h2_cube1024_sampled")
+    f = pkg.factorize(h2)
+    of = orc.factorize(h2)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((h2.count, 3))
+    x = pkg.solve(f, b)
+    assert x.shape == b.shape
+    assert _rel(x, orc.solve(of, b)) < RTOL_X
+    assert np.array_equal(pkg.solve(f, np.zeros(h2.count)), np.zeros(h2.count))
+
+
+def test_forward_backward_api(pkg):
+    from paper_2502_02395_b200 import ulv_solve
+
+    h2 = load_h2("h2_sphere1024_yukawa_tol")
+    f = pkg.factorize(h2)
+    of = orc.factorize(h2)
+    bt = np.random.default_rng(7).standard_normal(h2.count)
+    y = ulv_solve.forward_parallel(f, bt)
+    yr, yroot = orc.forward(of, bt)
+    for key, v in yr.items():
+        assert _rel(y.yr[key], v) < RTOL_X
+    assert _rel(y.root, yroot) < RTOL_X
+    x = ulv_solve.backward_parallel(f, y)
+    assert _rel(x, orc.backward(of, yr, yroot)[:, 0]) < RTOL_X
+
+
+def test_repeat_is_bitwise_deterministic(pkg):
+    h2 = load_h2("h2_cube512_rank16")
+    fa, fb = pkg.factorize(h2), pkg.factorize(h2, batched=False)
+    assert np.array_equal(fa.root, fb.root)
+    for l in fa.levels:
+        for i in fa.levels[l].lr_diag:
+            assert np.array_equal(fa.levels[l].lr_diag[i], fb.levels[l].lr_diag[i])
