@@ -263,6 +263,11 @@ typedef struct h2g_step {
 } h2g_step;
 
 int h2g_run_program(const h2g_step* steps, int nsteps, void* stream);
+/* Same as h2g_run_program, with a CUDA event recorded on `stream` before
+ * every step and after the last; synchronizes and writes the per-step device
+ * time (ms) to out_ms[nsteps] (host array).  Used by bench.py for the
+ * per-kernel roofline numbers. */
+int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* stream, float* out_ms);
 int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out);
 int h2g_graph_launch(void* exec, void* stream);
 int h2g_graph_destroy(void* exec);

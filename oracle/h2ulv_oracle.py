@@ -143,15 +143,13 @@ def factorize(h2):
         ss = {}
         fr.add(l, "diag_mul1", [("multiply", (n[i], n[i], n[i])) for i in range(nb)])
         fr.add(l, "diag_mul2", [("multiply", (n[i], n[i], n[i])) for i in range(nb)])
+        hs = [Q[i].T @ (cur[(i, i)] @ Q[i]) for i in range(nb)]
         for i in range(nb):
-            h = Q[i].T @ (cur[(i, i)] @ Q[i])
-            ri = r[i]
-            lr = chol(h[:ri, :ri], l, i)
-            lvl["lr_diag"][i] = lr
+            lvl["lr_diag"][i] = chol(hs[i][:r[i], :r[i]], l, i)
         # errors are raised per box in index order before any TRSM, as in the reference
         fr.add(l, "diag_chol", [("cholesky", (r[i],)) for i in range(nb)])
         for i in range(nb):
-            h = Q[i].T @ (cur[(i, i)] @ Q[i])
+            h = hs[i]
             ri = r[i]
             lr = lvl["lr_diag"][i]
             ls = trsm_right_lt(lr, h[ri:, :ri])
@@ -341,3 +339,57 @@ def residual(h2, x, b):
     perm = h2.cloud.perm
     r = h2_matvec(h2, np.asarray(x)[perm]) - np.asarray(b)[perm]
     return float(np.linalg.norm(r) / np.linalg.norm(b))
+
+
+# ----------------------------------------------------------------------------- construct (CPU)
+
+def construct(kernel, tree, lists, cfg, cloud, workers=None):
+    """CPU construction (h2_build.py:170-220) for the CPU baseline arm.
+
+    The skeleton pass is the package's host half (pinned bit-exact to the
+    reference by tests/test_host_parity.py); the complementary basis is
+    numpy's LAPACK QR (dense_core.py:136-148) and the blocks come from the
+    host kernel evaluator (kernels.py:46-64).  Returns an H2Matrix of host
+    numpy blocks (leaf near blocks only — the factorization reads no others).
+    """
+    import os
+
+    import scipy.linalg as sla
+
+    from paper_2502_02395_b200 import kernels
+    from paper_2502_02395_b200.dense_core import BasisDecomposition
+    from paper_2502_02395_b200.h2_build import H2Matrix, _skel_global, _skeleton_pass
+
+    h2 = H2Matrix(tree=tree, lists=lists, kernel=kernel, cloud=cloud, config=cfg)
+    depth = tree.depth
+    if depth == 0:
+        allp = np.arange(cloud.count, dtype=np.int64)
+        h2.near_blocks = {(0, 0, 0): kernels.gen_block(kernel, allp, allp, cloud)}
+        return h2
+    eff, choice = _skeleton_pass(kernel, tree, lists, cfg, cloud, h2.build_flops, workers or os.cpu_count())
+    h2.eff_points = eff
+    for l in range(depth, 0, -1):
+        for i in range(2 ** l):
+            c = choice[(l, i)]
+            n = len(eff[(l, i)])
+            k = 0 if c is None else c.rank
+            if k:
+                z = c.t
+                if l < depth:
+                    w = sla.block_diag(h2.bases[(l + 1, 2 * i)].frame, h2.bases[(l + 1, 2 * i + 1)].frame)
+                    z = w @ z
+                qf, fr = complete_qr(z, k)
+            else:
+                qf, fr = np.eye(n), np.zeros((0, 0))
+            skel = np.zeros(0, np.int64) if c is None else c.skeleton
+            h2.bases[(l, i)] = BasisDecomposition(q_skel=qf[:, n - k:], q_red=qf[:, :n - k], skeleton=skel,
+                                                  rank=k, frame=fr)
+            h2.skeletons[(l, i)] = _skel_global(eff, choice, l, i)
+        for (i, j) in lists.far[l]:
+            if i > j:
+                g = kernels.gen_block(kernel, h2.skeletons[(l, i)], h2.skeletons[(l, j)], cloud)
+                h2.couplings[(l, i, j)] = h2.bases[(l, i)].frame @ g @ h2.bases[(l, j)].frame.T
+    for (i, j) in lists.near[depth]:
+        if i >= j:
+            h2.near_blocks[(depth, i, j)] = kernels.gen_block(kernel, eff[(depth, i)], eff[(depth, j)], cloud)
+    return h2

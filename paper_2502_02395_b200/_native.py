@@ -55,7 +55,7 @@ QR_PANEL_WIDTH = 32
 
 EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_panel_potrf", "h2g_copy_tiles", "h2g_block_copy",
            "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
-           "h2g_run_program", "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
+           "h2g_run_program", "h2g_run_program_timed", "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
            "h2g_last_error", "h2g_device_sm_count"]
 
 _LIB = None
@@ -83,6 +83,7 @@ def load_library(path=LIB_PATH):
         "h2g_basis_finish": (i32, [vp, i32, vp]),
         "h2g_kernel_blocks": (i32, [vp, vp, i32, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp]),
         "h2g_run_program": (i32, [vp, i32, vp]),
+        "h2g_run_program_timed": (i32, [vp, i32, vp, vp]),
         "h2g_graph_capture": (i32, [vp, i32, vp, ctypes.POINTER(vp)]),
         "h2g_graph_launch": (i32, [vp, vp]),
         "h2g_graph_destroy": (i32, [vp]),

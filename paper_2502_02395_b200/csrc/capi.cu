@@ -81,6 +81,29 @@ extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream) 
   return H2G_OK;
 }
 
+extern "C" int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* stream, float* out_ms) {
+  if (nsteps <= 0) return H2G_OK;
+  if (!steps || !out_ms) return h2g_set_error(H2G_EINVAL, "h2g_run_program_timed: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t* ev = new cudaEvent_t[nsteps + 1];
+  for (int i = 0; i <= nsteps; ++i) cudaEventCreate(&ev[i]);
+  int rc = H2G_OK;
+  for (int i = 0; i < nsteps && rc == H2G_OK; ++i) {
+    cudaEventRecord(ev[i], st);
+    rc = run_step(steps[i], st);
+  }
+  cudaEventRecord(ev[nsteps], st);
+  cudaEventSynchronize(ev[nsteps]);
+  for (int i = 0; i < nsteps; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    out_ms[i] = ms;
+  }
+  for (int i = 0; i <= nsteps; ++i) cudaEventDestroy(ev[i]);
+  delete[] ev;
+  return rc;
+}
+
 extern "C" int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out) {
   if (!exec_out) return h2g_set_error(H2G_EINVAL, "h2g_graph_capture: null exec_out");
   cudaStream_t st = (cudaStream_t)stream;

@@ -42,6 +42,7 @@ class Program:
         self.steps = None
         self.graph = None
         self.kernel_launches = 0
+        self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
 
     # -- blob bookkeeping -------------------------------------------------------------
     def _blob(self, arr):
@@ -50,7 +51,8 @@ class Program:
         self._blobs.append(np.ascontiguousarray(arr).view(np.uint8).reshape(-1))
         return len(self._blobs) - 1
 
-    def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0):
+    def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0, flops=0, nbytes=0):
+        self.work.append((kind, int(flops), int(nbytes)))
         self._steps.append(dict(kind=kind, count=int(count), grid=int(grid), descs=descs, map=map_, npd=npd,
                                 arg=int(arg), aux=aux, d0=float(d0), d1=float(d1)))
 
@@ -71,7 +73,10 @@ class Program:
         tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
         # K == 0 problems still need their beta*C epilogue; keep them (tiles > 0)
         kind = nat.STEP["GEMM_NN"] + 2 * int(bool(trans_a)) + int(bool(trans_b))
-        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap))
+        m64, n64, k64 = arr["M"].astype(np.int64), arr["N"].astype(np.int64), arr["K"].astype(np.int64)
+        lower = (arr["flags"] & nat.GEMM_LOWER) != 0
+        fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl)
         return total
 
     def panel(self, descs, npd_ptr):
@@ -86,7 +91,10 @@ class Program:
         ctas = np.maximum(1, -(-rows_total // arr["rows_per_cta"]))
         arr["cta_start"] = np.concatenate([[0], np.cumsum(ctas)[:-1]])
         cmap = np.repeat(np.arange(len(descs), dtype=np.int32), ctas)
-        self._add(nat.STEP["PANEL"], len(descs), int(ctas.sum()), self._blob(arr), self._blob(cmap), npd=npd_ptr)
+        b64 = arr["b"].astype(np.int64)
+        fl = (b64 ** 3 // 3 + (rows_total * b64 * b64)).sum()
+        self._add(nat.STEP["PANEL"], len(descs), int(ctas.sum()), self._blob(arr), self._blob(cmap), npd=npd_ptr,
+                  flops=fl)
         return int(ctas.sum())
 
     def copy(self, descs):
@@ -101,12 +109,13 @@ class Program:
         tiles = np.array([copy_tiles(r, c) for r, c in zip(arr["rows"], arr["cols"])], dtype=np.int64)
         arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
-        self._add(nat.STEP["COPY"], len(rows), int(tiles.sum()), self._blob(arr), self._blob(tmap))
+        self._add(nat.STEP["COPY"], len(rows), int(tiles.sum()), self._blob(arr), self._blob(tmap),
+                  nbytes=16 * int((arr["rows"].astype(np.int64) * arr["cols"]).sum()))
         return int(tiles.sum())
 
     def memcpy(self, dst_ptr, src_ptr, nbytes):
         if nbytes > 0:
-            self._add(nat.STEP["MEMCPY"], int(nbytes), 0, ("raw", dst_ptr), ("raw", src_ptr))
+            self._add(nat.STEP["MEMCPY"], int(nbytes), 0, ("raw", dst_ptr), ("raw", src_ptr), nbytes=2 * int(nbytes))
 
     def qr_panel(self, descs):
         """descs: list of (Z, V, tau, T, n, ldz, p, b)."""
@@ -211,6 +220,14 @@ class Program:
         lib = nat.lib()
         rc = lib.h2g_run_program(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps), nat.stream_ptr(stream))
         nat.check(rc, "h2g_run_program")
+
+    def run_timed(self, stream=None):
+        """Eager run with an event pair around every step; returns per-step ms."""
+        out = np.zeros(len(self.steps), dtype=np.float32)
+        rc = nat.lib().h2g_run_program_timed(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps),
+                                             nat.stream_ptr(stream), out.ctypes.data_as(ctypes.c_void_p))
+        nat.check(rc, "h2g_run_program_timed")
+        return out
 
     def capture(self, stream=None):
         """Capture the whole program into one CUDA graph (on a side stream)."""
