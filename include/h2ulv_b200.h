@@ -66,34 +66,30 @@ int h2g_gemm_tiles(int M, int N, int flags); /* tiles one problem needs */
 int h2g_gemm_grouped(int trans_a, int trans_b, const h2g_gemm_problem* d_probs,
                      const int32_t* d_tile_map, int total_tiles, void* stream);
 
-/* ---- panel of the partial (ULV) Cholesky ----------------------------------
- * For one box: factor the b x b diagonal block H[p:p+b, p:p+b] (b <= 64) in
- * place (lower Cholesky) and overwrite every row x of
- *   H[p+b : n, p : p+b]   and   R[0 : nr, p : p+b]
- * with x * L^-T.  Together with the trailing update (h2g_gemm_grouped, NT,
- * alpha=-1, beta=1) this is the right-looking partial Cholesky of the
- * sparsified diagonal block that yields L(r)_ii, L(s)_ii, V_i and the single
- * Schur update of SS_ii in ONE pass (ulv_factor.py:217-241 =
- * factor_diag, ulv_factor.py:78-84).  The descriptor's CTAs split the rows;
- * d_cta_map[c] is the descriptor of CTA c.  A pivot that is not > 0 (or
- * NaN) at column p+j records atomicMin(&d_npd[npd_slot], p+j) — the same
- * pivot index dpotrf's info-1 reports (dense_core.py:60-63).
+/* ---- diagonal block of a panel of the partial (ULV) Cholesky ---------------
+ * One CTA per descriptor (box): factor the b x b diagonal block
+ * H[p:p+b, p:p+b] (b <= 64) in place (lower Cholesky) and write its inverse
+ * L_pp^-1 into the 64 x 64 scratch block `Linv` (ld ldl; zero padded).  The
+ * host program follows it with two h2g_gemm_grouped launches (NT):
+ *   TRSM  X <- X * Linv^T in place for X = H[p+b:n, p:p+b] and R[0:n, p:p+b]
+ *   TRAIL H[p+b:, p+b:] -= X X^T (H2G_GEMM_LOWER), R[:, p+b:r] -= V_P L^T
+ * which together are the right-looking partial Cholesky of the sparsified
+ * diagonal block yielding L(r)_ii, L(s)_ii, V_i and the single Schur update
+ * of SS_ii in ONE pass over H (ulv_factor.py:217-241 = factor_diag,
+ * ulv_factor.py:78-84).  A pivot that is not > 0 (or NaN) at column p+j
+ * records atomicMin(&d_npd[npd_slot], p+j) — the pivot index dpotrf's
+ * info-1 reports (dense_core.py:60-63).
  */
 typedef struct h2g_panel_desc {
   double* H;
-  double* R;          /* may be NULL when nr == 0 */
-  int32_t ldh, ldr;
-  int32_t n;          /* rows of H (trailing rows p+b..n-1 get the TRSM) */
-  int32_t nr;         /* rows of R */
+  double* Linv;       /* 64 x 64 scratch output */
+  int32_t ldh, ldl;
   int32_t p, b;       /* panel start column and width (1..64) */
   int32_t npd_slot;   /* index into d_npd */
-  int32_t cta_start;  /* first CTA of this descriptor */
-  int32_t rows_per_cta;
   int32_t pad_;
 } h2g_panel_desc;
 
-int h2g_panel_potrf(const h2g_panel_desc* d_descs, const int32_t* d_cta_map,
-                    int total_ctas, int32_t* d_npd, void* stream);
+int h2g_panel_potrf(const h2g_panel_desc* d_descs, int count, int32_t* d_npd, void* stream);
 
 /* ---- block copy / gather ----------------------------------------------------
  * dst[r, c] = src(r, c) for an rows x cols block, where src(r, c) is

@@ -20,9 +20,8 @@ LIB_PATH = os.path.join(HERE, "libh2ulv_b200.so")
 GEMM_DT = np.dtype([("A", "<u8"), ("B", "<u8"), ("C", "<u8"), ("M", "<i4"), ("N", "<i4"), ("K", "<i4"),
                     ("lda", "<i4"), ("ldb", "<i4"), ("ldc", "<i4"), ("tile_start", "<i4"), ("flags", "<i4"),
                     ("alpha", "<f8"), ("beta", "<f8")])
-PANEL_DT = np.dtype([("H", "<u8"), ("R", "<u8"), ("ldh", "<i4"), ("ldr", "<i4"), ("n", "<i4"), ("nr", "<i4"),
-                     ("p", "<i4"), ("b", "<i4"), ("npd_slot", "<i4"), ("cta_start", "<i4"),
-                     ("rows_per_cta", "<i4"), ("pad_", "<i4")])
+PANEL_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("ldh", "<i4"), ("ldl", "<i4"), ("p", "<i4"), ("b", "<i4"),
+                     ("npd_slot", "<i4"), ("pad_", "<i4")])
 COPY_DT = np.dtype([("src", "<u8"), ("dst", "<u8"), ("rows", "<i4"), ("cols", "<i4"), ("lds", "<i4"),
                     ("ldd", "<i4"), ("mode", "<i4"), ("tile_start", "<i4")])
 GEMV_TERM_DT = np.dtype([("A", "<u8"), ("x", "<u8"), ("lda", "<i4"), ("trans", "<i4"), ("K", "<i4"),
@@ -39,7 +38,7 @@ KBLOCK_DT = np.dtype([("rows", "<u8"), ("cols", "<u8"), ("out", "<u8"), ("m", "<
 STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", "<i4"), ("descs", "<u8"),
                     ("map", "<u8"), ("npd", "<u8"), ("aux", "<u8"), ("d0", "<f8"), ("d1", "<f8")])
 
-assert GEMM_DT.itemsize == 72 and PANEL_DT.itemsize == 56 and COPY_DT.itemsize == 40
+assert GEMM_DT.itemsize == 72 and PANEL_DT.itemsize == 40 and COPY_DT.itemsize == 40
 assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 24
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 64
 
@@ -74,7 +73,7 @@ def load_library(path=LIB_PATH):
     sig = {
         "h2g_gemm_tiles": (i32, [i32, i32, i32]),
         "h2g_gemm_grouped": (i32, [i32, i32, vp, vp, i32, vp]),
-        "h2g_panel_potrf": (i32, [vp, vp, i32, vp, vp]),
+        "h2g_panel_potrf": (i32, [vp, i32, vp, vp]),
         "h2g_copy_tiles": (i32, [i32, i32]),
         "h2g_block_copy": (i32, [vp, vp, i32, vp]),
         "h2g_gemv_grouped": (i32, [vp, i32, vp, i32, vp]),

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(THREADS) gemm_grouped_kernel(const h2g_gemm_pr
   cp_async_wait<0>();
 
   // epilogue: C = alpha*acc + beta*C
-  double* __restrict__ C = P.C;
+  double* C = P.C;  // may alias A (in-place TRSM with N <= 64)
   const int ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
 #pragma unroll

@@ -80,22 +80,16 @@ class Program:
         return total
 
     def panel(self, descs, npd_ptr):
-        """descs: list of (H, R, ldh, ldr, n, nr, p, b, npd_slot, rows_per_cta)."""
+        """descs: list of (H, Linv, ldh, ldl, p, b, npd_slot)."""
         if not descs:
             return 0
         arr = np.zeros(len(descs), dtype=nat.PANEL_DT)
-        cols = list(zip(*descs))
-        for name, col in zip(("H", "R", "ldh", "ldr", "n", "nr", "p", "b", "npd_slot", "rows_per_cta"), cols):
+        for name, col in zip(("H", "Linv", "ldh", "ldl", "p", "b", "npd_slot"), zip(*descs)):
             arr[name] = col
-        rows_total = (arr["n"] - arr["p"] - arr["b"]).astype(np.int64) + arr["nr"]
-        ctas = np.maximum(1, -(-rows_total // arr["rows_per_cta"]))
-        arr["cta_start"] = np.concatenate([[0], np.cumsum(ctas)[:-1]])
-        cmap = np.repeat(np.arange(len(descs), dtype=np.int32), ctas)
         b64 = arr["b"].astype(np.int64)
-        fl = (b64 ** 3 // 3 + (rows_total * b64 * b64)).sum()
-        self._add(nat.STEP["PANEL"], len(descs), int(ctas.sum()), self._blob(arr), self._blob(cmap), npd=npd_ptr,
-                  flops=fl)
-        return int(ctas.sum())
+        self._add(nat.STEP["PANEL"], len(descs), len(descs), self._blob(arr), npd=npd_ptr,
+                  flops=int((b64 ** 3 // 3 + b64 ** 3 // 3).sum()))
+        return len(descs)
 
     def copy(self, descs):
         """descs: list of (src, dst, rows, cols, lds, ldd, mode)."""

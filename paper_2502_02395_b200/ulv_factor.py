@@ -139,6 +139,7 @@ class FactorPlan:
         prog.memcpy(self.npd.data_ptr(), self._npd_init.data_ptr(), 4 * (acc + 1))
         self.bufs = {}
         self.merge_pairs = {}
+        self._linv_keep = []
 
         if depth == 0:
             d = int(dh2.root_a.shape[0])
@@ -220,27 +221,42 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0):
+        """Right-looking partial Cholesky of every box's H (and V rows in R),
+        panels of 64 columns: DIAG (chol + inverse of the 64x64 diagonal block),
+        TRSM as an in-place GEMM with L_pp^-T, TRAIL as a GEMM (lower tiles of H)."""
         nb = len(n)
         rmax = int(r.max()) if nb else 0
-        for p in range(0, rmax, nat.PANEL_WIDTH):
-            descs, prob = [], []
+        if rmax == 0:
+            return
+        W = nat.PANEL_WIDTH
+        linv = torch.empty(nb * W * W, dtype=F64, device=self.device)
+        self._linv_keep.append(linv)
+        lp = linv.data_ptr()
+        for p in range(0, rmax, W):
+            descs, trsm, trail = [], [], []
             for i in range(nb):
                 ri, ni = int(r[i]), int(n[i])
                 if ri <= p:
                     continue
-                b = min(nat.PANEL_WIDTH, ri - p)
+                b = min(W, ri - p)
                 h = Hp + 8 * int(qo[i])
-                rr = Rp + 8 * int(qo[i]) if Rp else 0
-                descs.append((h, rr, ni, ni, ni, ni if Rp else 0, p, b, slot0 + i, PANEL_ROWS_PER_CTA))
+                li = lp + 8 * i * W * W
+                descs.append((h, li, ni, W, p, b, slot0 + i))
                 m = ni - p - b
                 pan = h + 8 * ((p + b) * ni + p)
                 if m > 0:
-                    prob.append((pan, pan, h + 8 * ((p + b) * ni + p + b), m, m, b, ni, ni, ni,
-                                 nat.GEMM_LOWER, -1.0, 1.0))
-                if Rp and ri - p - b > 0:
-                    prob.append((rr + 8 * p, pan, rr + 8 * (p + b), ni, ri - p - b, b, ni, ni, ni, 0, -1.0, 1.0))
+                    trsm.append((pan, li, pan, m, b, b, ni, W, ni, 0, 1.0, 0.0))
+                    trail.append((pan, pan, h + 8 * ((p + b) * ni + p + b), m, m, b, ni, ni, ni,
+                                  nat.GEMM_LOWER, -1.0, 1.0))
+                if Rp:
+                    rr = Rp + 8 * int(qo[i])
+                    trsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
+                    if ri - p - b > 0:
+                        trail.append((rr + 8 * p, pan, rr + 8 * (p + b), ni, ri - p - b, b, ni, ni, ni,
+                                      0, -1.0, 1.0))
             prog.panel(descs, self.npd.data_ptr())
-            prog.gemm(0, 1, prob)
+            prog.gemm(0, 1, trsm)
+            prog.gemm(0, 1, trail)
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
         assert d == ld

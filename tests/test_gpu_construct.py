@@ -92,3 +92,22 @@ def test_yukawa_sampled_small(pkg):
     b = np.random.default_rng(1).standard_normal(2048)
     x, xo = pkg.solve(f, b), orc.solve(of, b)
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-8
+
+
+def test_many_boxes_multi_panel_matches_oracle(pkg):
+    """128 leaves with r > 64 (several Cholesky panels) and leaf near pairs:
+    many CTAs per launch, the regime where a panel-kernel race once showed up."""
+    h2 = _build(pkg, "cube", 32768, 256, "laplace", 1e5, tol=1e-8, s_far=512, s_near=512)
+    f = pkg.factorize(h2)
+    of = orc.factorize(h2)
+    depth = h2.tree.depth
+    for l in (depth, depth - 1):
+        lv, ol = f.levels[l], of.levels[l]
+        assert max(lv.dims[i][0] for i in lv.dims) > 64
+        for i in ol["v"]:
+            assert np.linalg.norm(lv.v[i] - ol["v"][i]) <= 1e-10 * np.linalg.norm(ol["v"][i])
+        for key in ol["lr_off"]:
+            assert np.linalg.norm(lv.lr_off[key] - ol["lr_off"][key]) <= 1e-10 * max(1.0, np.linalg.norm(ol["lr_off"][key]))
+    b = np.random.default_rng(1).standard_normal(h2.count)
+    x, xo = pkg.solve(f, b), orc.solve(of, b)
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-9

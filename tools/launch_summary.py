@@ -1,0 +1,30 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV: time per kernel name."""
+import collections
+import csv
+import sys
+
+
+def summarise(path, skip=0):
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.reader(lines[start:]))
+    h, data = rows[0], rows[1:]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.OrderedDict()
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    for r in data[skip:]:
+        name = r[ki].split("(")[0].replace("void ", "")
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += v
+    tot = sum(a[1] for a in agg.values())
+    out = [f"{'kernel':70s} {'launches':>8s} {'total ms':>10s} {'share':>7s}"]
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"{k[:70]:70s} {n:8d} {t / 1e3:10.3f} {100 * t / tot:6.1f}%")
+    out.append(f"{'TOTAL':70s} {sum(a[0] for a in agg.values()):8d} {tot / 1e3:10.3f}")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    print(summarise(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0))
