@@ -281,6 +281,11 @@ def main():
             g_fl += fl
             g_ms += t
     eager_ms = float(step_ms.sum())
+    if os.environ.get("BENCH_DUMP"):
+        with open(os.environ["BENCH_DUMP"], "w") as fh:
+            json.dump([{"kind": names[int(kd)], "flops": int(fl), "bytes": int(by), "ms": float(t),
+                        "count": int(st["count"]), "grid": int(st["grid"])}
+                       for (kd, fl, by), t, st in zip(prog.work, step_ms, prog.steps)], fh)
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")

@@ -124,6 +124,8 @@ int h2g_block_copy(const h2g_copy_desc* d_descs, const int32_t* d_tile_map,
  * rows [split, m) -> y2 (the basis transform of _transform_in,
  * ulv_solve.py:33-41, split = r).  Terms of output o are
  * d_terms[term_begin .. term_end).  With H2G_GEMV_PLUS the sum is added.
+ * Each output is split into 256-row chunks, one CTA each (chunk_start =
+ * running sum of ceil(m / 256)).
  * Replaces the per-box numpy products of _forward/_backward
  * (ulv_solve.py:98-113, 144-181).
  */
@@ -146,18 +148,21 @@ typedef struct h2g_gemv_out {
   int32_t split;     /* SPLIT only */
   int32_t term_begin, term_end;
   int32_t flags;
-  int32_t pad_;
+  int32_t chunk_start; /* first 256-row chunk (CTA) of this output */
 } h2g_gemv_out;
 
 int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
-                     int w, void* stream);
+                     int total_chunks, int w, void* stream);
 
 /* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
  * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
- * leading dimension ldl (dense_core.tri_solve, dense_core.py:69-81).
+ * leading dimension ldl, Linv the inverses of its 64 x 64 diagonal blocks
+ * (written by h2g_panel_potrf, 64*64 doubles per block, block q at
+ * Linv + q*4096) (dense_core.tri_solve, dense_core.py:69-81).
  */
 typedef struct h2g_trsv_desc {
   const double* L;
+  const double* Linv;
   double* x;
   int32_t n;
   int32_t ldl;
@@ -239,7 +244,7 @@ enum {
   H2G_STEP_MEMCPY = 6,   /* descs = dst, map = src (bytes in count) */
   H2G_STEP_QR_PANEL = 7,
   H2G_STEP_BASIS = 8,
-  H2G_STEP_GEMV = 9,     /* descs = outs, map = terms, grid = w            */
+  H2G_STEP_GEMV = 9,     /* descs = outs, map = terms, grid = chunks, arg = w */
   H2G_STEP_TRSV = 10,    /* descs = trsv descs, grid = w, arg = trans      */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay

@@ -27,8 +27,8 @@ COPY_DT = np.dtype([("src", "<u8"), ("dst", "<u8"), ("rows", "<i4"), ("cols", "<
 GEMV_TERM_DT = np.dtype([("A", "<u8"), ("x", "<u8"), ("lda", "<i4"), ("trans", "<i4"), ("K", "<i4"),
                          ("pad_", "<i4")])
 GEMV_OUT_DT = np.dtype([("y", "<u8"), ("y2", "<u8"), ("init", "<u8"), ("m", "<i4"), ("split", "<i4"),
-                        ("term_begin", "<i4"), ("term_end", "<i4"), ("flags", "<i4"), ("pad_", "<i4")])
-TRSV_DT = np.dtype([("L", "<u8"), ("x", "<u8"), ("n", "<i4"), ("ldl", "<i4")])
+                        ("term_begin", "<i4"), ("term_end", "<i4"), ("flags", "<i4"), ("chunk_start", "<i4")])
+TRSV_DT = np.dtype([("L", "<u8"), ("Linv", "<u8"), ("x", "<u8"), ("n", "<i4"), ("ldl", "<i4")])
 QRP_DT = np.dtype([("Z", "<u8"), ("V", "<u8"), ("tau", "<u8"), ("T", "<u8"), ("n", "<i4"), ("ldz", "<i4"),
                    ("p", "<i4"), ("b", "<i4")])
 BASIS_DT = np.dtype([("Q", "<u8"), ("Z", "<u8"), ("qfull", "<u8"), ("frame", "<u8"), ("n", "<i4"), ("k", "<i4"),
@@ -39,7 +39,7 @@ STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", 
                     ("map", "<u8"), ("npd", "<u8"), ("aux", "<u8"), ("d0", "<f8"), ("d1", "<f8")])
 
 assert GEMM_DT.itemsize == 72 and PANEL_DT.itemsize == 40 and COPY_DT.itemsize == 40
-assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 24
+assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 32
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 64
 
 STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "PANEL": 4, "COPY": 5, "MEMCPY": 6,
@@ -76,7 +76,7 @@ def load_library(path=LIB_PATH):
         "h2g_panel_potrf": (i32, [vp, i32, vp, vp]),
         "h2g_copy_tiles": (i32, [i32, i32]),
         "h2g_block_copy": (i32, [vp, vp, i32, vp]),
-        "h2g_gemv_grouped": (i32, [vp, i32, vp, i32, vp]),
+        "h2g_gemv_grouped": (i32, [vp, i32, vp, i32, i32, vp]),
         "h2g_trsv_batched": (i32, [vp, i32, i32, i32, vp]),
         "h2g_qr_panel": (i32, [vp, i32, vp]),
         "h2g_basis_finish": (i32, [vp, i32, vp]),

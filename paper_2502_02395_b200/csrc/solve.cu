@@ -1,180 +1,207 @@
 // Batched substitution kernels (forward / backward sweeps of the ULV
-// factors, ulv_solve.py:66-188).  The solve is HBM/latency bound: every
-// factor block is read once per sweep, so the kernels are written for
-// coalesced streaming of the block rows, one CTA per output segment / box.
+// factors, ulv_solve.py:66-188).  The solve streams every factor block once
+// per sweep, so the kernels are built for memory-level parallelism: all
+// loads of a thread are independent and unrolled, rows of a transposed
+// operand are split across warps and reduced through shared memory, and a
+// large segment is split over several CTAs (one 256-row output chunk each).
 #include "common.cuh"
 
 namespace h2g {
 
 constexpr int GV_THREADS = 256;
-constexpr int GV_WMAX = 8;        // columns processed per pass
-constexpr int GV_ROWS = 2048;     // rows per smem chunk (x GV_WMAX doubles = 128 KB max)
+constexpr int GV_CHUNK = 256;   // output rows per CTA
+constexpr int GV_W = 4;         // RHS columns per pass
 
-// acc (rows x wc) += sum over terms of op(A) x   for rows [r0, r0+nr), columns [j0, j0+wc)
-__global__ void __launch_bounds__(GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs,
-                                                                  const h2g_gemv_term* __restrict__ terms,
-                                                                  int w) {
-  extern __shared__ double acc[];  // GV_ROWS * GV_WMAX
-  const h2g_gemv_out O = outs[blockIdx.x];
+__device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (outs[mid].chunk_start <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t
+__global__ void __launch_bounds__(GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
+                                                                  const h2g_gemv_term* __restrict__ terms, int w) {
+  __shared__ double acc[GV_CHUNK * GV_W];
+  __shared__ double red[GV_THREADS / 32][GV_CHUNK];
+  const int oi = find_out(outs, n_outs, blockIdx.x);
+  const h2g_gemv_out O = outs[oi];
+  const int r0 = (blockIdx.x - O.chunk_start) * GV_CHUNK;
+  const int nr = min(GV_CHUNK, O.m - r0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = GV_THREADS / 32;
+  constexpr int NW = GV_THREADS / 32;
   const double sign = (O.flags & H2G_GEMV_PLUS) ? 1.0 : -1.0;
   const bool split = (O.flags & H2G_GEMV_SPLIT) != 0;
 
-  for (int j0 = 0; j0 < w; j0 += GV_WMAX) {
-    const int wc = min(GV_WMAX, w - j0);
-    for (int r0 = 0; r0 < O.m; r0 += GV_ROWS) {
-      const int nr = min(GV_ROWS, O.m - r0);
-      for (int e = tid; e < nr * GV_WMAX; e += GV_THREADS) acc[e] = 0.0;
-      __syncthreads();
-      for (int ti = O.term_begin; ti < O.term_end; ++ti) {
-        const h2g_gemv_term T = terms[ti];
-        const double* __restrict__ A = T.A;
-        const double* __restrict__ x = T.x;
-        if (!T.trans) {
-          // A is m x K: warp per row, lanes stride the (contiguous) columns
-          for (int rr = warp; rr < nr; rr += nwarps) {
-            const double* arow = A + (size_t)(r0 + rr) * T.lda;
-            double s[GV_WMAX];
+  for (int j0 = 0; j0 < w; j0 += GV_W) {
+    const int wc = min(GV_W, w - j0);
+    for (int e = tid; e < GV_CHUNK * GV_W; e += GV_THREADS) acc[e] = 0.0;
+    __syncthreads();
+    for (int ti = O.term_begin; ti < O.term_end; ++ti) {
+      const h2g_gemv_term T = terms[ti];
+      const double* __restrict__ A = T.A;
+      const double* __restrict__ x = T.x;
+      const int K = T.K, lda = T.lda;
+      if (!T.trans) {
+        // A is m x K: warp per output row, lanes over the contiguous K axis
+        for (int rr = warp; rr < nr; rr += NW) {
+          const double* arow = A + (size_t)(r0 + rr) * lda;
+          double s[GV_W] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+          for (int c = lane; c < K; c += 32) {
+            const double a = arow[c];
+            const double* xc = x + (size_t)c * w + j0;
 #pragma unroll
-            for (int j = 0; j < GV_WMAX; ++j) s[j] = 0.0;
-            for (int c = lane; c < T.K; c += 32) {
-              double a = arow[c];
-              const double* xc = x + (size_t)c * w + j0;
-#pragma unroll
-              for (int j = 0; j < GV_WMAX; ++j)
-                if (j < wc) s[j] += a * xc[j];
-            }
-#pragma unroll
-            for (int j = 0; j < GV_WMAX; ++j) {
-              double v = s[j];
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-              if (lane == 0 && j < wc) acc[rr * GV_WMAX + j] += v;
-            }
+            for (int j = 0; j < GV_W; ++j)
+              if (j < wc) s[j] += a * xc[j];
           }
-        } else {
-          // A is K x m: thread per output row, coalesced along the row of A
-          for (int rr = tid; rr < nr; rr += GV_THREADS) {
-            double s[GV_WMAX];
 #pragma unroll
-            for (int j = 0; j < GV_WMAX; ++j) s[j] = 0.0;
-            const double* acol = A + r0 + rr;
-            for (int c = 0; c < T.K; ++c) {
-              double a = acol[(size_t)c * T.lda];
-              const double* xc = x + (size_t)c * w + j0;
+          for (int j = 0; j < GV_W; ++j) {
+            double v = s[j];
 #pragma unroll
-              for (int j = 0; j < GV_WMAX; ++j)
-                if (j < wc) s[j] += a * xc[j];
-            }
-#pragma unroll
-            for (int j = 0; j < GV_WMAX; ++j)
-              if (j < wc) acc[rr * GV_WMAX + j] += s[j];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && j < wc) acc[rr * GV_W + j] += v;
           }
         }
         __syncthreads();
+      } else {
+        // A is K x m: warps split the K rows, lanes own output columns
+        for (int j = 0; j < wc; ++j) {
+          double s[GV_CHUNK / 32];
+#pragma unroll
+          for (int t = 0; t < GV_CHUNK / 32; ++t) s[t] = 0.0;
+#pragma unroll 2
+          for (int c = warp; c < K; c += NW) {
+            const double xv = x[(size_t)c * w + j0 + j];
+            const double* arow = A + (size_t)c * lda + r0;
+#pragma unroll
+            for (int t = 0; t < GV_CHUNK / 32; ++t) {
+              const int rr = lane + 32 * t;
+              if (rr < nr) s[t] += arow[rr] * xv;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < GV_CHUNK / 32; ++t) red[warp][lane + 32 * t] = s[t];
+          __syncthreads();
+          for (int rr = tid; rr < nr; rr += GV_THREADS) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) v += red[q][rr];
+            acc[rr * GV_W + j] += v;
+          }
+          __syncthreads();
+        }
       }
-      for (int e = tid; e < nr * wc; e += GV_THREADS) {
-        int rr = e / wc, j = e % wc;
-        int r = r0 + rr;
-        double v = sign * acc[rr * GV_WMAX + j];
-        if (O.init) v += O.init[(size_t)r * w + j0 + j];
-        if (split && r >= O.split) O.y2[(size_t)(r - O.split) * w + j0 + j] = v;
-        else O.y[(size_t)r * w + j0 + j] = v;
-      }
-      __syncthreads();
     }
+    for (int e = tid; e < nr * wc; e += GV_THREADS) {
+      const int rr = e / wc, j = e % wc;
+      const int r = r0 + rr;
+      double v = sign * acc[rr * GV_W + j];
+      if (O.init) v += O.init[(size_t)r * w + j0 + j];
+      if (split && r >= O.split) O.y2[(size_t)(r - O.split) * w + j0 + j] = v;
+      else O.y[(size_t)r * w + j0 + j] = v;
+    }
+    __syncthreads();
   }
 }
 
-// In-place triangular solve with the lower factor L (n x n, ld):
-//   trans = 0: x <- L^-1 x (forward);  trans = 1: x <- L^-T x (backward).
-// Blocked by 32 rows; the off-block products are warp dot products, the
-// 32x32 diagonal triangle is solved by one warp from shared memory.
-constexpr int TB = 32;
+// In-place triangular solve with the lower factor L (n x n, ld) of one box,
+// blocked by the 64-wide Cholesky panels whose inverses Linv_q (64 x 64,
+// written by the factorization's diagonal step) turn every diagonal solve
+// into a small GEMV:
+//   trans = 0:  x_P <- Linv_q (x_P - L[P, <P] x_<P)       (forward)
+//   trans = 1:  x_P <- Linv_q^T (x_P - L[>P, P]^T x_>P)   (backward)
+constexpr int TB = 64;
 __global__ void __launch_bounds__(256) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
                                                            int w) {
-  __shared__ double Ld[TB][TB + 1];
-  __shared__ double part[TB];
+  __shared__ double t[TB];
+  __shared__ double red[8][TB];
   const h2g_trsv_desc D = descs[blockIdx.x];
   const int n = D.n, ld = D.ldl;
   const double* __restrict__ L = D.L;
+  const double* __restrict__ Li = D.Linv;
   double* __restrict__ x = D.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (n == 0) return;
   const int nblk = (n + TB - 1) / TB;
   for (int j = 0; j < w; ++j) {
     for (int bi = 0; bi < nblk; ++bi) {
-      const int blk = trans ? (nblk - 1 - bi) : bi;
-      const int i0 = blk * TB;
+      const int q = trans ? (nblk - 1 - bi) : bi;
+      const int i0 = q * TB;
       const int nb = min(TB, n - i0);
-      // diagonal block -> smem
-      for (int e = tid; e < TB * TB; e += 256) {
-        int r = e / TB, c = e % TB;
-        Ld[r][c] = (r < nb && c < nb) ? L[(size_t)(i0 + r) * ld + i0 + c] : 0.0;
-      }
-      // off-block contribution
+      const double* Lq = Li + (size_t)q * TB * TB;
       if (!trans) {
-        // part[r] = sum_{c < i0} L[i0+r][c] x[c]
+        // t[r] = x[i0+r] - sum_{c < i0} L[i0+r][c] x[c]   (warp per row)
         for (int r = warp; r < nb; r += 8) {
           const double* lrow = L + (size_t)(i0 + r) * ld;
           double s = 0.0;
+#pragma unroll 4
           for (int c = lane; c < i0; c += 32) s += lrow[c] * x[(size_t)c * w + j];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) part[r] = s;
+          if (lane == 0) t[r] = x[(size_t)(i0 + r) * w + j] - s;
         }
-      } else {
-        // part[r] = sum_{c >= i0+nb} L[c][i0+r] x[c]; 8 warps split c, lanes over r
-        __shared__ double red[8][TB];
-        double s = 0.0;
-        if (lane < nb)
-          for (int c = i0 + nb + warp; c < n; c += 8) s += L[(size_t)c * ld + i0 + lane] * x[(size_t)c * w + j];
-        red[warp][lane] = s;
         __syncthreads();
-        if (warp == 0) {
-          double t = 0.0;
+        // x[i0+r] = sum_c Linv[r][c] t[c]
+        for (int r = warp; r < nb; r += 8) {
+          double s = 0.0;
+          for (int c = lane; c <= r; c += 32) s += Lq[r * TB + c] * t[c];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) t += red[q][lane];
-          part[lane] = t;
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) x[(size_t)(i0 + r) * w + j] = s;
         }
-      }
-      __syncthreads();
-      if (warp == 0) {
-        double xi = (lane < nb) ? x[(size_t)(i0 + lane) * w + j] - part[lane] : 0.0;
-        if (!trans) {
-          for (int c = 0; c < nb; ++c) {
-            double xc = __shfl_sync(0xffffffffu, xi / Ld[c][c], c);
-            if (lane == c) xi = xc;
-            else if (lane > c) xi -= Ld[lane][c] * xc;
-          }
-        } else {
-          for (int c = nb - 1; c >= 0; --c) {
-            double xc = __shfl_sync(0xffffffffu, xi / Ld[c][c], c);
-            if (lane == c) xi = xc;
-            else if (lane < c) xi -= Ld[c][lane] * xc;
-          }
+        __syncthreads();
+      } else {
+        // t[c] = x[i0+c] - sum_{r >= i0+nb} L[r][i0+c] x[r]  (warps split r, lanes own c)
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+        for (int r = i0 + nb + warp; r < n; r += 8) {
+          const double xv = x[(size_t)r * w + j];
+          const double* lrow = L + (size_t)r * ld + i0;
+          if (lane < nb) s0 += lrow[lane] * xv;
+          if (lane + 32 < nb) s1 += lrow[lane + 32] * xv;
         }
-        if (lane < nb) x[(size_t)(i0 + lane) * w + j] = xi;
+        red[warp][lane] = s0;
+        red[warp][lane + 32] = s1;
+        __syncthreads();
+        if (tid < nb) {
+          double v = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) v += red[qq][tid];
+          t[tid] = x[(size_t)(i0 + tid) * w + j] - v;
+        }
+        __syncthreads();
+        // x[i0+c] = sum_r Linv[r][c] t[r]   (r >= c)
+        double u0 = 0.0, u1 = 0.0;
+        for (int r = warp; r < nb; r += 8) {
+          const double tv = t[r];
+          if (lane <= r) u0 += Lq[r * TB + lane] * tv;
+          if (lane + 32 <= r) u1 += Lq[r * TB + lane + 32] * tv;
+        }
+        red[warp][lane] = u0;
+        red[warp][lane + 32] = u1;
+        __syncthreads();
+        if (tid < nb) {
+          double v = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) v += red[qq][tid];
+          x[(size_t)(i0 + tid) * w + j] = v;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
 }
 
 }  // namespace h2g
 
-extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms, int w,
-                                void* stream) {
-  if (n_outs <= 0) return H2G_OK;
+extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms, int total_chunks,
+                                int w, void* stream) {
+  if (n_outs <= 0 || total_chunks <= 0) return H2G_OK;
   if (!d_outs || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_gemv_grouped: bad argument");
-  static bool attr = false;
-  const int smem = h2g::GV_ROWS * h2g::GV_WMAX * 8;
-  if (!attr) {
-    cudaFuncSetAttribute(h2g::gemv_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  h2g::gemv_grouped_kernel<<<n_outs, h2g::GV_THREADS, smem, (cudaStream_t)stream>>>(d_outs, d_terms, w);
+  h2g::gemv_grouped_kernel<<<total_chunks, h2g::GV_THREADS, 0, (cudaStream_t)stream>>>(d_outs, n_outs, d_terms, w);
   return h2g_check_launch("gemv_grouped");
 }
 

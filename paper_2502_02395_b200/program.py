@@ -138,24 +138,29 @@ class Program:
             return 0
         oarr = np.zeros(len(outs), dtype=nat.GEMV_OUT_DT)
         tl = []
+        chunks = 0
+        nbytes = 0
         for q, (y, y2, init, m, split, flags, tms) in enumerate(outs):
-            oarr[q] = (y, y2, init, m, split, len(tl), len(tl) + len(tms), flags, 0)
+            oarr[q] = (y, y2, init, m, split, len(tl), len(tl) + len(tms), flags, chunks)
+            chunks += -(-int(m) // 256)
             tl.extend(tms)
+            nbytes += 8 * int(m) * sum(int(t[4]) for t in tms)
         tarr = np.zeros(max(len(tl), 1), dtype=nat.GEMV_TERM_DT)
         for q, (a, x, lda, trans, k) in enumerate(tl):
             tarr[q] = (a, x, lda, trans, k, 0)
-        self._add(nat.STEP["GEMV"], len(outs), w, self._blob(oarr), self._blob(tarr))
+        self._add(nat.STEP["GEMV"], len(outs), chunks, self._blob(oarr), self._blob(tarr), arg=w, nbytes=nbytes)
         return len(outs)
 
     def trsv(self, descs, trans, w):
-        """descs: list of (L, x, n, ldl)."""
-        descs = [d for d in descs if d[2] > 0]
+        """descs: list of (L, Linv, x, n, ldl)."""
+        descs = [d for d in descs if d[3] > 0]
         if not descs:
             return 0
         arr = np.zeros(len(descs), dtype=nat.TRSV_DT)
         for q, d in enumerate(descs):
             arr[q] = d
-        self._add(nat.STEP["TRSV"], len(descs), w, self._blob(arr), arg=trans)
+        nbytes = sum(4 * int(d[3]) * (int(d[3]) + 1) for d in descs)
+        self._add(nat.STEP["TRSV"], len(descs), w, self._blob(arr), arg=trans, nbytes=nbytes)
         return len(descs)
 
     def kblock(self, descs, points_ptr, family, shift, decay, flag_ptr):

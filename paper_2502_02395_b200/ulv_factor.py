@@ -139,7 +139,6 @@ class FactorPlan:
         prog.memcpy(self.npd.data_ptr(), self._npd_init.data_ptr(), 4 * (acc + 1))
         self.bufs = {}
         self.merge_pairs = {}
-        self._linv_keep = []
 
         if depth == 0:
             d = int(dh2.root_a.shape[0])
@@ -178,7 +177,7 @@ class FactorPlan:
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
                          int(n[i]), int(n[i]), int(n[i]), 0, 1.0, 0.0) for i in range(nb)]
                 prog.gemm(1, 0, prob)
-                self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l])
+                B.linv, B.loff = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l])
                 # ---- off-diagonal phase
                 offp = lay.off_pairs
                 B.toff, B.lsoff = {}, {}
@@ -226,11 +225,12 @@ class FactorPlan:
         TRSM as an in-place GEMM with L_pp^-T, TRAIL as a GEMM (lower tiles of H)."""
         nb = len(n)
         rmax = int(r.max()) if nb else 0
-        if rmax == 0:
-            return
         W = nat.PANEL_WIDTH
-        linv = torch.empty(nb * W * W, dtype=F64, device=self.device)
-        self._linv_keep.append(linv)
+        nblk = -(-np.asarray(r, dtype=np.int64) // W)
+        loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
+        linv = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=self.device)
+        if rmax == 0:
+            return linv, loff
         lp = linv.data_ptr()
         for p in range(0, rmax, W):
             descs, trsm, trail = [], [], []
@@ -240,7 +240,7 @@ class FactorPlan:
                     continue
                 b = min(W, ri - p)
                 h = Hp + 8 * int(qo[i])
-                li = lp + 8 * i * W * W
+                li = lp + 8 * (int(loff[i]) + p // W) * W * W
                 descs.append((h, li, ni, W, p, b, slot0 + i))
                 m = ni - p - b
                 pan = h + 8 * ((p + b) * ni + p)
@@ -257,10 +257,12 @@ class FactorPlan:
             prog.panel(descs, self.npd.data_ptr())
             prog.gemm(0, 1, trsm)
             prog.gemm(0, 1, trail)
+        return linv, loff
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
         assert d == ld
-        self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]), np.array([d]), slot)
+        self.root_linv, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]), np.array([d]),
+                                                         slot)
 
     def _merge_steps(self, prog, l, B, lists, dh2):
         lay = B.lay

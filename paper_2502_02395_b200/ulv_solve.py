@@ -99,6 +99,16 @@ class SolvePlan:
         B = self.fp.bufs[l]
         return B.H.data_ptr() + 8 * int(B.lay.qoff[i]), int(B.lay.n[i])
 
+    def _tr(self, l, i, x):
+        """TRSV descriptor (L, Linv, x, n, ld) of box i at level l (l = 0: root)."""
+        if l == 0:
+            d = self.fp.root_dim
+            return (self.fp.root_buf.data_ptr(), self.fp.root_linv.data_ptr(), x, d, d)
+        B = self.fp.bufs[l]
+        lay = B.lay
+        return (B.H.data_ptr() + 8 * int(lay.qoff[i]), B.linv.data_ptr() + 8 * int(B.loff[i]) * 4096, x,
+                int(lay.r[i]), int(lay.n[i]))
+
     # -------------------------------------------------------------- forward
     def _build_forward(self):
         fp, w = self.fp, self.w
@@ -107,7 +117,7 @@ class SolvePlan:
         if depth == 0:
             d = fp.root_dim
             prog.memcpy(self.yroot.data_ptr(), self.xin.data_ptr(), 8 * d * w)
-            prog.trsv([(fp.root_buf.data_ptr(), self.yroot.data_ptr(), d, d)], 0, w)
+            prog.trsv([self._tr(0, 0, self.yroot.data_ptr())], 0, w)
             return prog
         xin = self.xin
         for l in range(depth, 0, -1):
@@ -131,7 +141,7 @@ class SolvePlan:
             xin = V["BS"]
         d = fp.root_dim
         prog.memcpy(self.yroot.data_ptr(), xin.data_ptr(), 8 * d * w)
-        prog.trsv([(fp.root_buf.data_ptr(), self.yroot.data_ptr(), d, d)], 0, w)
+        prog.trsv([self._tr(0, 0, self.yroot.data_ptr())], 0, w)
         return prog
 
     def _forward_parallel_level(self, prog, l, V, lay, below):
@@ -141,7 +151,7 @@ class SolvePlan:
         B = self.fp.bufs[l]
         # P1  z_i = L_ii^-1 b_R,i
         prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
-        prog.trsv([(*self._L(l, i)[:1], self._p(V["Z"], offR[i]), int(r[i]), self._L(l, i)[1]) for i in range(nb)], 0, w)
+        prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb)], 0, w)
         # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j
         outs = []
         for i in range(nb):
@@ -150,7 +160,7 @@ class SolvePlan:
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
         prog.gemv(outs, w)
         # P3  y_i = L_ii^-1 t_i
-        prog.trsv([(self._L(l, i)[0], self._p(V["Y"], offR[i]), int(r[i]), self._L(l, i)[1]) for i in range(nb)], 0, w)
+        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in range(nb)], 0, w)
         # P4  b_S,a -= sum_b L(s)_ab y_b
         self._ls_update_forward(prog, l, V, lay)
 
@@ -175,8 +185,7 @@ class SolvePlan:
         _, above = _near_sets(lay)
         prog.memcpy(V["Y"].data_ptr(), V["BR"].data_ptr(), 8 * int(lay.r.sum()) * w)
         for i in range(lay.nb):
-            Lp, ld = self._L(l, i)
-            prog.trsv([(Lp, self._p(V["Y"], offR[i]), int(lay.r[i]), ld)], 0, w)
+            prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i]))], 0, w)
             outs = []
             for j in above[i]:
                 if lay.r[i] == 0 or lay.r[j] == 0:
@@ -194,7 +203,7 @@ class SolvePlan:
         depth = fp.depth
         d = fp.root_dim
         prog.memcpy(self.xroot.data_ptr(), self.yroot.data_ptr(), 8 * d * w)
-        prog.trsv([(fp.root_buf.data_ptr(), self.xroot.data_ptr(), d, d)], 1, w)
+        prog.trsv([self._tr(0, 0, self.xroot.data_ptr())], 1, w)
         xs = self.xroot
         for l in range(1, depth + 1):
             V = self.v[l]
@@ -213,16 +222,14 @@ class SolvePlan:
             if self.mode == "parallel":
                 _, above = _near_sets(lay)
                 prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
-                prog.trsv([(self._L(l, i)[0], self._p(V["Z2"], offR[i]), int(r[i]), self._L(l, i)[1])
-                           for i in range(nb)], 1, w)
+                prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb)], 1, w)
                 outs = []
                 for i in range(nb):
                     terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
                 prog.gemv(outs, w)
-                prog.trsv([(self._L(l, i)[0], self._p(V["XR"], offR[i]), int(r[i]), self._L(l, i)[1])
-                           for i in range(nb)], 1, w)
+                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in range(nb)], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
             # B3  full_i = q_red x_R + q_skel x_S
@@ -252,8 +259,7 @@ class SolvePlan:
                       int(lay.r[j])) for j in above[i] if lay.r[j] > 0]
             if terms:
                 prog.gemv([(self._p(V["XR"], offR[i]), 0, self._p(V["XR"], offR[i]), int(lay.r[i]), 0, 0, terms)], w)
-            Lp, ld = self._L(l, i)
-            prog.trsv([(Lp, self._p(V["XR"], offR[i]), int(lay.r[i]), ld)], 1, w)
+            prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i]))], 1, w)
 
     # -------------------------------------------------------------- run
     def run_forward(self, stream=None):
