@@ -1,17 +1,16 @@
 // Diagonal-block step of the batched partial (ULV) Cholesky.
 //
-// One CTA per box with r_i > p: D = H[p:p+b, p:p+b] (b <= 64) is factored in
-// shared memory and written back as L_pp, and W = L_pp^-1 is written to a
-// 64x64 scratch block.  Cholesky and inverse advance together, one column per
-// step and ONE barrier per step: in step j every thread owns one row i and a
-// quarter of its columns, and applies
-//     L[i][j] = D[i][j] / sqrt(d_jj)
-//     D[i][k] -= L[i][j] L[k][j]      (j < k <= i)   trailing update
-//     W[i][c] -= L[i][j] W[j][c]      (c <= j)       inverse, row elimination
-// using the still-unscaled column j / row j (scaled lazily after the
-// barrier, where nothing reads them any more).  All per-thread updates of a
-// step are independent, so they issue back to back (16-way unrolled).
-// A pivot that is not > 0 (or NaN) records atomicMin(npd[slot], p+j):
+// One CTA per box with r_i > p: D = H[p:p+b, p:p+b] (b <= 64, identity
+// padded to 64) is factored in shared memory, written back as L_pp, and
+// W = L_pp^-1 is written to a 64x64 scratch block (used by the TRSM GEMM and
+// later by the substitution).  The 64x64 factorization is blocked by 16:
+//   for each 16-column block K:
+//     warp 0   : unblocked Cholesky of the 16x16 diagonal block (warp-synchronous,
+//                no CTA barrier) and its 16x16 inverse
+//     all warps: TRSM of the rows below with that inverse, SYRK of the trailing part
+//   all warps  : block forward substitution W_IJ = -W_II sum_K L_IK W_KJ
+// so the serial chain is 4 x 16 cheap warp steps instead of 64 CTA-wide
+// steps.  A pivot that is not > 0 (or NaN) records atomicMin(npd[slot], p+j):
 // dpotrf's info-1 (dense_core.py:60-63).
 //
 // The rest of the panel step is tensor-pipe GEMM work issued by the host
@@ -25,20 +24,21 @@ namespace h2g {
 
 constexpr int PB = 64;        // max panel width
 constexpr int PS = PB + 1;    // odd stride: conflict-free row and column walks
+constexpr int SB = 16;        // inner block
 constexpr int DIAG_THREADS = 256;
 
 __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
                                                                   int32_t* __restrict__ npd) {
   extern __shared__ double dsm[];
   double* Ds = dsm;              // D, becomes L (lower)
-  double* Ws = dsm + PB * PS;    // W, becomes L^-1 (lower)
+  double* Ws = dsm + PB * PS;    // becomes L^-1 (lower)
+  __shared__ double Xt[48 * SB];  // TRSM results staging
   const h2g_panel_desc P = descs[blockIdx.x];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = P.p, b = P.b;
   double* H = P.H;
   const int ldh = P.ldh;
 
-  // load D (lower, identity padded) and W = I; 16 independent loads per thread
 #pragma unroll
   for (int t = 0; t < (PB * PB) / DIAG_THREADS; ++t) {
     const int e = tid + t * DIAG_THREADS;
@@ -47,34 +47,96 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
     if (r < b && c < b) v = (c <= r) ? H[(size_t)(p + r) * ldh + p + c] : 0.0;
     else v = (r == c) ? 1.0 : 0.0;
     Ds[r * PS + c] = v;
-    Ws[r * PS + c] = (r == c) ? 1.0 : 0.0;
+    Ws[r * PS + c] = 0.0;
   }
   __syncthreads();
 
-  const int i = tid >> 2, cq = tid & 3;
-  for (int j = 0; j < PB; ++j) {
-    const double djj = Ds[j * PS + j];
-    const double rinv = 1.0 / sqrt(djj);
-    if (i > j) {
-      const double lij = Ds[i * PS + j] * rinv;
-#pragma unroll
-      for (int t = 0; t < PB / 4; ++t) {
-        const int c = cq + 4 * t;
-        if (c <= j) {
-          Ws[i * PS + c] -= lij * (Ws[j * PS + c] * rinv);
-        } else if (c <= i) {
-          Ds[i * PS + c] -= lij * (Ds[c * PS + j] * rinv);
+  for (int kb = 0; kb < PB; kb += SB) {
+    // ---- (a) warp 0: 16x16 Cholesky + inverse of the diagonal block
+    if (warp == 0) {
+      double* Dk = Ds + kb * PS + kb;
+      for (int j = 0; j < SB; ++j) {
+        const double djj = Dk[j * PS + j];
+        const double rinv = 1.0 / sqrt(djj);
+        if (lane == 0 && !(djj > 0.0) && kb + j < b) atomicMin(&npd[P.npd_slot], p + kb + j);
+        // trailing update inside the block with the unscaled column j
+        for (int e = lane; e < SB * SB; e += 32) {
+          const int i = e >> 4, k = e & 15;
+          if (k > j && k <= i) Dk[i * PS + k] -= Dk[i * PS + j] * Dk[k * PS + j] * (rinv * rinv);
+        }
+        __syncwarp();
+        if (lane > j && lane < SB) Dk[lane * PS + j] *= rinv;
+        if (lane == j) Dk[j * PS + j] = djj * rinv;
+        __syncwarp();
+      }
+      // inverse of the 16x16 lower block: lane c < 16 solves column c
+      if (lane < SB) {
+        const int c = lane;
+        double* Wk = Ws + kb * PS + kb;
+        for (int i = 0; i < SB; ++i) {
+          double s = (i == c) ? 1.0 : 0.0;
+          for (int m = c; m < i; ++m) s -= Dk[i * PS + m] * Wk[m * PS + c];
+          Wk[i * PS + c] = (i >= c) ? s / Dk[i * PS + i] : 0.0;
         }
       }
     }
     __syncthreads();
-    // finalize column j of L and row j of W (no thread reads them in step j+1)
-    if (tid == 0 && !(djj > 0.0) && j < b) atomicMin(&npd[P.npd_slot], p + j);
-    if (tid > j && tid < PB) Ds[tid * PS + j] *= rinv;
-    if (tid == j) Ds[j * PS + j] = djj * rinv;   // sqrt(djj)
-    if (tid >= PB && tid - PB <= j) Ws[j * PS + (tid - PB)] *= rinv;
+    const int below = PB - kb - SB;  // rows under the block
+    if (below > 0) {
+      // ---- (b) TRSM: X[r][c] = sum_{m<=c} D[kb+16+r][kb+m] * W_kk[c][m]
+      for (int e = tid; e < below * SB; e += DIAG_THREADS) {
+        const int r = e >> 4, c = e & 15;
+        const double* xr = Ds + (kb + SB + r) * PS + kb;
+        const double* wc = Ws + (kb + c) * PS + kb;
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < SB; ++m)
+          if (m <= c) s += xr[m] * wc[m];
+        Xt[r * SB + c] = s;
+      }
+      __syncthreads();
+      for (int e = tid; e < below * SB; e += DIAG_THREADS) {
+        const int r = e >> 4, c = e & 15;
+        Ds[(kb + SB + r) * PS + kb + c] = Xt[r * SB + c];
+      }
+      // ---- (c) SYRK: D[i][k] -= sum_m X[i][m] X[k][m]   (kb+16 <= k <= i)
+      for (int e = tid; e < below * below; e += DIAG_THREADS) {
+        const int ii = e / below, kk = e % below;
+        if (kk > ii) continue;
+        const double* xi = Xt + ii * SB;
+        const double* xk = Xt + kk * SB;
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < SB; ++m) s += xi[m] * xk[m];
+        Ds[(kb + SB + ii) * PS + kb + SB + kk] -= s;
+      }
+      __syncthreads();
+    }
   }
-  __syncthreads();
+
+  // ---- block forward substitution for the off-diagonal blocks of W = L^-1
+  for (int I = 1; I < PB / SB; ++I) {
+    // T_J[r][c] = sum_{K=J}^{I-1} L[I][K] W[K][J]  for J < I  (into Xt, I*256 <= 768 entries)
+    for (int e = tid; e < I * SB * SB; e += DIAG_THREADS) {
+      const int J = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const double* lrow = Ds + (I * SB + r) * PS;
+      double s = 0.0;
+      for (int m = J * SB + c; m < I * SB; ++m) s += lrow[m] * Ws[m * PS + J * SB + c];
+      Xt[e] = s;
+    }
+    __syncthreads();
+    // W[I][J] = -W_II T_J
+    for (int e = tid; e < I * SB * SB; e += DIAG_THREADS) {
+      const int J = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const double* wrow = Ws + (I * SB + r) * PS + I * SB;
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < SB; ++m)
+        if (m <= r) s += wrow[m] * Xt[(J << 8) + (m << 4) + c];
+      Ws[(I * SB + r) * PS + J * SB + c] = -s;
+    }
+    __syncthreads();
+  }
 
   double* __restrict__ out = P.Linv;  // 64 x 64 scratch, ld = ldl
 #pragma unroll
