@@ -1,151 +1,152 @@
 // Diagonal-block step of the batched partial (ULV) Cholesky.
 //
 // One CTA per box with r_i > p: D = H[p:p+b, p:p+b] (b <= 64, identity
-// padded to 64) is factored in shared memory, written back as L_pp, and
-// W = L_pp^-1 is written to a 64x64 scratch block (used by the TRSM GEMM and
-// later by the substitution).  The 64x64 factorization is blocked by 16:
-//   for each 16-column block K:
-//     warp 0   : unblocked Cholesky of the 16x16 diagonal block (warp-synchronous,
-//                no CTA barrier) and its 16x16 inverse
-//     all warps: TRSM of the rows below with that inverse, SYRK of the trailing part
-//   all warps  : block forward substitution W_IJ = -W_II sum_K L_IK W_KJ
-// so the serial chain is 4 x 16 cheap warp steps instead of 64 CTA-wide
-// steps.  A pivot that is not > 0 (or NaN) records atomicMin(npd[slot], p+j):
-// dpotrf's info-1 (dense_core.py:60-63).
+// padded to 64) is factored and written back as L_pp, and W = L_pp^-1 is
+// written to a 64x64 scratch block (used by the TRSM GEMM and later by the
+// substitution).
+//
+// Latency is what matters here (one small block per box, all boxes in one
+// wave), so the factorization is a square-root-free LDL^T elimination with
+// the 64x64 matrix distributed over the CTA in 2x2 register blocks (thread
+// (br, bc) owns rows 2br.., columns 2bc..): in step j every thread updates
+// its 4 entries with the pivot column j and the finished row j of
+// V = U^-1 (U unit lower), then the owners of column j+1 / row j+1 publish
+// them to shared memory and ONE barrier ends the step.  No entry moves
+// between threads; the chain per step is barrier + 1 broadcast load + one
+// reciprocal + one FMA.  At the end L = U diag(sqrt d), L^-1 = diag(1/sqrt d) V.
+// A pivot that is not > 0 (or NaN) records atomicMin(npd[slot], p+j): the
+// pivot dpotrf reports as info-1 (dense_core.py:60-63).
 //
 // The rest of the panel step is tensor-pipe GEMM work issued by the host
 // program (ulv_factor.FactorPlan): TRSM X <- X Linv^T in place for the rows
 // below the panel of H and for the q_red rows of R, then the trailing update.
 // Over all panels: L(r)_ii = chol(RR), L(s)_ii = SR L^-T, V_i = q_red L^-T and
 // SS_ii - L(s) L(s)^T (ulv_factor.py:217-241).
+#include <climits>
+
 #include "common.cuh"
 
 namespace h2g {
 
 constexpr int PB = 64;        // max panel width
-constexpr int PS = PB + 1;    // odd stride: conflict-free row and column walks
-constexpr int SB = 16;        // inner block
-constexpr int DIAG_THREADS = 256;
+constexpr int BS = 2;                 // register block per thread
+constexpr int NBLK = (PB / BS) * (PB / BS + 1) / 2;   // 528 lower blocks
+constexpr int DIAG_THREADS = 544;
+
+#ifdef H2G_DIAG_TRACE
+__device__ long long g_diag_trace[64];
+#define TRACE(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_diag_trace[k] = clock64(); } while (0)
+#else
+#define TRACE(k) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
                                                                   int32_t* __restrict__ npd) {
-  extern __shared__ double dsm[];
-  double* Ds = dsm;              // D, becomes L (lower)
-  double* Ws = dsm + PB * PS;    // becomes L^-1 (lower)
-  __shared__ double Xt[48 * SB];  // TRSM results staging
+  __shared__ __align__(16) double colD[2][PB];   // pivot column j (double buffered)
+  __shared__ __align__(16) double rowV[2][PB];   // finished row j of V = U^-1
+  __shared__ double dg[PB];                      // pivots d_j
   const h2g_panel_desc P = descs[blockIdx.x];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  // the NBLK lower BSxBS blocks are enumerated row by row over threads 0..NBLK-1
+  int br = (int)((sqrtf(8.0f * tid + 1.0f) - 1.0f) * 0.5f);
+  while ((br + 1) * (br + 2) / 2 <= tid) ++br;
+  while (br * (br + 1) / 2 > tid) --br;
+  const int bc = tid - br * (br + 1) / 2;
+  const bool active = tid < NBLK;
+  const int r0 = BS * br, c0 = BS * bc;
   const int p = P.p, b = P.b;
   double* H = P.H;
   const int ldh = P.ldh;
+  TRACE(0);
 
+  double d[BS][BS], v[BS][BS];
 #pragma unroll
-  for (int t = 0; t < (PB * PB) / DIAG_THREADS; ++t) {
-    const int e = tid + t * DIAG_THREADS;
-    const int r = e >> 6, c = e & 63;
-    double v;
-    if (r < b && c < b) v = (c <= r) ? H[(size_t)(p + r) * ldh + p + c] : 0.0;
-    else v = (r == c) ? 1.0 : 0.0;
-    Ds[r * PS + c] = v;
-    Ws[r * PS + c] = 0.0;
+  for (int a = 0; a < BS; ++a)
+#pragma unroll
+    for (int e = 0; e < BS; ++e) {
+      const int i = r0 + a, x = c0 + e;
+      double val = 0.0;
+      if (active && x <= i) {
+        if (i < b && x < b) val = H[(size_t)(p + i) * ldh + p + x];
+        else val = (i == x) ? 1.0 : 0.0;
+      }
+      d[a][e] = val;
+      v[a][e] = (i == x) ? 1.0 : 0.0;
+    }
+  if (active && bc == 0) {
+#pragma unroll
+    for (int a = 0; a < BS; ++a) colD[0][r0 + a] = d[a][0];
   }
+  if (tid < PB) rowV[0][tid] = (tid == 0) ? 1.0 : 0.0;
   __syncthreads();
+  TRACE(1);
 
-  for (int kb = 0; kb < PB; kb += SB) {
-    // ---- (a) warp 0: 16x16 Cholesky + inverse of the diagonal block
-    if (warp == 0) {
-      double* Dk = Ds + kb * PS + kb;
-      for (int j = 0; j < SB; ++j) {
-        const double djj = Dk[j * PS + j];
-        const double rinv = 1.0 / sqrt(djj);
-        if (lane == 0 && !(djj > 0.0) && kb + j < b) atomicMin(&npd[P.npd_slot], p + kb + j);
-        // trailing update inside the block with the unscaled column j
-        for (int e = lane; e < SB * SB; e += 32) {
-          const int i = e >> 4, k = e & 15;
-          if (k > j && k <= i) Dk[i * PS + k] -= Dk[i * PS + j] * Dk[k * PS + j] * (rinv * rinv);
-        }
-        __syncwarp();
-        if (lane > j && lane < SB) Dk[lane * PS + j] *= rinv;
-        if (lane == j) Dk[j * PS + j] = djj * rinv;
-        __syncwarp();
-      }
-      // inverse of the 16x16 lower block: lane c < 16 solves column c
-      if (lane < SB) {
-        const int c = lane;
-        double* Wk = Ws + kb * PS + kb;
-        for (int i = 0; i < SB; ++i) {
-          double s = (i == c) ? 1.0 : 0.0;
-          for (int m = c; m < i; ++m) s -= Dk[i * PS + m] * Wk[m * PS + c];
-          Wk[i * PS + c] = (i >= c) ? s / Dk[i * PS + i] : 0.0;
-        }
-      }
+  int bad = INT_MAX;
+#pragma unroll 1
+  for (int j = 0; j < PB; ++j) {
+    const int cur = j & 1, nxt = cur ^ 1;
+    const double dj = colD[cur][j];
+    if (tid == 0) {
+      dg[j] = dj;
+      if (!(dj > 0.0) && j < b && bad == INT_MAX) bad = j;
     }
-    __syncthreads();
-    const int below = PB - kb - SB;  // rows under the block
-    if (below > 0) {
-      // ---- (b) TRSM: X[r][c] = sum_{m<=c} D[kb+16+r][kb+m] * W_kk[c][m]
-      for (int e = tid; e < below * SB; e += DIAG_THREADS) {
-        const int r = e >> 4, c = e & 15;
-        const double* xr = Ds + (kb + SB + r) * PS + kb;
-        const double* wc = Ws + (kb + c) * PS + kb;
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < SB; ++m)
-          if (m <= c) s += xr[m] * wc[m];
-        Xt[r * SB + c] = s;
-      }
-      __syncthreads();
-      for (int e = tid; e < below * SB; e += DIAG_THREADS) {
-        const int r = e >> 4, c = e & 15;
-        Ds[(kb + SB + r) * PS + kb + c] = Xt[r * SB + c];
-      }
-      // ---- (c) SYRK: D[i][k] -= sum_m X[i][m] X[k][m]   (kb+16 <= k <= i)
-      for (int e = tid; e < below * below; e += DIAG_THREADS) {
-        const int ii = e / below, kk = e % below;
-        if (kk > ii) continue;
-        const double* xi = Xt + ii * SB;
-        const double* xk = Xt + kk * SB;
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < SB; ++m) s += xi[m] * xk[m];
-        Ds[(kb + SB + ii) * PS + kb + SB + kk] -= s;
-      }
-      __syncthreads();
+    if (active && r0 + BS - 1 > j) {
+      const double rj = 1.0 / dj;
+      // rows > j take the multiplier; columns > j update D, columns <= j update V
+      const double2 cr = reinterpret_cast<const double2*>(colD[cur])[br];
+      const double2 cc = reinterpret_cast<const double2*>(colD[cur])[bc];
+      const double2 rv = reinterpret_cast<const double2*>(rowV[cur])[bc];
+      const double li0 = (r0 > j) ? cr.x * rj : 0.0;
+      const double li1 = cr.y * rj;                       // row r0+1 > j here
+      const bool rt0 = c0 > j, rt1 = c0 + 1 > j;
+      const double lx0 = rt0 ? cc.x : 0.0, lx1 = rt1 ? cc.y : 0.0;
+      const double vx0 = rt0 ? 0.0 : rv.x, vx1 = rt1 ? 0.0 : rv.y;
+      d[0][0] = fma(-li0, lx0, d[0][0]);
+      d[0][1] = fma(-li0, lx1, d[0][1]);
+      d[1][0] = fma(-li1, lx0, d[1][0]);
+      d[1][1] = fma(-li1, lx1, d[1][1]);
+      v[0][0] = fma(-li0, vx0, v[0][0]);
+      v[0][1] = fma(-li0, vx1, v[0][1]);
+      v[1][0] = fma(-li1, vx0, v[1][0]);
+      v[1][1] = fma(-li1, vx1, v[1][1]);
     }
-  }
-
-  // ---- block forward substitution for the off-diagonal blocks of W = L^-1
-  for (int I = 1; I < PB / SB; ++I) {
-    // T_J[r][c] = sum_{K=J}^{I-1} L[I][K] W[K][J]  for J < I  (into Xt, I*256 <= 768 entries)
-    for (int e = tid; e < I * SB * SB; e += DIAG_THREADS) {
-      const int J = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const double* lrow = Ds + (I * SB + r) * PS;
-      double s = 0.0;
-      for (int m = J * SB + c; m < I * SB; ++m) s += lrow[m] * Ws[m * PS + J * SB + c];
-      Xt[e] = s;
+    // publish column j+1 of D and row j+1 of V (both final after this step)
+    const int jn = j + 1;
+    if (active && (jn >> 1) == bc && jn < PB) {
+      const bool hi = jn & 1;
+      if (r0 >= jn) colD[nxt][r0] = hi ? d[0][1] : d[0][0];
+      if (r0 + 1 >= jn) colD[nxt][r0 + 1] = hi ? d[1][1] : d[1][0];
     }
-    __syncthreads();
-    // W[I][J] = -W_II T_J
-    for (int e = tid; e < I * SB * SB; e += DIAG_THREADS) {
-      const int J = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const double* wrow = Ws + (I * SB + r) * PS + I * SB;
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < SB; ++m)
-        if (m <= r) s += wrow[m] * Xt[(J << 8) + (m << 4) + c];
-      Ws[(I * SB + r) * PS + J * SB + c] = -s;
+    if (active && (jn >> 1) == br && jn < PB) {
+      const bool hi = jn & 1;
+      const double w0 = hi ? v[1][0] : v[0][0], w1 = hi ? v[1][1] : v[0][1];
+      rowV[nxt][c0] = (c0 <= jn) ? w0 : 0.0;
+      rowV[nxt][c0 + 1] = (c0 + 1 <= jn) ? w1 : 0.0;
     }
     __syncthreads();
   }
+  TRACE(2);
+  if (tid == 0 && bad != INT_MAX) atomicMin(&npd[P.npd_slot], p + bad);
 
+  // L[i][x] = D[i][x] / sqrt(d_x) (x < i), L[x][x] = sqrt(d_x);  Linv[i][x] = V[i][x] / sqrt(d_i)
   double* __restrict__ out = P.Linv;  // 64 x 64 scratch, ld = ldl
+  if (active) {
 #pragma unroll
-  for (int t = 0; t < (PB * PB) / DIAG_THREADS; ++t) {
-    const int e = tid + t * DIAG_THREADS;
-    const int r = e >> 6, c = e & 63;
-    out[(size_t)r * P.ldl + c] = (r < b && c < b && c <= r) ? Ws[r * PS + c] : 0.0;
-    if (r < b && c <= r) H[(size_t)(p + r) * ldh + p + c] = Ds[r * PS + c];
+    for (int a = 0; a < BS; ++a)
+#pragma unroll
+      for (int e = 0; e < BS; ++e) {
+        const int i = r0 + a, x = c0 + e;
+        double wv = 0.0;
+        if (x <= i && i < b) {
+          const double sx = sqrt(dg[x]);
+          wv = v[a][e] / sqrt(dg[i]);
+          H[(size_t)(p + i) * ldh + p + x] = (x == i) ? sx : d[a][e] / sx;
+        }
+        out[(size_t)i * P.ldl + x] = wv;
+        if (bc < br) out[(size_t)x * P.ldl + i] = 0.0;   // mirror block above the diagonal
+      }
   }
+  TRACE(3);
 }
 
 }  // namespace h2g
@@ -153,12 +154,6 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
 extern "C" int h2g_panel_potrf(const h2g_panel_desc* d_descs, int count, int32_t* d_npd, void* stream) {
   if (count <= 0) return H2G_OK;
   if (!d_descs || !d_npd) return h2g_set_error(H2G_EINVAL, "h2g_panel_potrf: null argument");
-  const int smem = 2 * h2g::PB * h2g::PS * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(h2g::potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  h2g::potrf_diag_kernel<<<count, h2g::DIAG_THREADS, smem, (cudaStream_t)stream>>>(d_descs, d_npd);
+  h2g::potrf_diag_kernel<<<count, h2g::DIAG_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_npd);
   return h2g_check_launch("potrf_diag");
 }
