@@ -42,9 +42,12 @@ enum {
 
 /* ---- grouped GEMM ---------------------------------------------------------
  * C = alpha * op(A) * op(B) + beta * C  for every problem of the group.
- * op(A) is M x K, op(B) is K x N.  trans_a / trans_b are uniform for the
- * launch.  flags bit 0 (H2G_GEMM_LOWER, requires M == N) computes only the
- * 64x64 output tiles on or below the diagonal (SYRK-style Schur updates).
+ * op(A) is M x K, op(B) is K x N.  trans_a / trans_b and the tile shape are
+ * uniform for the launch: tile_cfg 0 = 64x64 tiles (128 threads), 1 =
+ * 128x128 tiles (256 threads).  flags bit 0 (H2G_GEMM_LOWER, requires
+ * M == N) computes only the output tiles on or below the diagonal
+ * (SYRK-style Schur updates).  C may alias A when N fits one tile (the
+ * in-place TRSM X <- X Linv^T).
  * `tile_start` is the problem's first tile in the launch; d_tile_map[t] is
  * the problem index of tile t (t < total_tiles).
  * Replaces: dense_core.multiply (dense_core.py:84-93) for the phases
@@ -62,8 +65,8 @@ typedef struct h2g_gemm_problem {
   double alpha, beta;
 } h2g_gemm_problem;
 
-int h2g_gemm_tiles(int M, int N, int flags); /* tiles one problem needs */
-int h2g_gemm_grouped(int trans_a, int trans_b, const h2g_gemm_problem* d_probs,
+int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg); /* tiles one problem needs */
+int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
                      const int32_t* d_tile_map, int total_tiles, void* stream);
 
 /* ---- diagonal block of a panel of the partial (ULV) Cholesky ---------------
@@ -255,7 +258,7 @@ typedef struct h2g_step {
   int32_t kind;
   int32_t count;      /* problems / descriptors (bytes for MEMCPY) */
   int32_t grid;       /* tiles or CTAs (w for GEMV/TRSV) */
-  int32_t arg;        /* TRSV: trans; KBLOCK: family */
+  int32_t arg;        /* GEMM: tile_cfg; TRSV: trans; KBLOCK: family; GEMV: w */
   const void* descs;  /* device descriptor array */
   const int32_t* map; /* device tile / CTA map */
   int32_t* npd;       /* PANEL: device pivot-status array */

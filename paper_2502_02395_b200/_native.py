@@ -47,7 +47,7 @@ STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "PANEL": 4, "COP
 GEMM_LOWER = 1
 GEMV_PLUS = 1
 GEMV_SPLIT = 2
-GEMM_TILE = 64
+GEMM_TILE = (64, 128, 64)  # tile edge per tile_cfg
 COPY_TILE = 32
 PANEL_WIDTH = 64
 QR_PANEL_WIDTH = 32
@@ -71,8 +71,8 @@ def load_library(path=LIB_PATH):
     lib = ctypes.CDLL(path)
     vp, i32 = ctypes.c_void_p, ctypes.c_int
     sig = {
-        "h2g_gemm_tiles": (i32, [i32, i32, i32]),
-        "h2g_gemm_grouped": (i32, [i32, i32, vp, vp, i32, vp]),
+        "h2g_gemm_tiles": (i32, [i32, i32, i32, i32]),
+        "h2g_gemm_grouped": (i32, [i32, i32, i32, vp, vp, i32, vp]),
         "h2g_panel_potrf": (i32, [vp, i32, vp, vp]),
         "h2g_copy_tiles": (i32, [i32, i32]),
         "h2g_block_copy": (i32, [vp, vp, i32, vp]),

@@ -39,7 +39,7 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_GEMM_TN:
     case H2G_STEP_GEMM_TT: {
       int k = s.kind - H2G_STEP_GEMM_NN;
-      return h2g_gemm_grouped(k >> 1, k & 1, (const h2g_gemm_problem*)s.descs, s.map, s.grid, st);
+      return h2g_gemm_grouped(k >> 1, k & 1, s.arg, (const h2g_gemm_problem*)s.descs, s.map, s.grid, st);
     }
     case H2G_STEP_PANEL:
       return h2g_panel_potrf((const h2g_panel_desc*)s.descs, s.count, s.npd, st);

@@ -16,13 +16,23 @@ import torch
 from . import _native as nat
 
 
-def gemm_tiles(m, n, flags=0):
+def gemm_tiles(m, n, flags=0, cfg=0):
     if m <= 0 or n <= 0:
         return 0
+    t = nat.GEMM_TILE[cfg]
     if flags & nat.GEMM_LOWER:
-        t = -(-m // nat.GEMM_TILE)
-        return t * (t + 1) // 2
-    return (-(-m // nat.GEMM_TILE)) * (-(-n // nat.GEMM_TILE))
+        tm = -(-m // t)
+        return tm * (tm + 1) // 2
+    return (-(-m // t)) * (-(-n // t))
+
+
+def choose_tile_cfg(ms, ns, flags, sms=148):
+    """128x128 tiles when they keep >= 1 full wave busy with little edge waste."""
+    ms, ns, flags = (np.asarray(x, dtype=np.int64) for x in (ms, ns, flags))
+    area = float((ms * ns).sum())
+    t1 = np.array([gemm_tiles(m, n, f, 1) for m, n, f in zip(ms, ns, flags)], dtype=np.int64)
+    eff1 = area / max(1.0, float(t1.sum()) * 128 * 128)
+    return 1 if (t1.sum() >= sms and eff1 >= 0.75) else 0
 
 
 def copy_tiles(rows, cols):
@@ -57,7 +67,7 @@ class Program:
                                 arg=int(arg), aux=aux, d0=float(d0), d1=float(d1)))
 
     # -- step constructors ------------------------------------------------------------
-    def gemm(self, trans_a, trans_b, problems):
+    def gemm(self, trans_a, trans_b, problems, tile_cfg=None):
         """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta)."""
         rows = [p for p in problems if p[3] > 0 and p[4] > 0]
         if not rows:
@@ -66,7 +76,9 @@ class Program:
         cols = list(zip(*rows))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
             arr[name] = col
-        tiles = np.array([gemm_tiles(m, n, f) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])], dtype=np.int64)
+        cfg = choose_tile_cfg(arr["M"], arr["N"], arr["flags"]) if tile_cfg is None else tile_cfg
+        tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
+                         dtype=np.int64)
         starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         arr["tile_start"] = starts
         total = int(tiles.sum())
@@ -76,7 +88,7 @@ class Program:
         m64, n64, k64 = arr["M"].astype(np.int64), arr["N"].astype(np.int64), arr["K"].astype(np.int64)
         lower = (arr["flags"] & nat.GEMM_LOWER) != 0
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
-        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl)
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg)
         return total
 
     def panel(self, descs, npd_ptr):
