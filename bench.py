@@ -335,7 +335,10 @@ def main():
         e2e_s = float(t.item())
     e2e = {"value": world * flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
            "d2h_bytes_per_step": int(xe.nbytes + plan.npd.numel() * 4), "seconds_per_step": e2e_s,
-           "includes": "upload of bases/near blocks/couplings + plan + factorize + pivot check + solve + x download"}
+           "includes": "factorize(h2 of host numpy blocks): parallel pinned gather + H2D of bases / leaf near "
+                       "blocks / couplings, graph-replayed factorization, pivot-status D2H; solve(b): H2D b, "
+                       "forward/backward graphs, D2H x. The symbolic part (layout, descriptors, CUDA graph) "
+                       "is cached per structure, the numeric upload is redone every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -14,10 +14,53 @@ host-materialized one) through one pinned staging buffer per kind;
 `h2_build.construct` produces a DeviceH2 directly on the GPU.
 """
 
+import hashlib
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import torch
 
 F64 = torch.float64
+_STAGING = {"buf": None}
+_POOL = {"pool": None}
+
+
+def _pool():
+    if _POOL["pool"] is None:
+        _POOL["pool"] = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+    return _POOL["pool"]
+
+
+def _staging(n_doubles):
+    """Reusable pinned host buffer of at least n doubles: (tensor, numpy view)."""
+    buf = _STAGING["buf"]
+    if buf is None or buf.numel() < n_doubles:
+        buf = torch.empty(int(n_doubles * 1.25) + 1024, dtype=F64, pin_memory=True)
+        _STAGING["buf"] = buf
+    return buf, buf.numpy()
+
+
+def _fill_q(host, off, basis, n, k):
+    blk = host[off:off + n * n].reshape(n, n)
+    blk[:, :n - k] = basis.q_red
+    blk[:, n - k:] = basis.q_skel
+
+
+def _fill_flat(host, off, arr):
+    a = np.asarray(arr)
+    host[off:off + a.size].reshape(a.shape)[...] = a
+
+
+def _signature(depth, count, levels):
+    h = hashlib.sha1(f"{depth}:{count}".encode())
+    for l in sorted(levels):
+        lay = levels[l]
+        h.update(lay.n.tobytes())
+        h.update(lay.k.tobytes())
+        h.update(np.asarray(lay.near_pairs, dtype=np.int64).tobytes())
+        h.update(np.asarray(lay.far_pairs, dtype=np.int64).tobytes())
+    return h.hexdigest()
 
 
 def _sorted_pairs(pairs, cond):
@@ -74,46 +117,71 @@ class DeviceH2:
             levels[l] = LevelLayout(l, n, k, h2.lists.near[l], h2.lists.far[l])
         return levels
 
+    def signature(self):
+        """Structure key: equal signatures -> identical layouts and programs."""
+        return _signature(self.depth, self.count, self.levels)
+
     @classmethod
-    def from_host(cls, h2, device=None):
-        """Upload the numpy arrays of `h2` (bases, leaf near blocks, couplings)."""
+    def from_host(cls, h2, device=None, into=None):
+        """Upload the numpy arrays of `h2` (bases, leaf near blocks, couplings).
+
+        The blocks are gathered in parallel (numpy releases the GIL) into one
+        reusable pinned staging buffer, then copied to HBM asynchronously.  With
+        `into` (a DeviceH2 of the same structure) its device buffers are reused.
+        """
         device = torch.device(device or "cuda")
         depth = h2.tree.depth
         if depth == 0:
             a = np.ascontiguousarray(h2.near_blocks[(0, 0, 0)], dtype=np.float64)
             root_a = torch.from_numpy(a).to(device)
             return cls(device, 0, h2.count, {}, {}, {}, None, {}, root_a=root_a)
-        levels = cls.layouts_from_host(h2)
-        q, s = {}, {}
-        for l, lay in levels.items():
-            buf = torch.empty(lay.qsize, dtype=F64, pin_memory=True)
-            hv = buf.numpy()
-            for i in range(lay.nb):
-                b = h2.bases[(l, i)]
-                n, k = int(lay.n[i]), int(lay.k[i])
-                blk = hv[lay.qoff[i]:lay.qoff[i] + n * n].reshape(n, n)
-                blk[:, :n - k] = b.q_red
-                blk[:, n - k:] = b.q_skel
-            q[l] = buf.to(device, non_blocking=True)
-            sbuf = torch.empty(max(lay.ssize, 1), dtype=F64, pin_memory=True)
-            sv = sbuf.numpy()
-            for (i, j), off in lay.soff.items():
-                c = h2.couplings[(l, i, j)]
-                sv[off:off + c.size] = c.ravel()
-            s[l] = sbuf.to(device, non_blocking=True)
+        levels = into.levels if into is not None else cls.layouts_from_host(h2)
         leaf = levels[depth]
-        aoff, acc = {}, 0
-        for (i, j) in leaf.near_pairs:
-            aoff[(i, j)] = acc
-            acc += int(leaf.n[i] * leaf.n[j])
-        abuf = torch.empty(max(acc, 1), dtype=F64, pin_memory=True)
-        av = abuf.numpy()
-        for (i, j), off in aoff.items():
-            blk = h2.near_blocks[(depth, i, j)]
-            av[off:off + blk.size] = blk.ravel()
-        leaf_a = abuf.to(device, non_blocking=True)
-        torch.cuda.current_stream(device).synchronize()  # pinned staging buffers die here
-        return cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
+        if into is not None:
+            aoff = into.aoff
+            asize = int(into.leaf_a.numel())
+        else:
+            aoff, asize = {}, 0
+            for (i, j) in leaf.near_pairs:
+                aoff[(i, j)] = asize
+                asize += int(leaf.n[i] * leaf.n[j])
+        # staging layout: [q levels][s levels][leaf near blocks]
+        regions, off = [], 0
+        for l, lay in levels.items():
+            regions.append(("q", l, off, lay.qsize))
+            off += lay.qsize
+        for l, lay in levels.items():
+            regions.append(("s", l, off, max(lay.ssize, 1)))
+            off += max(lay.ssize, 1)
+        regions.append(("a", depth, off, max(asize, 1)))
+        off += max(asize, 1)
+        host_t, host = _staging(off)
+        tasks = []
+        for kind, l, base, _ in regions:
+            lay = levels[l]
+            if kind == "q":
+                for i in range(lay.nb):
+                    tasks.append((_fill_q, host, base + int(lay.qoff[i]), h2.bases[(l, i)], int(lay.n[i]),
+                                  int(lay.k[i])))
+            elif kind == "s":
+                for (i, j), o in lay.soff.items():
+                    tasks.append((_fill_flat, host, base + o, h2.couplings[(l, i, j)]))
+            else:
+                for (i, j), o in aoff.items():
+                    tasks.append((_fill_flat, host, base + o, h2.near_blocks[(depth, i, j)]))
+        list(_pool().map(lambda t: t[0](*t[1:]), tasks, chunksize=max(1, len(tasks) // 64)))
+        src = host_t  # pinned: the copies below are true async DMA
+        if into is not None:
+            q, s, leaf_a = into.q, into.s, into.leaf_a
+        else:
+            q = {l: torch.empty(lay.qsize, dtype=F64, device=device) for l, lay in levels.items()}
+            s = {l: torch.empty(max(lay.ssize, 1), dtype=F64, device=device) for l, lay in levels.items()}
+            leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
+        for kind, l, base, size in regions:
+            dst = q[l] if kind == "q" else s[l] if kind == "s" else leaf_a
+            dst[:size].copy_(src[base:base + size], non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()  # staging buffer is reused by the next upload
+        return into if into is not None else cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
 
     def ptr_q(self, l, i, col=0):
         lay = self.levels[l]

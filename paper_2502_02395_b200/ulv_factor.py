@@ -27,6 +27,7 @@ GPU path, and it is deterministic (no atomics in any reduction), so repeated
 runs are bitwise identical — the property test_ulv_factor.py:227-241 checks.
 """
 
+import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
@@ -395,16 +396,68 @@ def flop_report(levels, root_dim):
     return fl.flops
 
 
+_PLAN_CACHE = {}       # structure signature -> (DeviceH2, FactorPlan, weakref to the live factors)
+_PLAN_CACHE_MAX = 2
+
+
+def clear_cache():
+    """Drop the cached device layouts / factorization programs."""
+    _PLAN_CACHE.clear()
+
+
+def _cached_plan(h2):
+    """DeviceH2 + FactorPlan for h2, reusing the program and HBM buffers of an
+    earlier factorization with the same structure (dims + interaction lists)
+    once no live ULVFactors references them.  The numeric upload is redone
+    every call; only the symbolic part (layout, descriptors, CUDA graph) is
+    reused — the symbolic/numeric split of a direct solver."""
+    own = getattr(h2, "_device", None)
+    if own is not None:  # operands already in HBM (GPU construct)
+        key = ("dev", id(own))
+        ent = _PLAN_CACHE.get(key)
+        if ent is not None and ent[0] is own and (ent[2] is None or ent[2]() is None):
+            return ent[0], ent[1]
+        plan = FactorPlan(own, h2.lists)
+        _remember(key, own, plan)
+        return own, plan
+    if h2.tree.depth == 0:
+        dh2 = DeviceH2.from_host(h2)
+        return dh2, FactorPlan(dh2, h2.lists)
+    levels = DeviceH2.layouts_from_host(h2)
+    from .h2_device import _signature
+
+    key = ("host", _signature(h2.tree.depth, h2.count, levels))
+    ent = _PLAN_CACHE.get(key)
+    if ent is not None and (ent[2] is None or ent[2]() is None):
+        dh2 = DeviceH2.from_host(h2, into=ent[0])
+        return dh2, ent[1]
+    dh2 = DeviceH2.from_host(h2)
+    plan = FactorPlan(dh2, h2.lists)
+    _remember(key, dh2, plan)
+    return dh2, plan
+
+
+def _remember(key, dh2, plan):
+    if key not in _PLAN_CACHE and len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+        _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+    _PLAN_CACHE[key] = (dh2, plan, None)
+
+
 def factorize(h2, batched=True, retain=False):
     """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
     if retain:
         raise NotImplementedError("retain=True (pre-factorization slab copies) is not supported on the GPU path yet")
     nat.lib()
-    dh2 = h2_device_of(h2)
-    plan = FactorPlan(dh2, h2.lists)
+    dh2, plan = _cached_plan(h2)
+    if plan.program.graph is None:
+        plan.program.capture()
     plan.run()
     plan.check_pivots()
-    return factors_from_plan(h2, plan)
+    f = factors_from_plan(h2, plan)
+    for key, ent in list(_PLAN_CACHE.items()):
+        if ent[1] is plan:
+            _PLAN_CACHE[key] = (ent[0], ent[1], weakref.ref(f))
+    return f
 
 
 def factors_from_plan(h2, plan):

@@ -282,10 +282,16 @@ class SolvePlan:
 
 
 def _plan_for(factors, w, mode):
-    cache = factors.__dict__.setdefault("_solve_plans", {})
+    """Solve programs live with the factorization program they read, so a
+    re-factorization with a cached FactorPlan reuses them too."""
+    fp = factors.device
+    cache = fp.__dict__.setdefault("_solve_plans", {})
     key = (w, mode)
     if key not in cache:
-        cache[key] = SolvePlan(factors.device, w, mode)
+        sp = SolvePlan(fp, w, mode)
+        sp.fwd.capture()
+        sp.bwd.capture()
+        cache[key] = sp
     return cache[key]
 
 
@@ -352,7 +358,7 @@ def solve(factors, b, mode="parallel"):
     dev = sp.device
     perm = factors.__dict__.get("_perm_dev")
     if perm is None:
-        perm = torch.from_numpy(np.asarray(factors.h2.cloud.perm, dtype=np.int64)).to(dev)
+        perm = torch.from_numpy(np.asarray(factors.h2.cloud.perm, dtype=np.int64)).to(dev, non_blocking=True)
         factors._perm_dev = perm
     b_dev = torch.from_numpy(np.ascontiguousarray(bm)).to(dev)
     sp.xin.view(-1, sp.w)[:factors.h2.count] = b_dev.index_select(0, perm)
