@@ -42,17 +42,21 @@ __device__ long long g_diag_trace[64];
 
 __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
                                                                   int32_t* __restrict__ npd) {
-  __shared__ __align__(16) double colD[2][PB];   // pivot column j (double buffered)
-  __shared__ __align__(16) double rowV[2][PB];   // finished row j of V = U^-1
-  __shared__ double dg[PB];                      // pivots d_j
+  // colD[buf][r]: column j of the working matrix for rows r > j, ZERO for rows <= j
+  // (so the multiplier of a finished row is 0 without a branch); rowV[buf][x]:
+  // row j of V = U^-1, zero for x > j.  pv / rpv: pivots and their reciprocals.
+  __shared__ __align__(16) double colD[2][PB];
+  __shared__ __align__(16) double rowV[2][PB];
+  __shared__ double pv[PB], rpv[PB];
   const h2g_panel_desc P = descs[blockIdx.x];
   const int tid = threadIdx.x;
-  // the NBLK lower BSxBS blocks are enumerated row by row over threads 0..NBLK-1
+  // the NBLK lower 2x2 blocks are enumerated row by row over threads 0..NBLK-1
   int br = (int)((sqrtf(8.0f * tid + 1.0f) - 1.0f) * 0.5f);
   while ((br + 1) * (br + 2) / 2 <= tid) ++br;
   while (br * (br + 1) / 2 > tid) --br;
-  const int bc = tid - br * (br + 1) / 2;
+  int bc = tid - br * (br + 1) / 2;
   const bool active = tid < NBLK;
+  if (!active) br = bc = 0;          // idle threads shadow block (0,0) but never publish
   const int r0 = BS * br, c0 = BS * bc;
   const int p = P.p, b = P.b;
   double* H = P.H;
@@ -73,60 +77,71 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
       d[a][e] = val;
       v[a][e] = (i == x) ? 1.0 : 0.0;
     }
-  if (active && bc == 0) {
-#pragma unroll
-    for (int a = 0; a < BS; ++a) colD[0][r0 + a] = d[a][0];
+  if (tid < PB) {
+    rowV[0][tid] = (tid == 0) ? 1.0 : 0.0;
+    rowV[1][tid] = 0.0;
+    colD[1][tid] = 0.0;
   }
-  if (tid < PB) rowV[0][tid] = (tid == 0) ? 1.0 : 0.0;
+  if (active && bc == 0) {
+    colD[0][r0] = (r0 == 0) ? 0.0 : d[0][0];
+    colD[0][r0 + 1] = d[1][0];
+    if (r0 == 0) {
+      pv[0] = d[0][0];
+      rpv[0] = 1.0 / d[0][0];
+    }
+  }
   __syncthreads();
   TRACE(1);
 
-  int bad = INT_MAX;
 #pragma unroll 1
   for (int j = 0; j < PB; ++j) {
-    const int cur = j & 1, nxt = cur ^ 1;
-    const double dj = colD[cur][j];
-    if (tid == 0) {
-      dg[j] = dj;
-      if (!(dj > 0.0) && j < b && bad == INT_MAX) bad = j;
-    }
-    if (active && r0 + BS - 1 > j) {
-      const double rj = 1.0 / dj;
-      // rows > j take the multiplier; columns > j update D, columns <= j update V
-      const double2 cr = reinterpret_cast<const double2*>(colD[cur])[br];
-      const double2 cc = reinterpret_cast<const double2*>(colD[cur])[bc];
-      const double2 rv = reinterpret_cast<const double2*>(rowV[cur])[bc];
-      const double li0 = (r0 > j) ? cr.x * rj : 0.0;
-      const double li1 = cr.y * rj;                       // row r0+1 > j here
-      const bool rt0 = c0 > j, rt1 = c0 + 1 > j;
-      const double lx0 = rt0 ? cc.x : 0.0, lx1 = rt1 ? cc.y : 0.0;
-      const double vx0 = rt0 ? 0.0 : rv.x, vx1 = rt1 ? 0.0 : rv.y;
-      d[0][0] = fma(-li0, lx0, d[0][0]);
-      d[0][1] = fma(-li0, lx1, d[0][1]);
-      d[1][0] = fma(-li1, lx0, d[1][0]);
-      d[1][1] = fma(-li1, lx1, d[1][1]);
-      v[0][0] = fma(-li0, vx0, v[0][0]);
-      v[0][1] = fma(-li0, vx1, v[0][1]);
-      v[1][0] = fma(-li1, vx0, v[1][0]);
-      v[1][1] = fma(-li1, vx1, v[1][1]);
-    }
-    // publish column j+1 of D and row j+1 of V (both final after this step)
+    const int cur = j & 1;
+    const double rj = rpv[j];
+    const double2 cr = reinterpret_cast<const double2*>(&colD[cur][0])[br];
+    const double2 cc = reinterpret_cast<const double2*>(&colD[cur][0])[bc];
+    const double2 rv = reinterpret_cast<const double2*>(&rowV[cur][0])[bc];
+    const double li0 = cr.x * rj, li1 = cr.y * rj;          // 0 for rows <= j
+    d[0][0] = fma(-li0, cc.x, d[0][0]);                      // cc: 0 for columns <= j
+    d[0][1] = fma(-li0, cc.y, d[0][1]);
+    d[1][0] = fma(-li1, cc.x, d[1][0]);
+    d[1][1] = fma(-li1, cc.y, d[1][1]);
+    v[0][0] = fma(-li0, rv.x, v[0][0]);                      // rv: 0 for columns > j
+    v[0][1] = fma(-li0, rv.y, v[0][1]);
+    v[1][0] = fma(-li1, rv.x, v[1][0]);
+    v[1][1] = fma(-li1, rv.y, v[1][1]);
+    // publish column / row jn = j+1 (final after this update) into the other buffer
     const int jn = j + 1;
-    if (active && (jn >> 1) == bc && jn < PB) {
+    if (active && jn < PB) {
       const bool hi = jn & 1;
-      if (r0 >= jn) colD[nxt][r0] = hi ? d[0][1] : d[0][0];
-      if (r0 + 1 >= jn) colD[nxt][r0 + 1] = hi ? d[1][1] : d[1][0];
-    }
-    if (active && (jn >> 1) == br && jn < PB) {
-      const bool hi = jn & 1;
-      const double w0 = hi ? v[1][0] : v[0][0], w1 = hi ? v[1][1] : v[0][1];
-      rowV[nxt][c0] = (c0 <= jn) ? w0 : 0.0;
-      rowV[nxt][c0 + 1] = (c0 + 1 <= jn) ? w1 : 0.0;
+      if ((jn >> 1) == bc) {
+        const double c_0 = hi ? d[0][1] : d[0][0], c_1 = hi ? d[1][1] : d[1][0];
+        double* cn = colD[cur ^ 1];
+        cn[r0] = (r0 > jn) ? c_0 : 0.0;
+        cn[r0 + 1] = (r0 + 1 > jn) ? c_1 : 0.0;
+        if (br == bc) {                                      // owner of the pivot d_jn
+          const double dn = hi ? d[1][1] : d[0][0];
+          pv[jn] = dn;
+          rpv[jn] = 1.0 / dn;
+          if (jn >= 2) cn[jn - 2] = 0.0;                     // rows that finished since
+          cn[jn - 1] = 0.0;                                  //   this buffer was last filled
+        }
+      }
+      if ((jn >> 1) == br) {
+        double* rn = rowV[cur ^ 1];
+        rn[c0] = hi ? v[1][0] : v[0][0];
+        rn[c0 + 1] = hi ? v[1][1] : v[0][1];
+      }
     }
     __syncthreads();
   }
   TRACE(2);
-  if (tid == 0 && bad != INT_MAX) atomicMin(&npd[P.npd_slot], p + bad);
+  if (tid == 0) {
+    for (int j = 0; j < b; ++j)
+      if (!(pv[j] > 0.0)) {
+        atomicMin(&npd[P.npd_slot], p + j);
+        break;
+      }
+  }
 
   // L[i][x] = D[i][x] / sqrt(d_x) (x < i), L[x][x] = sqrt(d_x);  Linv[i][x] = V[i][x] / sqrt(d_i)
   double* __restrict__ out = P.Linv;  // 64 x 64 scratch, ld = ldl
@@ -138,8 +153,8 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
         const int i = r0 + a, x = c0 + e;
         double wv = 0.0;
         if (x <= i && i < b) {
-          const double sx = sqrt(dg[x]);
-          wv = v[a][e] / sqrt(dg[i]);
+          const double sx = sqrt(pv[x]);
+          wv = v[a][e] / sqrt(pv[i]);
           H[(size_t)(p + i) * ldh + p + x] = (x == i) ? sx : d[a][e] / sx;
         }
         out[(size_t)i * P.ldl + x] = wv;

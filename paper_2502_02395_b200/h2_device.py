@@ -41,6 +41,14 @@ def _staging(n_doubles):
     return buf, buf.numpy()
 
 
+_CHUNK = 4 << 20   # doubles per upload chunk (32 MB)
+
+
+def _run_tasks(tasks):
+    for t in tasks:
+        t[0](*t[1:])
+
+
 def _fill_q(host, off, basis, n, k):
     blk = host[off:off + n * n].reshape(n, n)
     blk[:, :n - k] = basis.q_red
@@ -156,30 +164,41 @@ class DeviceH2:
         regions.append(("a", depth, off, max(asize, 1)))
         off += max(asize, 1)
         host_t, host = _staging(off)
-        tasks = []
-        for kind, l, base, _ in regions:
-            lay = levels[l]
-            if kind == "q":
-                for i in range(lay.nb):
-                    tasks.append((_fill_q, host, base + int(lay.qoff[i]), h2.bases[(l, i)], int(lay.n[i]),
-                                  int(lay.k[i])))
-            elif kind == "s":
-                for (i, j), o in lay.soff.items():
-                    tasks.append((_fill_flat, host, base + o, h2.couplings[(l, i, j)]))
-            else:
-                for (i, j), o in aoff.items():
-                    tasks.append((_fill_flat, host, base + o, h2.near_blocks[(depth, i, j)]))
-        list(_pool().map(lambda t: t[0](*t[1:]), tasks, chunksize=max(1, len(tasks) // 64)))
-        src = host_t  # pinned: the copies below are true async DMA
         if into is not None:
             q, s, leaf_a = into.q, into.s, into.leaf_a
         else:
             q = {l: torch.empty(lay.qsize, dtype=F64, device=device) for l, lay in levels.items()}
             s = {l: torch.empty(max(lay.ssize, 1), dtype=F64, device=device) for l, lay in levels.items()}
             leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
+        # chunks of ~4M doubles inside one region: gathered by the thread pool, each
+        # DMA'd to HBM as soon as it is complete (gather and H2D overlap)
+        chunks = []
         for kind, l, base, size in regions:
+            lay = levels[l]
             dst = q[l] if kind == "q" else s[l] if kind == "s" else leaf_a
-            dst[:size].copy_(src[base:base + size], non_blocking=True)
+            if kind == "q":
+                items = [(int(lay.qoff[i]), int(lay.n[i] * lay.n[i]),
+                          (_fill_q, host, base + int(lay.qoff[i]), h2.bases[(l, i)], int(lay.n[i]), int(lay.k[i])))
+                         for i in range(lay.nb)]
+            elif kind == "s":
+                items = [(o, int(lay.k[i] * lay.k[j]), (_fill_flat, host, base + o, h2.couplings[(l, i, j)]))
+                         for (i, j), o in lay.soff.items()]
+            else:
+                items = [(o, int(leaf.n[i] * leaf.n[j]), (_fill_flat, host, base + o, h2.near_blocks[(depth, i, j)]))
+                         for (i, j), o in aoff.items()]
+            cur, c0, c1 = [], 0, 0
+            for o, sz, task in items:
+                if cur and (o + sz) - c0 > _CHUNK:
+                    chunks.append((dst, base, c0, c1, cur))
+                    cur, c0 = [], o
+                cur.append(task)
+                c1 = o + sz
+            if cur:
+                chunks.append((dst, base, c0, c1, cur))
+        futs = [_pool().submit(_run_tasks, ch[4]) for ch in chunks]
+        for (dst, base, c0, c1, _), fu in zip(chunks, futs):
+            fu.result()
+            dst[c0:c1].copy_(host_t[base + c0:base + c1], non_blocking=True)
         torch.cuda.current_stream(device).synchronize()  # staging buffer is reused by the next upload
         return into if into is not None else cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
 
