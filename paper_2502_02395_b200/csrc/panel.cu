@@ -40,17 +40,33 @@ __device__ long long g_diag_trace[64];
 #define TRACE(k) do { } while (0)
 #endif
 
+// 2x2 pivot block [[a, .], [b, c]]: a, b, c, 1/a, u = b/a, 1/d1, d1 = c - b^2/a
+__device__ __forceinline__ void pivot_block(double* s, double a, double b, double c) {
+  const double ra = 1.0 / a;
+  const double det = fma(a, c, -b * b);
+  const double rdet = 1.0 / det;
+  s[0] = a;
+  s[1] = b;
+  s[2] = c;
+  s[3] = ra;
+  s[4] = b * ra;
+  s[5] = a * rdet;
+  s[6] = det * ra;
+}
+
 __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
                                                                   int32_t* __restrict__ npd) {
-  // colD[buf][r]: column j of the working matrix for rows r > j, ZERO for rows <= j
-  // (so the multiplier of a finished row is 0 without a branch); rowV[buf][x]:
-  // row j of V = U^-1, zero for x > j.  pv / rpv: pivots and their reciprocals.
-  __shared__ __align__(16) double colD[2][PB];
-  __shared__ __align__(16) double rowV[2][PB];
-  __shared__ double pv[PB], rpv[PB];
+  // Step q eliminates the 2x2 pivot block {2q, 2q+1} (two scalar LDL^T steps
+  // fused, so 32 barriers instead of 64).  Published per step, double buffered:
+  //   colX / colY : columns 2q and 2q+1 of the working matrix for rows > 2q+1,
+  //                 zero for rows <= 2q+1 (multipliers of finished rows are 0)
+  //   rowA / rowB : rows 2q and 2q+1 of V = U^-1 (rowB before its in-block step)
+  //   scal        : the pivot block a = D[2q][2q], b = D[2q+1][2q], c = D[2q+1][2q+1]
+  __shared__ __align__(16) double colX[2][PB], colY[2][PB], rowA[2][PB], rowB[2][PB];
+  __shared__ __align__(16) double scal[2][8];
+  __shared__ double pv[PB];
   const h2g_panel_desc P = descs[blockIdx.x];
   const int tid = threadIdx.x;
-  // the NBLK lower 2x2 blocks are enumerated row by row over threads 0..NBLK-1
   int br = (int)((sqrtf(8.0f * tid + 1.0f) - 1.0f) * 0.5f);
   while ((br + 1) * (br + 2) / 2 <= tid) ++br;
   while (br * (br + 1) / 2 > tid) --br;
@@ -78,58 +94,79 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
       v[a][e] = (i == x) ? 1.0 : 0.0;
     }
   if (tid < PB) {
-    rowV[0][tid] = (tid == 0) ? 1.0 : 0.0;
-    rowV[1][tid] = 0.0;
-    colD[1][tid] = 0.0;
+    colX[1][tid] = colY[1][tid] = 0.0;
+    rowA[0][tid] = (tid == 0) ? 1.0 : 0.0;
+    rowB[0][tid] = (tid == 1) ? 1.0 : 0.0;
+    rowA[1][tid] = rowB[1][tid] = 0.0;
   }
   if (active && bc == 0) {
-    colD[0][r0] = (r0 == 0) ? 0.0 : d[0][0];
-    colD[0][r0 + 1] = d[1][0];
-    if (r0 == 0) {
-      pv[0] = d[0][0];
-      rpv[0] = 1.0 / d[0][0];
-    }
+    colX[0][r0] = (br > 0) ? d[0][0] : 0.0;
+    colX[0][r0 + 1] = (br > 0) ? d[1][0] : 0.0;
+    colY[0][r0] = (br > 0) ? d[0][1] : 0.0;
+    colY[0][r0 + 1] = (br > 0) ? d[1][1] : 0.0;
+    if (br == 0) pivot_block(scal[0], d[0][0], d[1][0], d[1][1]);
   }
   __syncthreads();
   TRACE(1);
 
 #pragma unroll 1
-  for (int j = 0; j < PB; ++j) {
-    const int cur = j & 1;
-    const double rj = rpv[j];
-    const double2 cr = reinterpret_cast<const double2*>(&colD[cur][0])[br];
-    const double2 cc = reinterpret_cast<const double2*>(&colD[cur][0])[bc];
-    const double2 rv = reinterpret_cast<const double2*>(&rowV[cur][0])[bc];
-    const double li0 = cr.x * rj, li1 = cr.y * rj;          // 0 for rows <= j
-    d[0][0] = fma(-li0, cc.x, d[0][0]);                      // cc: 0 for columns <= j
-    d[0][1] = fma(-li0, cc.y, d[0][1]);
-    d[1][0] = fma(-li1, cc.x, d[1][0]);
-    d[1][1] = fma(-li1, cc.y, d[1][1]);
-    v[0][0] = fma(-li0, rv.x, v[0][0]);                      // rv: 0 for columns > j
-    v[0][1] = fma(-li0, rv.y, v[0][1]);
-    v[1][0] = fma(-li1, rv.x, v[1][0]);
-    v[1][1] = fma(-li1, rv.y, v[1][1]);
-    // publish column / row jn = j+1 (final after this update) into the other buffer
-    const int jn = j + 1;
-    if (active && jn < PB) {
-      const bool hi = jn & 1;
-      if ((jn >> 1) == bc) {
-        const double c_0 = hi ? d[0][1] : d[0][0], c_1 = hi ? d[1][1] : d[1][0];
-        double* cn = colD[cur ^ 1];
-        cn[r0] = (r0 > jn) ? c_0 : 0.0;
-        cn[r0 + 1] = (r0 + 1 > jn) ? c_1 : 0.0;
-        if (br == bc) {                                      // owner of the pivot d_jn
-          const double dn = hi ? d[1][1] : d[0][0];
-          pv[jn] = dn;
-          rpv[jn] = 1.0 / dn;
-          if (jn >= 2) cn[jn - 2] = 0.0;                     // rows that finished since
-          cn[jn - 1] = 0.0;                                  //   this buffer was last filled
+  for (int q = 0; q < PB / 2; ++q) {
+    const int cur = q & 1, nxt = cur ^ 1;
+    const double ra = scal[cur][3], u = scal[cur][4], rd1 = scal[cur][5];
+    if (tid == 0) {
+      pv[2 * q] = scal[cur][0];
+      pv[2 * q + 1] = scal[cur][6];
+    }
+    if (br > q) {
+      const double2 xr = reinterpret_cast<const double2*>(&colX[cur][0])[br];
+      const double2 yr = reinterpret_cast<const double2*>(&colY[cur][0])[br];
+      const double2 xc = reinterpret_cast<const double2*>(&colX[cur][0])[bc];
+      const double2 yc = reinterpret_cast<const double2*>(&colY[cur][0])[bc];
+      const double2 ac = reinterpret_cast<const double2*>(&rowA[cur][0])[bc];
+      const double2 bcv = reinterpret_cast<const double2*>(&rowB[cur][0])[bc];
+      const double xrs[2] = {xr.x, xr.y}, yrs[2] = {yr.x, yr.y};
+      const double xcs[2] = {xc.x, xc.y}, ycs[2] = {fma(-u, xc.x, yc.x), fma(-u, xc.y, yc.y)};
+      const double acs[2] = {ac.x, ac.y}, bcs[2] = {bcv.x, bcv.y};
+#pragma unroll
+      for (int a = 0; a < BS; ++a) {
+        const double al = xrs[a] * ra;                    // X_i / a
+        const double be = fma(-u, xrs[a], yrs[a]) * rd1;  // Y'_i / d1
+        const double ga = fma(-be, u, al);                // coefficient of row 2q of V
+#pragma unroll
+        for (int e = 0; e < BS; ++e) {
+          d[a][e] = fma(-al, xcs[e], fma(-be, ycs[e], d[a][e]));
+          v[a][e] = fma(-ga, acs[e], fma(-be, bcs[e], v[a][e]));
         }
       }
-      if ((jn >> 1) == br) {
-        double* rn = rowV[cur ^ 1];
-        rn[c0] = hi ? v[1][0] : v[0][0];
-        rn[c0 + 1] = hi ? v[1][1] : v[0][1];
+    }
+    if (active && bc == q) {              // column 2q+1 of L uses Y' = Y - u X
+      d[0][1] = fma(-u, d[0][0], d[0][1]);
+      d[1][1] = fma(-u, d[1][0], d[1][1]);
+    }
+    if (active && br == q) {              // row 2q+1 of V after its in-block step
+      v[1][0] = fma(-u, v[0][0], v[1][0]);
+      v[1][1] = fma(-u, v[0][1], v[1][1]);
+    }
+    // publish pivot block q+1 (final after this step) into the other buffer
+    const int qn = q + 1;
+    if (active && qn < PB / 2) {
+      if (bc == qn) {
+        const bool below = br > qn;
+        colX[nxt][r0] = below ? d[0][0] : 0.0;
+        colX[nxt][r0 + 1] = below ? d[1][0] : 0.0;
+        colY[nxt][r0] = below ? d[0][1] : 0.0;
+        colY[nxt][r0 + 1] = below ? d[1][1] : 0.0;
+        if (br == qn) {
+          pivot_block(scal[nxt], d[0][0], d[1][0], d[1][1]);
+          colX[nxt][2 * q] = colX[nxt][2 * q + 1] = 0.0;   // stale rows of this buffer
+          colY[nxt][2 * q] = colY[nxt][2 * q + 1] = 0.0;
+        }
+      }
+      if (br == qn) {
+        rowA[nxt][c0] = v[0][0];
+        rowA[nxt][c0 + 1] = v[0][1];
+        rowB[nxt][c0] = v[1][0];
+        rowB[nxt][c0 + 1] = v[1][1];
       }
     }
     __syncthreads();
