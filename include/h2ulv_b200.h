@@ -249,6 +249,7 @@ enum {
   H2G_STEP_BASIS = 8,
   H2G_STEP_GEMV = 9,     /* descs = outs, map = terms, grid = chunks, arg = w */
   H2G_STEP_TRSV = 10,    /* descs = trsv descs, grid = w, arg = trans      */
+  H2G_STEP_NOP = 12,     /* no kernel: carries a lane's event wait / record  */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */
@@ -264,15 +265,25 @@ typedef struct h2g_step {
   int32_t* npd;       /* PANEL: device pivot-status array */
   const void* aux;    /* KBLOCK: device points (N x 3) */
   double d0, d1;      /* KBLOCK: shift, decay */
+  int32_t lane;       /* 0: the caller's stream, 1: the context's side stream */
+  int32_t wait_ev;    /* event index to wait on before the step, or -1 */
+  int32_t rec_ev;     /* event index to record after the step, or -1 */
+  int32_t pad_;
 } h2g_step;
 
-int h2g_run_program(const h2g_step* steps, int nsteps, void* stream);
-/* Same as h2g_run_program, with a CUDA event recorded on `stream` before
- * every step and after the last; synchronizes and writes the per-step device
- * time (ms) to out_ms[nsteps] (host array).  Used by bench.py for the
+/* Execution context of a two-lane program: a side stream and n_events events
+ * (look-ahead: e.g. the trailing update of Cholesky panel q runs on lane 1
+ * while panel q+1 is factored on lane 0).  With ctx == NULL every step runs
+ * on `stream` in order. */
+int h2g_exec_ctx_create(int n_events, void** ctx_out);
+int h2g_exec_ctx_destroy(void* ctx);
+int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, void* ctx);
+/* Serialized run (lanes ignored) with a CUDA event recorded on `stream`
+ * before every step and after the last; synchronizes and writes the per-step
+ * device time (ms) to out_ms[nsteps] (host array).  Used by bench.py for the
  * per-kernel roofline numbers. */
 int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* stream, float* out_ms);
-int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out);
+int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void* ctx, void** exec_out);
 int h2g_graph_launch(void* exec, void* stream);
 int h2g_graph_destroy(void* exec);
 

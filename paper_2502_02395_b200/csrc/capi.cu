@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -62,21 +63,79 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_KBLOCK:
       return h2g_kernel_blocks((const h2g_kblock_desc*)s.descs, s.map, s.grid, (const double*)s.aux, s.arg,
                                s.d0, s.d1, (int64_t*)s.npd, st);
+    case H2G_STEP_NOP:
+      return H2G_OK;
     default:
       return h2g_set_error(H2G_ESTEP, "unknown step kind %d", s.kind);
   }
 }
 
-extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream) {
+struct ExecCtx {
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+extern "C" int h2g_exec_ctx_create(int n_events, void** ctx_out) {
+  if (!ctx_out || n_events < 0) return h2g_set_error(H2G_EINVAL, "h2g_exec_ctx_create: bad arguments");
+  ExecCtx* c = new ExecCtx();
+  cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
+  c->ev.resize(n_events, nullptr);
+  for (int i = 0; i < n_events && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    h2g_exec_ctx_destroy(c);
+    return h2g_set_error(H2G_ECUDA, "h2g_exec_ctx_create: %s", cudaGetErrorString(e));
+  }
+  *ctx_out = c;
+  return H2G_OK;
+}
+
+extern "C" int h2g_exec_ctx_destroy(void* ctx) {
+  ExecCtx* c = (ExecCtx*)ctx;
+  if (!c) return H2G_OK;
+  for (cudaEvent_t e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
+  return H2G_OK;
+}
+
+extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, void* ctx) {
   if (nsteps < 0 || (nsteps > 0 && !steps)) return h2g_set_error(H2G_EINVAL, "h2g_run_program: bad steps");
-  cudaStream_t st = (cudaStream_t)stream;
+  cudaStream_t main_st = (cudaStream_t)stream;
+  ExecCtx* c = (ExecCtx*)ctx;
+  bool two = false;
+  if (c)
+    for (int i = 0; i < nsteps; ++i) two |= steps[i].lane == 1;
+  if (two) {  // fork: the side lane starts after everything already queued on main
+    cudaEventRecord(c->fork, main_st);
+    cudaStreamWaitEvent(c->side, c->fork, 0);
+  }
   for (int i = 0; i < nsteps; ++i) {
-    int rc = run_step(steps[i], st);
+    const h2g_step& sp = steps[i];
+    cudaStream_t st = (two && sp.lane == 1) ? c->side : main_st;
+    if (two && sp.wait_ev >= 0) {
+      if (sp.wait_ev >= (int)c->ev.size()) return h2g_set_error(H2G_EINVAL, "step %d: bad wait event", i);
+      cudaStreamWaitEvent(st, c->ev[sp.wait_ev], 0);
+    }
+    int rc = run_step(sp, st);
     if (rc) {
       char buf[400];
       snprintf(buf, sizeof(buf), "%.380s", g_err);
-      return h2g_set_error(rc, "step %d (kind %d): %s", i, steps[i].kind, buf);
+      return h2g_set_error(rc, "step %d (kind %d): %s", i, sp.kind, buf);
     }
+    if (two && sp.rec_ev >= 0) {
+      if (sp.rec_ev >= (int)c->ev.size()) return h2g_set_error(H2G_EINVAL, "step %d: bad record event", i);
+      cudaEventRecord(c->ev[sp.rec_ev], st);
+    }
+  }
+  if (two) {  // join: main continues only after the side lane drained
+    cudaEventRecord(c->join, c->side);
+    cudaStreamWaitEvent(main_st, c->join, 0);
   }
   return H2G_OK;
 }
@@ -88,7 +147,7 @@ extern "C" int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* st
   cudaEvent_t* ev = new cudaEvent_t[nsteps + 1];
   for (int i = 0; i <= nsteps; ++i) cudaEventCreate(&ev[i]);
   int rc = H2G_OK;
-  for (int i = 0; i < nsteps && rc == H2G_OK; ++i) {
+  for (int i = 0; i < nsteps && rc == H2G_OK; ++i) {  // lanes ignored: serialized timing
     cudaEventRecord(ev[i], st);
     rc = run_step(steps[i], st);
   }
@@ -104,13 +163,13 @@ extern "C" int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* st
   return rc;
 }
 
-extern "C" int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void** exec_out) {
+extern "C" int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void* ctx, void** exec_out) {
   if (!exec_out) return h2g_set_error(H2G_EINVAL, "h2g_graph_capture: null exec_out");
   cudaStream_t st = (cudaStream_t)stream;
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "begin capture: %s", cudaGetErrorString(e));
-  int rc = h2g_run_program(steps, nsteps, stream);
+  int rc = h2g_run_program(steps, nsteps, stream, ctx);
   e = cudaStreamEndCapture(st, &graph);
   if (rc) {
     if (graph) cudaGraphDestroy(graph);

@@ -54,6 +54,9 @@ class Program:
         self.graph = None
         self.kernel_launches = 0
         self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
+        self.lane = 0         # lane of the steps added next (0: caller's stream, 1: side stream)
+        self.n_events = 0
+        self.ctx = None
 
     # -- blob bookkeeping -------------------------------------------------------------
     def _blob(self, arr):
@@ -62,10 +65,25 @@ class Program:
         self._blobs.append(np.ascontiguousarray(arr).view(np.uint8).reshape(-1))
         return len(self._blobs) - 1
 
-    def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0, flops=0, nbytes=0):
+    def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0, flops=0, nbytes=0,
+             wait=-1, rec=-1):
         self.work.append((kind, int(flops), int(nbytes)))
         self._steps.append(dict(kind=kind, count=int(count), grid=int(grid), descs=descs, map=map_, npd=npd,
-                                arg=int(arg), aux=aux, d0=float(d0), d1=float(d1)))
+                                arg=int(arg), aux=aux, d0=float(d0), d1=float(d1), lane=self.lane,
+                                wait=int(wait), rec=int(rec)))
+
+    # -- two-lane scheduling ----------------------------------------------------------
+    def event(self):
+        self.n_events += 1
+        return self.n_events - 1
+
+    def record(self, ev):
+        """Record `ev` on the current lane (after the steps added so far)."""
+        self._add(nat.STEP["NOP"], 0, 0, rec=ev)
+
+    def wait(self, ev):
+        """Make the current lane wait for `ev`."""
+        self._add(nat.STEP["NOP"], 0, 0, wait=ev)
 
     # -- step constructors ------------------------------------------------------------
     def gemm(self, trans_a, trans_b, problems, tile_cfg=None):
@@ -222,15 +240,24 @@ class Program:
             steps[q]["aux"] = st["aux"]
             steps[q]["d0"] = st["d0"]
             steps[q]["d1"] = st["d1"]
+            steps[q]["lane"] = st["lane"]
+            steps[q]["wait_ev"] = st["wait"]
+            steps[q]["rec_ev"] = st["rec"]
         self.steps = steps
-        self.kernel_launches = int(sum(1 for st in self._steps if st["kind"] != nat.STEP["MEMCPY"]))
+        self.kernel_launches = int(sum(1 for st in self._steps
+                                      if st["kind"] not in (nat.STEP["MEMCPY"], nat.STEP["NOP"])))
+        if any(st["lane"] for st in self._steps):
+            ctx = ctypes.c_void_p()
+            nat.check(nat.lib().h2g_exec_ctx_create(max(self.n_events, 1), ctypes.byref(ctx)), "h2g_exec_ctx_create")
+            self.ctx = ctx
         self.step_kinds = [st["kind"] for st in self._steps]
         self._blobs = []
         return self
 
     def run(self, stream=None):
         lib = nat.lib()
-        rc = lib.h2g_run_program(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps), nat.stream_ptr(stream))
+        rc = lib.h2g_run_program(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps), nat.stream_ptr(stream),
+                                 self.ctx)
         nat.check(rc, "h2g_run_program")
 
     def run_timed(self, stream=None):
@@ -248,7 +275,7 @@ class Program:
         torch.cuda.current_stream(self.device).synchronize()
         exe = ctypes.c_void_p()
         rc = lib.h2g_graph_capture(self.steps.ctypes.data_as(ctypes.c_void_p), len(self.steps),
-                                   nat.stream_ptr(s), ctypes.byref(exe))
+                                   nat.stream_ptr(s), self.ctx, ctypes.byref(exe))
         nat.check(rc, "h2g_graph_capture")
         self.graph = exe
         return self
@@ -260,8 +287,10 @@ class Program:
         nat.check(rc, "h2g_graph_launch")
 
     def __del__(self):
-        if getattr(self, "graph", None) is not None:
-            try:
+        try:
+            if getattr(self, "graph", None) is not None:
                 nat.load_library().h2g_graph_destroy(self.graph)
-            except Exception:
-                pass
+            if getattr(self, "ctx", None) is not None:
+                nat.load_library().h2g_exec_ctx_destroy(self.ctx)
+        except Exception:
+            pass

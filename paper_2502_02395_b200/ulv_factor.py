@@ -222,8 +222,16 @@ class FactorPlan:
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0):
         """Right-looking partial Cholesky of every box's H (and V rows in R),
-        panels of 64 columns: DIAG (chol + inverse of the 64x64 diagonal block),
-        TRSM as an in-place GEMM with L_pp^-T, TRAIL as a GEMM (lower tiles of H)."""
+        panels of W = 64 columns, with a look-ahead of one panel:
+
+          lane 0:  DIAG(q) -> TRSM(q) -> [wait REST(q-1)] -> NEXT(q) -> DIAG(q+1) ...
+          lane 1:                [wait TRSM(q)] -> REST(q)
+
+        DIAG = chol + inverse of the 64x64 diagonal block, TRSM = in-place GEMM
+        with L_pp^-T, NEXT = trailing update of the next block column only,
+        REST = trailing update of everything right of it (lower tiles of H,
+        R[:, ...]).  The factorization of panel q+1 thus overlaps the bulk of
+        panel q's trailing update."""
         nb = len(n)
         rmax = int(r.max()) if nb else 0
         W = nat.PANEL_WIDTH
@@ -233,8 +241,9 @@ class FactorPlan:
         if rmax == 0:
             return linv, loff
         lp = linv.data_ptr()
+        rest_done = None
         for p in range(0, rmax, W):
-            descs, trsm, trail = [], [], []
+            descs, trsm, nxt, rest = [], [], [], []
             for i in range(nb):
                 ri, ni = int(r[i]), int(n[i])
                 if ri <= p:
@@ -243,21 +252,45 @@ class FactorPlan:
                 h = Hp + 8 * int(qo[i])
                 li = lp + 8 * (int(loff[i]) + p // W) * W * W
                 descs.append((h, li, ni, W, p, b, slot0 + i))
-                m = ni - p - b
-                pan = h + 8 * ((p + b) * ni + p)
+                m = ni - p - b                       # rows below the panel
+                pan = h + 8 * ((p + b) * ni + p)     # H[p+b:, p:p+b]
+                q0 = p + b                           # first trailing column
                 if m > 0:
                     trsm.append((pan, li, pan, m, b, b, ni, W, ni, 0, 1.0, 0.0))
-                    trail.append((pan, pan, h + 8 * ((p + b) * ni + p + b), m, m, b, ni, ni, ni,
-                                  nat.GEMM_LOWER, -1.0, 1.0))
+                    wn = min(W, ni - q0)             # next block column of H
+                    nxt.append((pan, pan, h + 8 * (q0 * ni + q0), m, wn, b, ni, ni, ni, 0, -1.0, 1.0))
+                    mr = m - wn                      # the rest, lower tiles
+                    if mr > 0:
+                        pr = pan + 8 * wn * ni
+                        rest.append((pr, pr, h + 8 * ((q0 + wn) * ni + q0 + wn), mr, mr, b, ni, ni, ni,
+                                     nat.GEMM_LOWER, -1.0, 1.0))
                 if Rp:
                     rr = Rp + 8 * int(qo[i])
                     trsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
-                    if ri - p - b > 0:
-                        trail.append((rr + 8 * p, pan, rr + 8 * (p + b), ni, ri - p - b, b, ni, ni, ni,
-                                      0, -1.0, 1.0))
+                    rn = min(W, ri - q0)
+                    if rn > 0:
+                        nxt.append((rr + 8 * p, pan, rr + 8 * q0, ni, rn, b, ni, ni, ni, 0, -1.0, 1.0))
+                    if ri - q0 - W > 0:
+                        rest.append((rr + 8 * p, pan + 8 * W * ni, rr + 8 * (q0 + W), ni, ri - q0 - W, b, ni, ni, ni,
+                                     0, -1.0, 1.0))
             prog.panel(descs, self.npd.data_ptr())
             prog.gemm(0, 1, trsm)
-            prog.gemm(0, 1, trail)
+            ev_trsm = prog.event()
+            prog.record(ev_trsm)
+            if rest_done is not None:
+                prog.wait(rest_done)             # NEXT(q) and REST(q-1) touch the same block column
+            prog.gemm(0, 1, nxt)
+            if rest:
+                prog.lane = 1
+                prog.wait(ev_trsm)
+                prog.gemm(0, 1, rest)
+                rest_done = prog.event()
+                prog.record(rest_done)
+                prog.lane = 0
+            else:
+                rest_done = None
+        if rest_done is not None:
+            prog.wait(rest_done)
         return linv, loff
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
