@@ -175,8 +175,10 @@ class FactorPlan:
                     prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
                                  0, 1.0, 0.0))
                 prog.gemm(0, 0, prob)
+                # H = Q^T (A Q) is symmetric and only its lower half is ever read
+                # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
-                         int(n[i]), int(n[i]), int(n[i]), 0, 1.0, 0.0) for i in range(nb)]
+                         int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb)]
                 prog.gemm(1, 0, prob)
                 B.linv, B.loff = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l])
                 # ---- off-diagonal phase
