@@ -1,0 +1,257 @@
+"""Multi-GPU factorization and solve: boxes sharded over ranks, top levels
+replicated (arXiv 2502.02395 §5; the reference only SIMULATES this plan in
+comm_sim.py:1-186 — here the data really moves).
+
+Ownership follows the reference's ProcAssignment (comm_sim.py:17-37): with
+P = 2^L0 ranks, rank g owns box i of level l >= L0 iff i >> (l - L0) == g
+(contiguous leaf ranges); levels < L0 and the root are computed redundantly
+by every rank (replicated_work, comm_sim.py:151-167).
+
+Exchanges (one process per GPU, torch.distributed; NCCL over NVLink on a
+multi-GPU node, gloo through host memory in the CPU tests):
+  factorization
+    halo_v(l)     after the diagonal phase of a distributed level: the
+                  [V_j | q_skel_j] block of every box j that is the column of a
+                  near pair whose row box lives on another rank (all_gather of
+                  the packed exports)
+    boundary(L0)  after level L0: every rank receives all level-L0 Schur blocks
+                  (H_i, T_ij) and assembles the replicated parent level — the
+                  reference's merge AllReduce (Eq. 34, comm_sim.simulate_factor)
+                  done as one all_gather
+    solve_halo    cross-pair off-diagonal factor blocks (T_ij, L(s)_ji) also
+                  land on the column box's owner, so the solve only moves vectors
+  solve           per distributed level, the owned segments of each
+                  intermediate vector are summed across ranks (all_reduce of a
+                  masked level vector; comm_sim.simulate_solve's neighbour
+                  reduce/broadcast + merge AllReduce)
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .program import Program
+
+F64 = torch.float64
+
+
+class Partition:
+    """Box ownership over P = 2^L0 ranks (comm_sim.ProcAssignment semantics)."""
+
+    def __init__(self, p, depth):
+        if p < 1 or p & (p - 1):
+            raise ValueError("process count must be a power of 2")
+        if p > 2 ** depth:
+            raise ValueError(f"p = {p} exceeds the leaf count {2 ** depth}")
+        self.p = p
+        self.depth = depth
+        self.L0 = int(math.log2(p))
+
+    def group(self, l, i):
+        if l >= self.L0:
+            g = i >> (l - self.L0)
+            return (g, g + 1)
+        span = self.p >> l
+        return (i * span, (i + 1) * span)
+
+    def owner(self, l, i):
+        return self.group(l, i)[0]
+
+    def owned_mask(self, l, rank):
+        i = np.arange(2 ** l)
+        if l < self.L0:
+            return np.ones(2 ** l, dtype=bool)
+        return (i >> (l - self.L0)) == rank
+
+
+@dataclass
+class CommEvent:
+    phase: str
+    level: int
+    kind: str
+    bytes: int
+
+
+@dataclass
+class Comm:
+    """Thin torch.distributed wrapper that also records a communication trace."""
+
+    rank: int = 0
+    world: int = 1
+    group: object = None
+    host_staged: bool = False      # gloo: collectives on host copies
+    trace: list = field(default_factory=list)
+
+    @classmethod
+    def from_env(cls, group=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            return cls()
+        backend = dist.get_backend(group)
+        return cls(rank=dist.get_rank(group), world=dist.get_world_size(group), group=group,
+                   host_staged=(backend != "nccl"))
+
+    def _log(self, phase, level, kind, nbytes):
+        self.trace.append(CommEvent(phase, level, kind, int(nbytes)))
+
+    def all_gather(self, t, phase="factor", level=-1):
+        import torch.distributed as dist
+
+        self._log(phase, level, "all_gather", t.numel() * t.element_size() * self.world)
+        if self.host_staged:
+            h = t.cpu()
+            out = [torch.empty_like(h) for _ in range(self.world)]
+            dist.all_gather(out, h, group=self.group)
+            return [o.to(t.device) for o in out]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return out
+
+    def all_reduce_(self, t, op="sum", phase="solve", level=-1):
+        import torch.distributed as dist
+
+        self._log(phase, level, "all_reduce", t.numel() * t.element_size())
+        rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MIN
+        if self.host_staged:
+            h = t.cpu()
+            dist.all_reduce(h, op=rop, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=rop, group=self.group)
+        return t
+
+    def allreduce_min_(self, t):
+        return self.all_reduce_(t, op="min", phase="factor", level=0)
+
+    def all_max(self, x):
+        import torch.distributed as dist
+
+        t = torch.tensor([float(x)], dtype=F64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+# --------------------------------------------------------------------------- factorization exchanges
+
+def _exchange_blocks(plan, blocks, phase, level):
+    """all_gather of per-rank block exports.
+
+    blocks: list of (owner_rank, flat device tensor, offset, size) — every rank
+    lists the same blocks in the same order; after the call each rank's copy of
+    every block equals its owner's."""
+    comm = plan.comm
+    dev = plan.device
+    sizes = np.zeros(comm.world, dtype=np.int64)
+    for own, _, _, sz in blocks:
+        sizes[own] += sz
+    cap = int(sizes.max())
+    if cap == 0:
+        return
+    send = torch.zeros(cap, dtype=F64, device=dev)
+    pos = 0
+    for own, t, off, sz in blocks:
+        if own == comm.rank:
+            send[pos:pos + sz].copy_(t[off:off + sz])
+            pos += sz
+    recv = comm.all_gather(send, phase=phase, level=level)
+    cursor = np.zeros(comm.world, dtype=np.int64)
+    for own, t, off, sz in blocks:
+        c = int(cursor[own])
+        if own != comm.rank:
+            t[off:off + sz].copy_(recv[own][c:c + sz])
+        cursor[own] = c + sz
+
+
+def _halo_v_blocks(plan, l):
+    part, B = plan.part, plan.bufs[l]
+    lay = B.lay
+    need = sorted({j for (i, j) in lay.off_pairs if part.owner(l, i) != part.owner(l, j)})
+    return [(part.owner(l, j), B.R, int(lay.qoff[j]), int(lay.n[j] * lay.n[j])) for j in need]
+
+
+def _boundary_blocks(plan, l):
+    part, B = plan.part, plan.bufs[l]
+    lay = B.lay
+    out = [(part.owner(l, i), B.H, int(lay.qoff[i]), int(lay.n[i] * lay.n[i])) for i in range(lay.nb)]
+    out += [(part.owner(l, i), B.T, int(B.toff[(i, j)]), int(lay.n[i] * lay.n[j])) for (i, j) in lay.off_pairs]
+    return out
+
+
+def _solve_halo_blocks(plan):
+    """Cross-owner off-diagonal factor blocks, for the column box's owner."""
+    part = plan.part
+    out = []
+    for l, B in sorted(plan.bufs.items(), reverse=True):
+        if not plan.distributed_level(l):
+            continue
+        lay = B.lay
+        for (i, j) in lay.off_pairs:
+            oi = part.owner(l, i)
+            if oi == part.owner(l, j):
+                continue
+            out.append((oi, B.T, int(B.toff[(i, j)]), int(lay.n[i] * lay.n[j])))
+            out.append((oi, B.LSm, int(B.lsoff[(i, j)]), int(lay.k[j] * lay.r[i])))
+    return out
+
+
+def run_segments(plan, stream=None):
+    for seg in plan.segments:
+        if isinstance(seg, Program):
+            seg.launch(stream)
+            continue
+        kind, l = seg
+        torch.cuda.current_stream(plan.device).synchronize()
+        if kind == "halo_v":
+            _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l)
+        elif kind == "boundary":
+            _exchange_blocks(plan, _boundary_blocks(plan, l), "factor", l)
+        else:
+            raise ValueError(f"unknown exchange {kind}")
+    if plan.part is not None and plan.part.p > 1:
+        torch.cuda.current_stream(plan.device).synchronize()
+        _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1)
+
+
+# --------------------------------------------------------------------------- public API
+
+def factorize_distributed(h2, comm=None):
+    """Sharded factorization of `h2` over the ranks of `comm` (default: the
+    initialized torch.distributed world).  Every rank passes the same H2
+    (construction is replicated); returns ULVFactors whose distributed levels
+    hold this rank's boxes (``factors.partition``) and whose replicated top
+    levels and root are complete on every rank."""
+    from . import _native as nat
+    from .h2_device import DeviceH2
+    from .ulv_factor import FactorPlan, factors_from_plan
+
+    nat.lib()
+    comm = comm or Comm.from_env()
+    if comm.world == 1 or h2.tree.depth == 0:
+        from .ulv_factor import factorize
+
+        return factorize(h2)
+    part = Partition(comm.world, h2.tree.depth)
+    dh2 = getattr(h2, "_device", None) or DeviceH2.from_host(h2)
+    plan = FactorPlan(dh2, h2.lists, part=part, comm=comm)
+    plan.run()
+    plan.check_pivots()
+    f = factors_from_plan(h2, plan)
+    f.partition = part
+    f.comm = comm
+    return f
+
+
+def solve_distributed(factors, b, mode="parallel"):
+    """Distributed solve; every rank passes b (user order) and gets x."""
+    from . import _native as nat
+    from .ulv_solve import solve
+
+    if getattr(factors, "partition", None) is None:
+        return solve(factors, b, mode=mode)
+    if mode != "parallel":
+        raise ValueError("the distributed solve implements the parallel substitution")
+    nat.lib()
+    return solve(factors, b, mode=mode)

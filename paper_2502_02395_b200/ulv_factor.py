@@ -119,15 +119,23 @@ class _LevelBuffers:
 
 
 class FactorPlan:
-    """Device buffers + the static step program of one factorization."""
+    """Device buffers + the static step program(s) of one factorization.
 
-    def __init__(self, dh2: DeviceH2, lists):
+    Single GPU: one Program.  Distributed (`part` = Partition, `comm` = Comm):
+    every rank computes the boxes it owns at the distributed levels
+    (l >= log2 P) and everything above; the program is cut into segments
+    with collective exchanges in between (distributed.py)."""
+
+    def __init__(self, dh2: DeviceH2, lists, part=None, comm=None):
         self.dh2 = dh2
         self.depth = dh2.depth
+        self.part = part
+        self.comm = comm
         dev = dh2.device
         self.device = dev
-        prog = Program(dev)
         depth = self.depth
+        self.segments = []
+        prog = Program(dev)
         # pivot status: one slot per box of every level plus the root
         self.slot_base = {}
         acc = 0
@@ -155,6 +163,8 @@ class FactorPlan:
                 self.bufs[l] = B
                 B.lay = lay
                 n, k, r = lay.n, lay.k, lay.r
+                nb = lay.nb
+                mine = self.mine(l)
                 qsz = max(lay.qsize, 1)
                 B.M = torch.empty(qsz, dtype=F64, device=dev)
                 B.H = torch.empty(qsz, dtype=F64, device=dev)
@@ -164,13 +174,14 @@ class FactorPlan:
                 ap = a_buf.data_ptr()
                 qo = lay.qoff
                 for (i, j) in lay.near_pairs:
-                    if (i, j) not in a_off:
+                    if (i, j) not in a_off and mine[i]:
                         raise StructureError(f"missing near block ({l}, {i}, {j})")
-                nb = lay.nb
                 # ---- diagonal phase
                 prog.memcpy(Rp, qp, 8 * lay.qsize)
                 prob = []
                 for i in range(nb):
+                    if not mine[i]:
+                        continue
                     ni = int(n[i])
                     prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
                                  0, 1.0, 0.0))
@@ -178,9 +189,9 @@ class FactorPlan:
                 # H = Q^T (A Q) is symmetric and only its lower half is ever read
                 # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
-                         int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb)]
+                         int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
                 prog.gemm(1, 0, prob)
-                B.linv, B.loff = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l])
+                B.linv, B.loff = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine)
                 # ---- off-diagonal phase
                 offp = lay.off_pairs
                 B.toff, B.lsoff = {}, {}
@@ -194,14 +205,21 @@ class FactorPlan:
                 B.T = torch.empty(max(tacc, 1), dtype=F64, device=dev)
                 B.LSm = torch.empty(max(lacc, 1), dtype=F64, device=dev)
                 MOp, Tp, LSp = B.MO.data_ptr(), B.T.data_ptr(), B.LSm.data_ptr()
+                if self.distributed_level(l):
+                    # V_j of boxes owned elsewhere but coupled to mine by a near pair
+                    prog = self._cut(prog, ("halo_v", l))
                 prob = []
                 for (i, j) in offp:
+                    if not mine[i]:
+                        continue
                     ni, nj = int(n[i]), int(n[j])
                     prob.append((ap + 8 * a_off[(i, j)], Rp + 8 * qo[j], MOp + 8 * B.toff[(i, j)], ni, nj, nj,
                                  nj, nj, nj, 0, 1.0, 0.0))
                 prog.gemm(0, 0, prob)
                 prob = []
                 for (i, j) in offp:
+                    if not mine[i]:
+                        continue
                     ni, nj, ri, rj, kj = int(n[i]), int(n[j]), int(r[i]), int(r[j]), int(k[j])
                     mo = MOp + 8 * B.toff[(i, j)]
                     prob.append((qp + 8 * qo[i], mo, Tp + 8 * B.toff[(i, j)], ni, nj, ni, ni, nj, nj, 0, 1.0, 0.0))
@@ -209,6 +227,9 @@ class FactorPlan:
                     prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
                                  0, 1.0, 0.0))
                 prog.gemm(1, 0, prob)
+                if self.distributed_level(l) and not self.distributed_level(l - 1):
+                    # boundary: the parent level is replicated -> every rank needs all SS blocks
+                    prog = self._cut(prog, ("boundary", l))
                 # ---- merge into the parent level (or the root)
                 a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2)
             d = self._root_d
@@ -219,10 +240,27 @@ class FactorPlan:
         self.flops = flop_report({l: (B.lay.n, B.lay.k, B.lay.off_pairs) for l, B in self.bufs.items()},
                                  self.root_dim)
         self.audit = self._audit()
-        self.program = prog.finalize()
+        self.segments.append(prog.finalize())
+        self.program = self.segments[0] if len(self.segments) == 1 else None
+
+    # ------------------------------------------------------------------ distribution hooks
+    def mine(self, l):
+        """Boolean mask of the level-l boxes this rank computes."""
+        nb = 2 ** l
+        if self.part is None or not self.distributed_level(l):
+            return np.ones(nb, dtype=bool)
+        return self.part.owned_mask(l, self.comm.rank)
+
+    def distributed_level(self, l):
+        return self.part is not None and self.part.p > 1 and l >= self.part.L0
+
+    def _cut(self, prog, tag):
+        self.segments.append(prog.finalize())
+        self.segments.append(tag)
+        return Program(self.device)
 
     # ------------------------------------------------------------------ steps
-    def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0):
+    def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None):
         """Right-looking partial Cholesky of every box's H (and V rows in R),
         panels of W = 64 columns, with a look-ahead of one panel:
 
@@ -235,7 +273,8 @@ class FactorPlan:
         R[:, ...]).  The factorization of panel q+1 thus overlaps the bulk of
         panel q's trailing update."""
         nb = len(n)
-        rmax = int(r.max()) if nb else 0
+        mine = np.ones(nb, dtype=bool) if mine is None else mine
+        rmax = int(np.asarray(r)[mine].max()) if mine.any() else 0
         W = nat.PANEL_WIDTH
         nblk = -(-np.asarray(r, dtype=np.int64) // W)
         loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
@@ -248,7 +287,7 @@ class FactorPlan:
             descs, trsm, nxt, rest = [], [], [], []
             for i in range(nb):
                 ri, ni = int(r[i]), int(n[i])
-                if ri <= p:
+                if ri <= p or not mine[i]:
                     continue
                 b = min(W, ri - p)
                 h = Hp + 8 * int(qo[i])
@@ -305,6 +344,8 @@ class FactorPlan:
         n, k, r = lay.n, lay.k, lay.r
         parents = sorted((pi, pj) for (pi, pj) in lists.near[l - 1] if pi >= pj)
         self.merge_pairs[l] = parents
+        pmine = self.mine(l - 1) if l - 1 >= 1 else np.ones(1, dtype=bool)
+        built = [(pi, pj) for (pi, pj) in parents if pmine[pi]]
         pn = {p: int(k[2 * p] + k[2 * p + 1]) for p in range(2 ** (l - 1))}
         aoff, acc = {}, 0
         for (pi, pj) in parents:
@@ -316,7 +357,7 @@ class FactorPlan:
         Hp, Tp, Sp = B.H.data_ptr(), B.T.data_ptr(), dh2.s[l].data_ptr()
         qo = lay.qoff
         descs = []
-        for (pi, pj) in parents:
+        for (pi, pj) in built:
             dst0 = abuf.data_ptr() + 8 * aoff[(pi, pj)]
             ldd = pn[pj]
             for a in (0, 1):
@@ -361,9 +402,22 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ run / check
     def run(self, stream=None):
-        self.program.launch(stream)
+        if self.program is not None:
+            self.program.launch(stream)
+            return
+        from .distributed import run_segments
+
+        run_segments(self, stream)
+
+    def capture(self):
+        """CUDA-graph every program segment (collectives stay outside)."""
+        for seg in self.segments:
+            if isinstance(seg, Program) and seg.graph is None:
+                seg.capture()
 
     def check_pivots(self):
+        if self.comm is not None and self.part is not None and self.part.p > 1:
+            self.comm.allreduce_min_(self.npd)
         npd = self.npd.cpu().numpy()
         if (npd == INT_MAX).all():
             return
@@ -484,8 +538,7 @@ def factorize(h2, batched=True, retain=False):
         raise NotImplementedError("retain=True (pre-factorization slab copies) is not supported on the GPU path yet")
     nat.lib()
     dh2, plan = _cached_plan(h2)
-    if plan.program.graph is None:
-        plan.program.capture()
+    plan.capture()
     plan.run()
     plan.check_pivots()
     f = factors_from_plan(h2, plan)

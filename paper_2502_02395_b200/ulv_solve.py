@@ -72,9 +72,54 @@ class SolvePlan:
                              offR=np.concatenate([[0], np.cumsum(lay.r)[:-1]]).astype(np.int64),
                              offS=np.concatenate([[0], np.cumsum(lay.k)[:-1]]).astype(np.int64),
                              offX=np.concatenate([[0], np.cumsum(lay.n)[:-1]]).astype(np.int64))
-        self.fwd = self._build_forward().finalize()
-        self.bwd = self._build_backward().finalize()
+        self.dist = fplan.part is not None and fplan.part.p > 1
+        self._segs = []
+        self._masks = {}
+        self.fwd_segments = self._finish(self._build_forward())
+        self.bwd_segments = self._finish(self._build_backward())
+        self.fwd = self.fwd_segments[0] if len(self.fwd_segments) == 1 else None
+        self.bwd = self.bwd_segments[0] if len(self.bwd_segments) == 1 else None
         self.output = self.v[depth]["FULL"] if depth >= 1 else self.xroot
+
+    # -------------------------------------------------------------- distribution
+    def _mine(self, l):
+        return self.fp.mine(l) if l >= 1 else np.ones(1, dtype=bool)
+
+    def _cut(self, prog, tag):
+        """End the current program segment; `tag` = (vector, level, offsets key)
+        is all-reduced across ranks (owned segments only) before the next one."""
+        if not self.dist:
+            return prog
+        self._segs.append(prog.finalize())
+        self._segs.append(tag)
+        return Program(self.device)
+
+    def _finish(self, prog):
+        segs = self._segs + [prog.finalize()]
+        self._segs = []
+        return segs
+
+    def _mask(self, l, offkey):
+        """0/1 row mask (x w columns) of the owned segments of a level-l vector."""
+        key = (l, offkey)
+        if key not in self._masks:
+            lay = self.fp.bufs[l].lay
+            sizes = {"offR": lay.r, "offS": lay.k, "offX": lay.n}[offkey]
+            mine = self._mine(l)
+            m = np.repeat(mine.astype(np.float64), np.asarray(sizes, dtype=np.int64))
+            self._masks[key] = torch.from_numpy(np.repeat(m, self.w)).to(self.device)
+        return self._masks[key]
+
+    def _run_segments(self, segs, stream=None):
+        for seg in segs:
+            if isinstance(seg, Program):
+                seg.launch(stream)
+                continue
+            name, l, offkey = seg
+            vec = self.v[l][name]
+            m = self._mask(l, offkey)
+            vec[:m.numel()].mul_(m)
+            self.fp.comm.all_reduce_(vec[:m.numel()], phase="solve", level=l)
 
     # -------------------------------------------------------------- pointers
     def _p(self, t, off_rows=0):
@@ -127,17 +172,22 @@ class SolvePlan:
             offR, offS, offX = V["offR"], V["offS"], V["offX"]
             below, _ = _near_sets(lay)
             q = fp.dh2.q[l]
+            mine = self._mine(l)
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
             outs = []
             for i in range(nb):
+                if not mine[i]:
+                    continue
                 outs.append((self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
                              nat.GEMV_PLUS | nat.GEMV_SPLIT,
                              [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))]))
             prog.gemv(outs, w)
             if self.mode == "parallel":
-                self._forward_parallel_level(prog, l, V, lay, below)
+                prog = self._forward_parallel_level(prog, l, V, lay, below)
             else:
                 self._forward_naive_level(prog, l, V, lay)
+            if self.dist and fp.distributed_level(l) and not fp.distributed_level(l - 1):
+                prog = self._cut(prog, ("BS", l, "offS"))   # the parent level is replicated
             xin = V["BS"]
         d = fp.root_dim
         prog.memcpy(self.yroot.data_ptr(), xin.data_ptr(), 8 * d * w)
@@ -149,27 +199,38 @@ class SolvePlan:
         n, k, r, nb = lay.n, lay.k, lay.r, lay.nb
         offR, offS = V["offR"], V["offS"]
         B = self.fp.bufs[l]
+        mine = self._mine(l)
+        dist = self.dist and self.fp.distributed_level(l)
         # P1  z_i = L_ii^-1 b_R,i
         prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
-        prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb)], 0, w)
+        prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb) if mine[i]], 0, w)
+        if dist:
+            prog = self._cut(prog, ("Z", l, "offR"))
         # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j
         outs = []
         for i in range(nb):
+            if not mine[i]:
+                continue
             terms = [(B.T.data_ptr() + 8 * int(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
                      for j in below[i] if r[j] > 0]
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
         prog.gemv(outs, w)
         # P3  y_i = L_ii^-1 t_i
-        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in range(nb)], 0, w)
+        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in range(nb) if mine[i]], 0, w)
+        if dist:
+            prog = self._cut(prog, ("Y", l, "offR"))
         # P4  b_S,a -= sum_b L(s)_ab y_b
-        self._ls_update_forward(prog, l, V, lay)
+        self._ls_update_forward(prog, l, V, lay, owned=mine)
+        return prog
 
-    def _ls_update_forward(self, prog, l, V, lay, only_b=None):
+    def _ls_update_forward(self, prog, l, V, lay, only_b=None, owned=None):
         w = self.w
         offR, offS = V["offR"], V["offS"]
         terms = {}
         for (a, b) in self._ls_keys(lay):
             if only_b is not None and b != only_b:
+                continue
+            if owned is not None and not owned[a]:
                 continue
             ptr, ld = self._ls(l, a, b)
             terms.setdefault(a, []).append((ptr, self._p(V["Y"], offR[b]), ld, 0, int(lay.r[b])))
@@ -211,31 +272,41 @@ class SolvePlan:
             n, k, r, nb = lay.n, lay.k, lay.r, lay.nb
             offR, offS, offX = V["offR"], V["offS"], V["offX"]
             B = fp.bufs[l]
+            mine = self._mine(l)
+            dist = self.dist and fp.distributed_level(l)
+            if dist and fp.distributed_level(l - 1):
+                prog = self._cut(prog, ("FULL", l - 1, "offX"))   # x_S of neighbours owned elsewhere
             # B1  y_R,i -= sum_a L(s)_ai^T x_S,a
             src = {}
             for (a, b) in self._ls_keys(lay):
                 ptr, ld = self._ls(l, a, b)
                 src.setdefault(b, []).append((ptr, self._p(xs, offS[a]), ld, 1, int(k[a])))
             outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0, sorted(src.get(i, [])))
-                    for i in range(nb)]
+                    for i in range(nb) if mine[i]]
             prog.gemv(outs, w)
             if self.mode == "parallel":
                 _, above = _near_sets(lay)
                 prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
-                prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb)], 1, w)
+                prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
+                if dist:
+                    prog = self._cut(prog, ("Z2", l, "offR"))
                 outs = []
                 for i in range(nb):
+                    if not mine[i]:
+                        continue
                     terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
                 prog.gemv(outs, w)
-                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in range(nb)], 1, w)
+                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in range(nb) if mine[i]], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
             # B3  full_i = q_red x_R + q_skel x_S
             q = fp.dh2.q[l]
             outs = []
             for i in range(nb):
+                if not mine[i]:
+                    continue
                 qi = q.data_ptr() + 8 * int(lay.qoff[i])
                 terms = []
                 if r[i] > 0:
@@ -245,6 +316,8 @@ class SolvePlan:
                 outs.append((self._p(V["FULL"], offX[i]), 0, 0, int(n[i]), 0, nat.GEMV_PLUS, terms))
             prog.gemv(outs, w)
             xs = V["FULL"]
+        if self.dist and depth >= 1 and fp.distributed_level(depth):
+            prog = self._cut(prog, ("FULL", depth, "offX"))     # assemble x on every rank
         return prog
 
     def _backward_naive_level(self, prog, l, V, lay):
@@ -263,10 +336,16 @@ class SolvePlan:
 
     # -------------------------------------------------------------- run
     def run_forward(self, stream=None):
-        self.fwd.launch(stream)
+        if self.fwd is not None:
+            self.fwd.launch(stream)
+        else:
+            self._run_segments(self.fwd_segments, stream)
 
     def run_backward(self, stream=None):
-        self.bwd.launch(stream)
+        if self.bwd is not None:
+            self.bwd.launch(stream)
+        else:
+            self._run_segments(self.bwd_segments, stream)
 
     def block_vector(self, vector):
         bv = BlockVector(width=self.w, vector=vector, _plan=self)
@@ -289,8 +368,9 @@ def _plan_for(factors, w, mode):
     key = (w, mode)
     if key not in cache:
         sp = SolvePlan(fp, w, mode)
-        sp.fwd.capture()
-        sp.bwd.capture()
+        for seg in sp.fwd_segments + sp.bwd_segments:
+            if isinstance(seg, Program):
+                seg.capture()
         cache[key] = sp
     return cache[key]
 
