@@ -16,9 +16,10 @@ not part of the reference metric).
                 its CUDA-event time inside an instrumented pass of K steps
   cpu_baseline  the CPU oracle port (oracle/h2ulv_oracle.py) on the host cores
 
-Multi-GPU (`torchrun ... bench.py --gpus N`): replicas — every rank factors its
-own instance (weak scaling, no collective on the data path); value sums the
-flops of all ranks over the max-over-ranks time.
+Multi-GPU (`torchrun ... bench.py --gpus N`): ONE factorization sharded over
+the ranks (distributed.py: boxes of the levels >= log2 N split by contiguous
+leaf ranges, NCCL all_gather of halo / boundary blocks, top levels replicated);
+strong scaling, time = max over ranks.
 `--impl reference` times the CPU oracle port (the reference is pure Python and
 does not travel to the GPU box) on rank 0 only.
 """
@@ -219,24 +220,36 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BENCH_SHARE_GPU"):   # test mode: all ranks on GPU 0 (gloo)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     kernel, cloud, tree, lists, cfg = build_problem(pkg, c)
     t0 = time.perf_counter()
     h2 = pkg.construct(kernel, tree, lists, cfg, cloud, device=dev)
     construct_s = time.perf_counter() - t0
 
-    plan = FactorPlan(h2._device, lists)
-    prog = plan.program
-    prog.capture()
+    comm = part = None
+    if world > 1:
+        from paper_2502_02395_b200.distributed import Comm, Partition
+
+        comm = Comm.from_env()
+        part = Partition(world, tree.depth)
+    plan = FactorPlan(h2._device, lists, part=part, comm=comm)
+    plan.capture()
+    progs = [sg for sg in plan.segments if not isinstance(sg, tuple)]
     flops = plan.flops["total_true"]
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        prog.launch(stream)
+        plan.run(stream)
     torch.cuda.synchronize(dev)
     plan.check_pivots()
 
@@ -248,7 +261,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        prog.launch(stream)
+        plan.run(stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -259,18 +272,30 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * flops / (ms * 1e-3) / 1e9
+    # one matrix per step: replicas would multiply by world; the sharded factorization
+    # splits ONE factorization over the ranks (strong scaling)
+    value = flops / (ms * 1e-3) / 1e9
 
     # ---- roofline: per-step CUDA events over K instrumented (eager) factorizations
     per_kind = {}
-    step_ms = np.zeros(len(prog.steps))
+    work = [w for pg in progs for w in pg.work]
+    steps_arr = np.concatenate([pg.steps for pg in progs])
+    step_ms = np.zeros(len(steps_arr))
     for _ in range(args.steps):
-        step_ms += prog.run_timed(stream)
+        parts = []
+        for sg in plan.segments:
+            if isinstance(sg, tuple):
+                from paper_2502_02395_b200.distributed import run_exchange
+
+                run_exchange(plan, sg)
+            else:
+                parts.append(sg.run_timed(stream))
+        step_ms += np.concatenate(parts)
     step_ms /= args.steps
     gemm_kinds = {nat.STEP[k] for k in ("GEMM_NN", "GEMM_NT", "GEMM_TN", "GEMM_TT")}
     names = {v: k for k, v in nat.STEP.items()}
     g_fl = g_ms = 0.0
-    for (kind, fl, by), t in zip(prog.work, step_ms):
+    for (kind, fl, by), t in zip(work, step_ms):
         nm = "GEMM" if kind in gemm_kinds else names[kind]
         d = per_kind.setdefault(nm, {"ms": 0.0, "launches": 0, "flops": 0, "bytes": 0})
         d["ms"] += float(t)
@@ -285,7 +310,7 @@ def main():
         with open(os.environ["BENCH_DUMP"], "w") as fh:
             json.dump([{"kind": names[int(kd)], "flops": int(fl), "bytes": int(by), "ms": float(t),
                         "count": int(st["count"]), "grid": int(st["grid"])}
-                       for (kd, fl, by), t, st in zip(prog.work, step_ms, prog.steps)], fh)
+                       for (kd, fl, by), t, st in zip(work, step_ms, steps_arr)], fh)
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -305,12 +330,19 @@ def main():
 
     # ---- solve + residual (device factors)
     f = factors_from_plan(h2, plan)
+    if world > 1:
+        from paper_2502_02395_b200.distributed import factorize_distributed, solve_distributed
+
+        f.partition, f.comm = part, comm
+        solve_fn, factor_fn = solve_distributed, factorize_distributed
+    else:
+        solve_fn, factor_fn = pkg.solve, pkg.factorize
     b = np.random.default_rng(1).standard_normal(c["n"])
-    x = pkg.solve(f, b)
+    x = solve_fn(f, b)
     torch.cuda.synchronize(dev)
     ts0 = time.perf_counter()
     for _ in range(3):
-        x = pkg.solve(f, b)
+        x = solve_fn(f, b)
     solve_ms = (time.perf_counter() - ts0) / 3 * 1e3
     perm = cloud.perm
     res = float(np.linalg.norm(h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b))
@@ -322,8 +354,8 @@ def main():
     for s in range(1 + args.e2e_steps):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        fe = pkg.factorize(h2_host)
-        xe = pkg.solve(fe, b)
+        fe = factor_fn(h2_host)
+        xe = solve_fn(fe, b)
         torch.cuda.synchronize(dev)
         if s:
             e2e_times.append(time.perf_counter() - t0)
@@ -333,7 +365,7 @@ def main():
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": world * flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
+    e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
            "d2h_bytes_per_step": int(xe.nbytes + plan.npd.numel() * 4), "seconds_per_step": e2e_s,
            "includes": "factorize(h2 of host numpy blocks): parallel pinned gather + H2D of bases / leaf near "
                        "blocks / couplings, graph-replayed factorization, pivot-status D2H; solve(b): H2D b, "
@@ -350,16 +382,20 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
-                "config": {"workload": workload_name(args.config, c), "parallelism": f"replicas{world}",
+                "config": {"workload": workload_name(args.config, c),
+                           "parallelism": (f"sharded{world}: boxes of levels >= log2 P split by contiguous leaf "
+                                           f"ranges, top levels + root replicated, {backend} exchanges")
+                           if world > 1 else "single GPU",
                            "flops_per_step": flops, "padded_flops": plan.flops["total_padded"],
                            "factor_seconds": ms * 1e-3, "solve_ms": solve_ms, "residual": res,
                            "construct_seconds": construct_s, "eager_ms_per_step": eager_ms,
                            "l2": "inputs > L2 (leaf near blocks + bases ~0.4 GB per step)",
                            "depth": tree.depth, "root_dim": plan.root_dim},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": prog.kernel_launches * args.steps}
+                "gpu_launches": sum(pg.kernel_launches for pg in progs) * args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

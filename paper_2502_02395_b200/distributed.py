@@ -197,22 +197,26 @@ def _solve_halo_blocks(plan):
     return out
 
 
+def run_exchange(plan, seg):
+    kind, l = seg
+    if plan.comm.host_staged:
+        torch.cuda.current_stream(plan.device).synchronize()
+    if kind == "halo_v":
+        _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l)
+    elif kind == "boundary":
+        _exchange_blocks(plan, _boundary_blocks(plan, l), "factor", l)
+    elif kind == "solve_halo":
+        _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1)
+    else:
+        raise ValueError(f"unknown exchange {kind}")
+
+
 def run_segments(plan, stream=None):
     for seg in plan.segments:
         if isinstance(seg, Program):
             seg.launch(stream)
-            continue
-        kind, l = seg
-        torch.cuda.current_stream(plan.device).synchronize()
-        if kind == "halo_v":
-            _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l)
-        elif kind == "boundary":
-            _exchange_blocks(plan, _boundary_blocks(plan, l), "factor", l)
         else:
-            raise ValueError(f"unknown exchange {kind}")
-    if plan.part is not None and plan.part.p > 1:
-        torch.cuda.current_stream(plan.device).synchronize()
-        _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1)
+            run_exchange(plan, seg)
 
 
 # --------------------------------------------------------------------------- public API

@@ -240,6 +240,9 @@ class FactorPlan:
         self.flops = flop_report({l: (B.lay.n, B.lay.k, B.lay.off_pairs) for l, B in self.bufs.items()},
                                  self.root_dim)
         self.audit = self._audit()
+        if self.part is not None and self.part.p > 1 and depth >= 1:
+            # cross-owner off-diagonal factor blocks also go to the column box's owner (solve)
+            prog = self._cut(prog, ("solve_halo", -1))
         self.segments.append(prog.finalize())
         self.program = self.segments[0] if len(self.segments) == 1 else None
 
