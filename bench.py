@@ -197,7 +197,7 @@ def run_reference(args, c, key):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
@@ -312,13 +312,17 @@ def main():
                         "count": int(st["count"]), "grid": int(st["grid"])}
                        for (kd, fl, by), t, st in zip(work, step_ms, steps_arr)], fh)
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-    traffic = None
+    traffic = traffic_note = None
     tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tfile):
         with open(tfile) as fh:
-            traffic = json.load(fh).get(args.config)
+            tr = json.load(fh).get(args.config)
+        if tr:
+            traffic = tr["bytes"]
+            traffic_note = (f"{tr['launch']}; algorithmic bytes of that launch {tr['algorithmic_bytes']} "
+                            f"({tr['source']})")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_note": traffic_note,
                 "kernel": "gemm_grouped_kernel (FP64 DMMA.8x8x4)",
                 "peak_source": "measured FP64 DMMA issue peak (profiles/r01_fp64_peak.txt); "
                                "cuBLAS DGEMM 8192^3 = 35.5 TFLOP/s",

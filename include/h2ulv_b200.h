@@ -94,6 +94,35 @@ typedef struct h2g_panel_desc {
 
 int h2g_panel_potrf(const h2g_panel_desc* d_descs, int count, int32_t* d_npd, void* stream);
 
+/* ---- panel step of the partial (ULV) Cholesky --------------------------------
+ * For panel q (columns p = 64q .. p+b-1) of every box:
+ *   kernel 1, one CTA per descriptor: apply the previous panel's update
+ *      (columns p-64 .. p-1, final L; nothing when p == 0) to the diagonal
+ *      block, factor it: L_pp -> H, L_pp^-1 -> the 64 x 64 block `Linv`,
+ *      pivot status -> d_npd exactly like h2g_panel_potrf;
+ *   kernel 2, one CTA per 64-row chunk of the rows below the panel: apply
+ *      the previous panel's update to the chunk rows, then X <- X L_pp^-T.
+ * The update of the columns >= p+b+64 by the previous panel (REST) is left
+ * to a grouped GEMM issued before this step, so the factorization's critical
+ * lane issues two kernels per panel (ulv_factor.py:217-241).  Chunks per
+ * box: h2g_chol_panel_tiles (0 when nothing is below); d_tile_map[t] =
+ * descriptor of chunk CTA t, tile_start = its first chunk CTA.
+ */
+typedef struct h2g_chol_panel_desc {
+  double* H;          /* n x n, row-major, ld ldh (lower triangle used) */
+  double* Linv;       /* 64 x 64 output, ld ldl */
+  int32_t ldh, ldl;
+  int32_t n;          /* rows of H */
+  int32_t p, b;       /* panel start column (multiple of 64) and width (1..64) */
+  int32_t npd_slot;
+  int32_t tile_start;
+  int32_t pad_;
+} h2g_chol_panel_desc;
+
+int h2g_chol_panel_tiles(int n, int p, int b);
+int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map, int total_tiles,
+                   int32_t* d_npd, void* stream);
+
 /* ---- block copy / gather ----------------------------------------------------
  * dst[r, c] = src(r, c) for an rows x cols block, where src(r, c) is
  *   mode 0: src[r*lds + c]            (copy)
@@ -250,6 +279,7 @@ enum {
   H2G_STEP_GEMV = 9,     /* descs = outs, map = terms, grid = chunks, arg = w */
   H2G_STEP_TRSV = 10,    /* descs = trsv descs, grid = w, arg = trans      */
   H2G_STEP_NOP = 12,     /* no kernel: carries a lane's event wait / record  */
+  H2G_STEP_CHOL_PANEL = 13, /* descs/map = chol panel descs/tile map; npd = status */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */
@@ -265,15 +295,18 @@ typedef struct h2g_step {
   int32_t* npd;       /* PANEL: device pivot-status array */
   const void* aux;    /* KBLOCK: device points (N x 3) */
   double d0, d1;      /* KBLOCK: shift, decay */
-  int32_t lane;       /* 0: the caller's stream, 1: the context's side stream */
+  int32_t lane;       /* 0: the caller's stream, 1..4: the context's side streams */
   int32_t wait_ev;    /* event index to wait on before the step, or -1 */
   int32_t rec_ev;     /* event index to record after the step, or -1 */
   int32_t pad_;
 } h2g_step;
 
-/* Execution context of a two-lane program: a side stream and n_events events
- * (look-ahead: e.g. the trailing update of Cholesky panel q runs on lane 1
- * while panel q+1 is factored on lane 0).  With ctx == NULL every step runs
+/* Execution context of a multi-lane program: four side streams (lanes 1..4)
+ * and n_events events.  The factorization uses lane 0 for the critical
+ * chain (diagonal transform, Cholesky panels, merge), lane 1 for the
+ * look-ahead trailing updates, lane 4 for the V ride-along, lane 2 for the
+ * chain-independent off-diagonal skeleton products and lane 3 for the
+ * deferred off-diagonal factor blocks (only the solve reads them).  With ctx == NULL every step runs
  * on `stream` in order. */
 int h2g_exec_ctx_create(int n_events, void** ctx_out);
 int h2g_exec_ctx_destroy(void* ctx);

@@ -63,6 +63,8 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_KBLOCK:
       return h2g_kernel_blocks((const h2g_kblock_desc*)s.descs, s.map, s.grid, (const double*)s.aux, s.arg,
                                s.d0, s.d1, (int64_t*)s.npd, st);
+    case H2G_STEP_CHOL_PANEL:
+      return h2g_chol_panel((const h2g_chol_panel_desc*)s.descs, s.count, s.map, s.grid, s.npd, st);
     case H2G_STEP_NOP:
       return H2G_OK;
     default:
@@ -70,18 +72,22 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
   }
 }
 
+constexpr int kMaxLanes = 5;   // lane 0 = the caller's stream, lanes 1..4 = side streams
+
 struct ExecCtx {
-  cudaStream_t side = nullptr;
+  cudaStream_t side[kMaxLanes] = {};   // side[0] unused
   std::vector<cudaEvent_t> ev;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join[kMaxLanes] = {};
 };
 
 extern "C" int h2g_exec_ctx_create(int n_events, void** ctx_out) {
   if (!ctx_out || n_events < 0) return h2g_set_error(H2G_EINVAL, "h2g_exec_ctx_create: bad arguments");
   ExecCtx* c = new ExecCtx();
-  cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
+  cudaError_t e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  for (int l = 1; l < kMaxLanes && e == cudaSuccess; ++l) {
+    e = cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[l], cudaEventDisableTiming);
+  }
   c->ev.resize(n_events, nullptr);
   for (int i = 0; i < n_events && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -98,8 +104,10 @@ extern "C" int h2g_exec_ctx_destroy(void* ctx) {
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->fork) cudaEventDestroy(c->fork);
-  if (c->join) cudaEventDestroy(c->join);
-  if (c->side) cudaStreamDestroy(c->side);
+  for (int l = 1; l < kMaxLanes; ++l) {
+    if (c->join[l]) cudaEventDestroy(c->join[l]);
+    if (c->side[l]) cudaStreamDestroy(c->side[l]);
+  }
   delete c;
   return H2G_OK;
 }
@@ -108,17 +116,22 @@ extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, 
   if (nsteps < 0 || (nsteps > 0 && !steps)) return h2g_set_error(H2G_EINVAL, "h2g_run_program: bad steps");
   cudaStream_t main_st = (cudaStream_t)stream;
   ExecCtx* c = (ExecCtx*)ctx;
-  bool two = false;
-  if (c)
-    for (int i = 0; i < nsteps; ++i) two |= steps[i].lane == 1;
-  if (two) {  // fork: the side lane starts after everything already queued on main
+  bool used[kMaxLanes] = {true};
+  bool multi = false;
+  for (int i = 0; i < nsteps; ++i) {
+    const int ln = steps[i].lane;
+    if (ln < 0 || ln >= kMaxLanes) return h2g_set_error(H2G_EINVAL, "step %d: bad lane %d", i, ln);
+    if (ln > 0 && c) used[ln] = multi = true;
+  }
+  if (multi) {  // fork: the side lanes start after everything already queued on main
     cudaEventRecord(c->fork, main_st);
-    cudaStreamWaitEvent(c->side, c->fork, 0);
+    for (int l = 1; l < kMaxLanes; ++l)
+      if (used[l]) cudaStreamWaitEvent(c->side[l], c->fork, 0);
   }
   for (int i = 0; i < nsteps; ++i) {
     const h2g_step& sp = steps[i];
-    cudaStream_t st = (two && sp.lane == 1) ? c->side : main_st;
-    if (two && sp.wait_ev >= 0) {
+    cudaStream_t st = (multi && sp.lane > 0) ? c->side[sp.lane] : main_st;
+    if (multi && sp.wait_ev >= 0) {
       if (sp.wait_ev >= (int)c->ev.size()) return h2g_set_error(H2G_EINVAL, "step %d: bad wait event", i);
       cudaStreamWaitEvent(st, c->ev[sp.wait_ev], 0);
     }
@@ -128,14 +141,17 @@ extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, 
       snprintf(buf, sizeof(buf), "%.380s", g_err);
       return h2g_set_error(rc, "step %d (kind %d): %s", i, sp.kind, buf);
     }
-    if (two && sp.rec_ev >= 0) {
+    if (multi && sp.rec_ev >= 0) {
       if (sp.rec_ev >= (int)c->ev.size()) return h2g_set_error(H2G_EINVAL, "step %d: bad record event", i);
       cudaEventRecord(c->ev[sp.rec_ev], st);
     }
   }
-  if (two) {  // join: main continues only after the side lane drained
-    cudaEventRecord(c->join, c->side);
-    cudaStreamWaitEvent(main_st, c->join, 0);
+  if (multi) {  // join: main continues only after every side lane drained
+    for (int l = 1; l < kMaxLanes; ++l)
+      if (used[l]) {
+        cudaEventRecord(c->join[l], c->side[l]);
+        cudaStreamWaitEvent(main_st, c->join[l], 0);
+      }
   }
   return H2G_OK;
 }

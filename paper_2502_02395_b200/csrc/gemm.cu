@@ -38,6 +38,7 @@ struct GemmCfg {
 using Cfg64 = GemmCfg<64, 64, 2, 2, 1, 3>;      // 3 CTAs/SM (smem-bound), 3 stages
 using Cfg128 = GemmCfg<128, 128, 2, 4, 1, 3>;
 using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // 4 CTAs/SM, <= 128 registers, 2 stages
+using Cfg64k3 = GemmCfg<64, 64, 2, 2, 3, 3>;    // 3 CTAs/SM, 3 stages (m16n8k16 path)
 
 template <class C, bool TA, bool TB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
@@ -189,6 +190,179 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
 }
 
+// Same tiling with the m16n8k16 FP64 MMA (one instruction per 16x8x16 block):
+// warp tile 32x32 = 2 x 4 MMAs per 16-deep k step.
+template <class C, bool TA, bool TB>
+__global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_kernel(const h2g_gemm_problem* __restrict__ probs,
+                                                                      const int32_t* __restrict__ tile_map) {
+  static_assert(C::WM == 32 && C::WN == 32, "k16 path: 32x32 warp tiles");
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + C::STAGES * C::A_DBL;
+  constexpr int tBM = C::TBM, tBN = C::TBN, wn_count = C::NWARP_N;
+
+  const int tile = blockIdx.x;
+  const int pi = tile_map[tile];
+  const h2g_gemm_problem P = probs[pi];
+  int t = tile - P.tile_start;
+  int tm, tn;
+  if (P.flags & H2G_GEMM_LOWER) {
+    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    tm = i;
+    tn = t - i * (i + 1) / 2;
+  } else {
+    int ntn = (P.N + tBN - 1) / tBN;
+    tm = t / ntn;
+    tn = t - tm * ntn;
+  }
+  const int m0 = tm * tBM, n0 = tn * tBN;
+  const int M = P.M, N = P.N, K = P.K;
+  const double* __restrict__ A = P.A;
+  const double* __restrict__ B = P.B;
+  const int lda = P.lda, ldb = P.ldb;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp / wn_count, wn = warp % wn_count;
+
+  double acc[2][4][4];
+  double* Cp = P.C;
+  const int ldc = P.ldc;
+  const double alpha = P.alpha, beta = P.beta;
+  const double cscale = (beta != 0.0 && alpha != 0.0) ? beta / alpha : 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = m0 + wm * 32 + i * 16 + g + 8 * (e >> 1);
+        const int col = n0 + wn * 32 + j * 8 + 2 * tq + (e & 1);
+        double v = 0.0;
+        if (cscale != 0.0 && row < M && col < N) v = cscale * Cp[(size_t)row * ldc + col];
+        acc[i][j][e] = v;
+      }
+
+  auto load_stage = [&](int stage, int k0) {
+    double* as = As + stage * C::A_DBL;
+    double* bs = Bs + stage * C::B_DBL;
+#pragma unroll
+    for (int jj = 0; jj < (tBM * BK) / C::THREADS; ++jj) {
+      int idx = tid + jj * C::THREADS;
+      if (!TA) {
+        int m = idx / BK, k = idx % BK;
+        int gm = m0 + m, gk = k0 + k;
+        bool v = gm < M && gk < K;
+        cp_async8(as + m * C::S_MK + k, v ? A + (size_t)gm * lda + gk : A, v);
+      } else {
+        int k = idx / tBM, m = idx % tBM;
+        int gm = m0 + m, gk = k0 + k;
+        bool v = gm < M && gk < K;
+        cp_async8(as + k * C::SA_KM + m, v ? A + (size_t)gk * lda + gm : A, v);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < (tBN * BK) / C::THREADS; ++jj) {
+      int idx = tid + jj * C::THREADS;
+      if (!TB) {
+        int k = idx / tBN, n = idx % tBN;
+        int gn = n0 + n, gk = k0 + k;
+        bool v = gn < N && gk < K;
+        cp_async8(bs + k * C::SB_KN + n, v ? B + (size_t)gk * ldb + gn : B, v);
+      } else {
+        int n = idx / BK, k = idx % BK;
+        int gn = n0 + n, gk = k0 + k;
+        bool v = gn < N && gk < K;
+        cp_async8(bs + n * C::S_MK + k, v ? B + (size_t)gn * ldb + gk : B, v);
+      }
+    }
+  };
+
+  const int KT = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + C::STAGES - 1;
+      if (nk < KT) load_stage(nk % C::STAGES, nk * BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % C::STAGES) * C::A_DBL;
+    const double* bs = Bs + (kt % C::STAGES) * C::B_DBL;
+    double af[2][8], bf[4][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int m = wm * 32 + i * 16 + g + 8 * (e & 1), k = tq + 4 * (e >> 1);
+        af[i][e] = TA ? as[k * C::SA_KM + m] : as[m * C::S_MK + k];
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int n = wn * 32 + j * 8 + g, k = tq + 4 * e;
+        bf[j][e] = TB ? bs[n * C::S_MK + k] : bs[k * C::SB_KN + n];
+      }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma16816(acc[i][j], af[i], bf[j]);
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = m0 + wm * 32 + i * 16 + g + 8 * h;
+      if (row >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = n0 + wn * 32 + j * 8 + 2 * tq;
+        double* cp = Cp + (size_t)row * ldc + col;
+        if (alpha == 0.0) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (col + e < N) cp[e] = beta * cp[e];
+          continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (col + e < N) cp[e] = alpha * acc[i][j][2 * h + e];
+      }
+    }
+}
+
+template <class C, bool TA, bool TB>
+static int launch_gemm_k16(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_grouped_k16_kernel<C, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  gemm_grouped_k16_kernel<C, TA, TB><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map);
+  return h2g_check_launch("gemm_grouped_k16");
+}
+
+template <class C>
+static int dispatch_k16(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles,
+                        cudaStream_t s) {
+  if (!trans_a && !trans_b) return launch_gemm_k16<C, false, false>(d_probs, d_map, tiles, s);
+  if (!trans_a && trans_b) return launch_gemm_k16<C, false, true>(d_probs, d_map, tiles, s);
+  if (trans_a && !trans_b) return launch_gemm_k16<C, true, false>(d_probs, d_map, tiles, s);
+  return launch_gemm_k16<C, true, true>(d_probs, d_map, tiles, s);
+}
+
 template <class C, bool TA, bool TB>
 static int launch_gemm(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s) {
   static bool attr_set = false;
@@ -213,7 +387,7 @@ static int dispatch(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, c
 
 extern "C" int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg) {
   if (M <= 0 || N <= 0) return 0;
-  const int T = tile_cfg == 1 ? 128 : 64;
+  const int T = tile_cfg == 1 ? 128 : 64;   // cfg 0, 2, 3, 4: 64x64 tiles
   if (flags & H2G_GEMM_LOWER) {
     int t = (M + T - 1) / T;
     return t * (t + 1) / 2;
@@ -228,6 +402,8 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   cudaStream_t s = (cudaStream_t)stream;
   if (tile_cfg == 1) return h2g::dispatch<h2g::Cfg128>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 2) return h2g::dispatch<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 3) return h2g::dispatch_k16<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 4) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg != 0) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d", tile_cfg);
   return h2g::dispatch<h2g::Cfg64>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
 }

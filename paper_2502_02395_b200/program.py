@@ -54,7 +54,7 @@ class Program:
         self.graph = None
         self.kernel_launches = 0
         self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
-        self.lane = 0         # lane of the steps added next (0: caller's stream, 1: side stream)
+        self.lane = 0         # lane of the steps added next (0: caller's stream, 1..4: side streams)
         self.n_events = 0
         self.ctx = None
 
@@ -72,7 +72,7 @@ class Program:
                                 arg=int(arg), aux=aux, d0=float(d0), d1=float(d1), lane=self.lane,
                                 wait=int(wait), rec=int(rec)))
 
-    # -- two-lane scheduling ----------------------------------------------------------
+    # -- multi-lane scheduling ----------------------------------------------------------
     def event(self):
         self.n_events += 1
         return self.n_events - 1
@@ -122,6 +122,26 @@ class Program:
                   flops=int((b64 ** 3 // 3 + b64 ** 3 // 3).sum()))
         return len(descs)
 
+    def chol_panel(self, descs, npd_ptr):
+        """descs: list of (H, Linv, ldh, ldl, n, p, b, npd_slot): one diag CTA per box plus one
+        CTA per 64-row chunk below the panel (h2g_chol_panel)."""
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.CHOLP_DT)
+        for name, col in zip(("H", "Linv", "ldh", "ldl", "n", "p", "b", "npd_slot"), zip(*descs)):
+            arr[name] = col
+        below = (arr["n"].astype(np.int64) - arr["p"] - arr["b"]).clip(min=0)
+        tiles = -(-below // nat.PANEL_WIDTH)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        b64 = arr["b"].astype(np.int64)
+        # useful flops: previous-panel update of block column p (K = 64) + chol + TRSM of the rows below
+        upd = np.where(arr["p"] > 0, (b64 * (b64 + 1) + 2 * below * b64) * nat.PANEL_WIDTH, 0)
+        fl = int((upd + b64 ** 3 // 3 + below * b64 * b64).sum())
+        self._add(nat.STEP["CHOL_PANEL"], len(descs), int(tiles.sum()), self._blob(arr),
+                  self._blob(tmap) if tmap.size else -1, npd=npd_ptr, flops=fl)
+        return int(tiles.sum())
+
     def copy(self, descs):
         """descs: list of (src, dst, rows, cols, lds, ldd, mode)."""
         rows = [d for d in descs if d[2] > 0 and d[3] > 0]
@@ -139,8 +159,13 @@ class Program:
         return int(tiles.sum())
 
     def memcpy(self, dst_ptr, src_ptr, nbytes):
-        if nbytes > 0:
-            self._add(nat.STEP["MEMCPY"], int(nbytes), 0, ("raw", dst_ptr), ("raw", src_ptr), nbytes=2 * int(nbytes))
+        """Device-to-device copy (split into <= 1 GiB steps: the step count is int32)."""
+        nbytes = int(nbytes)
+        off = 0
+        while off < nbytes:
+            sz = min(nbytes - off, 1 << 30)
+            self._add(nat.STEP["MEMCPY"], sz, 0, ("raw", dst_ptr + off), ("raw", src_ptr + off), nbytes=2 * sz)
+            off += sz
 
     def qr_panel(self, descs):
         """descs: list of (Z, V, tau, T, n, ldz, p, b)."""
@@ -244,8 +269,10 @@ class Program:
             steps[q]["wait_ev"] = st["wait"]
             steps[q]["rec_ev"] = st["rec"]
         self.steps = steps
-        self.kernel_launches = int(sum(1 for st in self._steps
-                                      if st["kind"] not in (nat.STEP["MEMCPY"], nat.STEP["NOP"])))
+        # CHOL_PANEL issues a diag kernel plus, when rows lie below the panel, a row-chunk kernel
+        self.kernel_launches = int(sum((2 if st["kind"] == nat.STEP["CHOL_PANEL"] and st["grid"] > 0 else 1)
+                                       for st in self._steps
+                                       if st["kind"] not in (nat.STEP["MEMCPY"], nat.STEP["NOP"])))
         if any(st["lane"] for st in self._steps):
             ctx = ctypes.c_void_p()
             nat.check(nat.lib().h2g_exec_ctx_create(max(self.n_events, 1), ctypes.byref(ctx)), "h2g_exec_ctx_create")

@@ -7,20 +7,27 @@ factor, `merge_map`, the flop report and the write audit.  The blocks stay
 in HBM; the numpy views materialize lazily on first access.
 
 Per level l (fine to coarse) the whole level is a handful of batched launches
-(one `Program`, optionally one CUDA graph for the entire factorization):
+on five lanes (CUDA streams joined by events; the whole factorization is one
+`Program`, replayed as one CUDA graph):
 
-  R <- Q (device copy)                       q_full kept for the solve
-  GEMM NN   M_i = A_ii Q_i                   diag_mul1 (ulv_factor.py:189-194)
-  GEMM TN   H_i = Q_i^T M_i                  diag_mul2 (195-200)
-  for p in 0, 64, ...:                       partial Cholesky of H_i (217-241):
-    PANEL   chol(H[p:p+b,p:p+b]); rows below and R rows <- X L^-T
-    GEMM NT trailing update (lower tiles of H, and R[:, p+b:r])
-            -> H = [[L(r)], [L(s)_ii, SS_ii - L(s) L(s)^T]],  R = [V_i | q_skel_i]
-  GEMM NN   MO_ij = A_ij [V_j | q_skel_j]    off_mul1 (243-253)
-  GEMM TN   T_ij  = Q_i^T MO_ij              off_mul2 (254-259)
-            L(s)_ji = (A_ij q_skel_j)^T V_i  = (L(r)_ii^-1 RS_ij)^T  off_mirror (282-286)
-  COPY      parent near blocks <- 2x2 child SS / couplings           merge (289-303)
+  lane 2  GEMM NN  MO_ij[:, r_j:] = A_ij q_skel_j                     off_mul1, skeleton part
+          GEMM TN  SS_ij = q_skel_i^T MO_ij[:, r_j:]                   off_mul2, skeleton part
+  lane 0  R <- Q (device copy); GEMM NN M_i = A_ii Q_i; TN H_i = Q_i^T M_i   diag_mul1/2 (189-200)
+          for p in 0, 64, ...: PANEL chol(H[p:p+b,p:p+b]) + inverse; TRSM of the rows below;
+                               NEXT = update of the next block column          partial Cholesky
+  lane 1  REST = the remaining trailing update (lower tiles)             (217-241): H becomes
+  lane 4  V ride-along: R[:, :r] <- q_red L^-T panel by panel            [[L(r)],[L(s), SS - L(s)L(s)^T]]
+  lane 3  (deferred, only the solve reads it)
+          GEMM NN  MO_ij[:, :r_j] = A_ij V_j ; GEMM TN T_ij[:, :r_j] = Q_i^T MO  -> lr_off, L(s)_ij
+          GEMM TN  L(s)_ji = (A_ij q_skel_j)^T V_i = (L(r)_ii^-1 RS_ij)^T        off_mirror (282-286)
+  lane 0  COPY parent near blocks <- 2x2 child SS / couplings             merge (289-303)
 root: the same PANEL/GEMM loop on the merged d x d block (309-314).
+
+Only the diagonal transform, the Cholesky panels and the merge are on the
+critical path: the off-diagonal skeleton blocks SS_ij = q_skel_i^T A_ij
+q_skel_j do not depend on the level's Cholesky (lane 2 runs them as soon as
+the parent blocks exist), and the remaining off-diagonal factor blocks are
+not read by the next level at all (lane 3 overlaps them with it).
 
 `batched` is accepted for signature compatibility: there is only the batched
 GPU path, and it is deterministic (no atomics in any reduction), so repeated
@@ -148,6 +155,7 @@ class FactorPlan:
         prog.memcpy(self.npd.data_ptr(), self._npd_init.data_ptr(), 4 * (acc + 1))
         self.bufs = {}
         self.merge_pairs = {}
+        self._keep = []
 
         if depth == 0:
             d = int(dh2.root_a.shape[0])
@@ -157,6 +165,7 @@ class FactorPlan:
             self._cholesky_steps(prog, self.root_buf.data_ptr(), d, d, self.slot_base[0])
         else:
             a_buf, a_off = dh2.leaf_a, dh2.aoff
+            merge_ev = None
             for l in range(depth, 0, -1):
                 lay = dh2.levels[l]
                 B = _LevelBuffers()
@@ -176,8 +185,38 @@ class FactorPlan:
                 for (i, j) in lay.near_pairs:
                     if (i, j) not in a_off and mine[i]:
                         raise StructureError(f"missing near block ({l}, {i}, {j})")
-                # ---- diagonal phase
+                # ---- off-diagonal skeleton products (lane 2): chain-independent, needed by the merge
+                #   MO[:, r_j:] = A_ij q_skel_j            (kept: the mirror's left operand)
+                #   T[r_i:, r_j:] = q_skel_i^T MO[:, r_j:] = SS_ij
+                offp = lay.off_pairs
+                B.toff, B.lsoff = {}, {}
+                tacc = lacc = 0
+                for (i, j) in offp:
+                    B.toff[(i, j)] = tacc
+                    tacc += int(n[i] * n[j])
+                    B.lsoff[(i, j)] = lacc
+                    lacc += int(k[j] * r[i])
+                B.MO = torch.empty(max(tacc, 1), dtype=F64, device=dev)
+                B.T = torch.empty(max(tacc, 1), dtype=F64, device=dev)
+                B.LSm = torch.empty(max(lacc, 1), dtype=F64, device=dev)
+                MOp, Tp, LSp = B.MO.data_ptr(), B.T.data_ptr(), B.LSm.data_ptr()
+                own_off = [(i, j) for (i, j) in offp if mine[i]]
+                prog.lane = 2
+                if merge_ev is not None:
+                    prog.wait(merge_ev)
+                prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], qp + 8 * (qo[j] + r[j]), MOp + 8 * (B.toff[(i, j)] + r[j]),
+                                  int(n[i]), int(k[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
+                                 for (i, j) in own_off])
+                prog.gemm(1, 0, [(qp + 8 * (qo[i] + r[i]), MOp + 8 * (B.toff[(i, j)] + r[j]),
+                                  Tp + 8 * (B.toff[(i, j)] + r[i] * n[j] + r[j]),
+                                  int(k[i]), int(k[j]), int(n[i]), int(n[i]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
+                                 for (i, j) in own_off])
+                ev_ss = prog.event()
+                prog.record(ev_ss)
+                # ---- diagonal phase (lane 0 = the critical chain)
+                prog.lane = 4                   # R <- Q for the V ride-along, off the critical lane
                 prog.memcpy(Rp, qp, 8 * lay.qsize)
+                prog.lane = 0
                 prob = []
                 for i in range(nb):
                     if not mine[i]:
@@ -191,47 +230,41 @@ class FactorPlan:
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
                          int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
                 prog.gemm(1, 0, prob)
-                B.linv, B.loff = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine)
-                # ---- off-diagonal phase
-                offp = lay.off_pairs
-                B.toff, B.lsoff = {}, {}
-                tacc = lacc = 0
-                for (i, j) in offp:
-                    B.toff[(i, j)] = tacc
-                    tacc += int(n[i] * n[j])
-                    B.lsoff[(i, j)] = lacc
-                    lacc += int(k[j] * r[i])
-                B.MO = torch.empty(max(tacc, 1), dtype=F64, device=dev)
-                B.T = torch.empty(max(tacc, 1), dtype=F64, device=dev)
-                B.LSm = torch.empty(max(lacc, 1), dtype=F64, device=dev)
-                MOp, Tp, LSp = B.MO.data_ptr(), B.T.data_ptr(), B.LSm.data_ptr()
+                B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine)
                 if self.distributed_level(l):
                     # V_j of boxes owned elsewhere but coupled to mine by a near pair
                     prog = self._cut(prog, ("halo_v", l))
+                    ev_v = ev_ss = None          # the cut joined every lane
+                # ---- deferred off-diagonal factor blocks (lane 3): read only by the solve
+                #   MO[:, :r_j] = A_ij V_j
+                #   T[:, :r_j]  = Q_i^T MO[:, :r_j]        -> lr_off (rows < r_i), L(s)_ij (rows >= r_i)
+                #   L(s)_ji     = (A_ij q_skel_j)^T V_i     = (L(r)_ii^-1 RS_ij)^T   off_mirror (282-286)
+                prog.lane = 3
+                for ev in (ev_v, ev_ss):
+                    if ev is not None:
+                        prog.wait(ev)
+                prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], Rp + 8 * qo[j], MOp + 8 * B.toff[(i, j)],
+                                  int(n[i]), int(r[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
+                                 for (i, j) in own_off])
                 prob = []
-                for (i, j) in offp:
-                    if not mine[i]:
-                        continue
-                    ni, nj = int(n[i]), int(n[j])
-                    prob.append((ap + 8 * a_off[(i, j)], Rp + 8 * qo[j], MOp + 8 * B.toff[(i, j)], ni, nj, nj,
-                                 nj, nj, nj, 0, 1.0, 0.0))
-                prog.gemm(0, 0, prob)
-                prob = []
-                for (i, j) in offp:
-                    if not mine[i]:
-                        continue
+                for (i, j) in own_off:
                     ni, nj, ri, rj, kj = int(n[i]), int(n[j]), int(r[i]), int(r[j]), int(k[j])
                     mo = MOp + 8 * B.toff[(i, j)]
-                    prob.append((qp + 8 * qo[i], mo, Tp + 8 * B.toff[(i, j)], ni, nj, ni, ni, nj, nj, 0, 1.0, 0.0))
-                    # mirror: L(s)_ji = (A_ij q_skel_j)^T V_i   (k_j x r_i)
+                    prob.append((qp + 8 * qo[i], mo, Tp + 8 * B.toff[(i, j)], ni, rj, ni, ni, nj, nj, 0, 1.0, 0.0))
                     prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
                                  0, 1.0, 0.0))
                 prog.gemm(1, 0, prob)
+                prog.lane = 0
                 if self.distributed_level(l) and not self.distributed_level(l - 1):
                     # boundary: the parent level is replicated -> every rank needs all SS blocks
                     prog = self._cut(prog, ("boundary", l))
+                    ev_ss = None
                 # ---- merge into the parent level (or the root)
+                if ev_ss is not None:
+                    prog.wait(ev_ss)
                 a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2)
+                merge_ev = prog.event()
+                prog.record(merge_ev)
             d = self._root_d
             self.root_dim = d
             self.root_buf = a_buf
@@ -264,17 +297,21 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None):
-        """Right-looking partial Cholesky of every box's H (and V rows in R),
-        panels of W = 64 columns, with a look-ahead of one panel:
+        """Right-looking partial Cholesky of every box's H (and the V ride-along
+        rows in R), panels of W = 64 columns, one fused kernel per panel on the
+        critical lane:
 
-          lane 0:  DIAG(q) -> TRSM(q) -> [wait REST(q-1)] -> NEXT(q) -> DIAG(q+1) ...
-          lane 1:                [wait TRSM(q)] -> REST(q)
+          lane 0:  [wait REST(q-2)] -> PANEL(q) -> [wait REST(q-1)] -> PANEL(q+1) ...
+          lane 1:          [wait PANEL(q)] -> REST(q)
+          lane 4:          [wait PANEL(q)] -> RTRSM(q) -> RUPD(q)
 
-        DIAG = chol + inverse of the 64x64 diagonal block, TRSM = in-place GEMM
-        with L_pp^-T, NEXT = trailing update of the next block column only,
-        REST = trailing update of everything right of it (lower tiles of H,
-        R[:, ...]).  The factorization of panel q+1 thus overlaps the bulk of
-        panel q's trailing update."""
+        PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
+        panel q-1 to block column q, factors the diagonal block and TRSMs the
+        rows below; REST(q) applies panel q to
+        everything right of block column q+1 (lower tiles of H).  RTRSM / RUPD
+        apply the panel to the V rows R = q_red (V = q_red L^-T), off the
+        critical lane.  Returns (linv, loff, event after the last R update or
+        None)."""
         nb = len(n)
         mine = np.ones(nb, dtype=bool) if mine is None else mine
         rmax = int(np.asarray(r)[mine].max()) if mine.any() else 0
@@ -283,64 +320,66 @@ class FactorPlan:
         loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
         linv = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=self.device)
         if rmax == 0:
-            return linv, loff
+            return linv, loff, None
         lp = linv.data_ptr()
-        rest_done = None
-        for p in range(0, rmax, W):
-            descs, trsm, nxt, rest = [], [], [], []
+        rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
+        for q, p in enumerate(range(0, rmax, W)):
+            descs, rest, rtrsm, rupd = [], [], [], []
             for i in range(nb):
                 ri, ni = int(r[i]), int(n[i])
                 if ri <= p or not mine[i]:
                     continue
                 b = min(W, ri - p)
                 h = Hp + 8 * int(qo[i])
-                li = lp + 8 * (int(loff[i]) + p // W) * W * W
-                descs.append((h, li, ni, W, p, b, slot0 + i))
-                m = ni - p - b                       # rows below the panel
-                pan = h + 8 * ((p + b) * ni + p)     # H[p+b:, p:p+b]
-                q0 = p + b                           # first trailing column
-                if m > 0:
-                    trsm.append((pan, li, pan, m, b, b, ni, W, ni, 0, 1.0, 0.0))
-                    wn = min(W, ni - q0)             # next block column of H
-                    nxt.append((pan, pan, h + 8 * (q0 * ni + q0), m, wn, b, ni, ni, ni, 0, -1.0, 1.0))
-                    mr = m - wn                      # the rest, lower tiles
-                    if mr > 0:
-                        pr = pan + 8 * wn * ni
-                        rest.append((pr, pr, h + 8 * ((q0 + wn) * ni + q0 + wn), mr, mr, b, ni, ni, ni,
-                                     nat.GEMM_LOWER, -1.0, 1.0))
+                li = lp + 8 * (int(loff[i]) + q) * W * W
+                descs.append((h, li, ni, W, ni, p, b, slot0 + i))
+                q0 = p + b                               # first column right of the panel
+                c0 = q0 + (min(W, ri - q0) if ri > q0 else 0)   # right of the next panel
+                if ni > c0:
+                    x = h + 8 * (c0 * ni + p)            # panel rows c0.. : H[c0:, p:p+b]
+                    rest.append((x, x, h + 8 * (c0 * ni + c0), ni - c0, ni - c0, b, ni, ni, ni,
+                                 nat.GEMM_LOWER, -1.0, 1.0))
                 if Rp:
                     rr = Rp + 8 * int(qo[i])
-                    trsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
-                    rn = min(W, ri - q0)
-                    if rn > 0:
-                        nxt.append((rr + 8 * p, pan, rr + 8 * q0, ni, rn, b, ni, ni, ni, 0, -1.0, 1.0))
-                    if ri - q0 - W > 0:
-                        rest.append((rr + 8 * p, pan + 8 * W * ni, rr + 8 * (q0 + W), ni, ri - q0 - W, b, ni, ni, ni,
-                                     0, -1.0, 1.0))
-            prog.panel(descs, self.npd.data_ptr())
-            prog.gemm(0, 1, trsm)
-            ev_trsm = prog.event()
-            prog.record(ev_trsm)
-            if rest_done is not None:
-                prog.wait(rest_done)             # NEXT(q) and REST(q-1) touch the same block column
-            prog.gemm(0, 1, nxt)
+                    rtrsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
+                    if ri - q0 > 0:
+                        pan = h + 8 * (q0 * ni + p)      # L[q0:r, p:p+b]
+                        rupd.append((rr + 8 * p, pan, rr + 8 * q0, ni, ri - q0, b, ni, ni, ni, 0, -1.0, 1.0))
+            done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
+            if done:
+                prog.wait(done[-1])              # block column q has all updates of panels <= q-2
+            prog.chol_panel(descs, self.npd.data_ptr())
+            ev_fp = prog.event()
+            prog.record(ev_fp)
+            ev_rest = None
             if rest:
                 prog.lane = 1
-                prog.wait(ev_trsm)
+                prog.wait(ev_fp)
                 prog.gemm(0, 1, rest)
-                rest_done = prog.event()
-                prog.record(rest_done)
-                prog.lane = 0
-            else:
-                rest_done = None
-        if rest_done is not None:
-            prog.wait(rest_done)
-        return linv, loff
+                ev_rest = prog.event()
+                prog.record(ev_rest)
+            rest_ev.append(ev_rest)
+            if rtrsm:
+                prog.lane = 4
+                prog.wait(ev_fp)
+                prog.gemm(0, 1, rtrsm)
+                prog.gemm(0, 1, rupd)
+            prog.lane = 0
+        ev_v = None
+        if Rp:
+            ev_v = prog.event()
+            prog.lane = 4
+            prog.record(ev_v)
+            prog.lane = 0
+        last = [e for e in rest_ev if e is not None]
+        if last:
+            prog.wait(last[-1])                  # lane 1 is in order: the last REST covers all
+        return linv, loff, ev_v
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
         assert d == ld
-        self.root_linv, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]), np.array([d]),
-                                                         slot)
+        self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]),
+                                                            np.array([d]), slot)
 
     def _merge_steps(self, prog, l, B, lists, dh2):
         lay = B.lay

@@ -1,5 +1,4 @@
-// Standalone timing of the diagonal-block factorization kernel (potrf_diag) with phase tracing.
-#define H2G_DIAG_TRACE 1
+// Standalone timing of the diagonal-block factorization kernel (potrf_diag).
 #include "../../paper_2502_02395_b200/csrc/panel.cu"
 #include <cstdio>
 #include <cstdlib>
@@ -35,11 +34,7 @@ int main(int argc, char** argv) {
     h2g_panel_potrf(dd, nbox, dnpd, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    long long tr[64]; cudaMemcpyFromSymbol(tr, h2g::g_diag_trace, sizeof(tr));
-    printf("rep %d nbox %d: %.1f us | phases (cycles from start):", rep, nbox, ms * 1e3);
-    int idx[] = {1, 2, 3};
-    for (int k : idx) printf(" %d:%lld", k, tr[k] - tr[0]);
-    printf("\n");
+    printf("rep %d nbox %d: %.1f us\n", rep, nbox, ms * 1e3);
   }
   // check: L L^T = D for box 0
   std::vector<double> L(n * n), Li(4096);
