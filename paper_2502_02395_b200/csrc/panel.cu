@@ -32,7 +32,7 @@
 namespace h2g {
 
 #ifdef H2G_PANEL_TRACE
-__device__ long long g_panel_trace[16];
+__device__ long long g_panel_trace[32];
 #define PTRACE(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_panel_trace[k] = clock64(); } while (0)
 #else
 #define PTRACE(k) do { } while (0)
@@ -48,7 +48,7 @@ struct Ldlt {
 };
 
 struct LdltShared {
-  double colX[2][PB], colY[2][PB], rowA[2][PB], rowB[2][PB];
+  double colX[2][PB], colY[2][PB], rowA[2][PB], rowB[2][PB];   // (colX/colY double as Chol16Shared)
   double scal[2][8];
   double pv[PB];
 };
@@ -232,6 +232,215 @@ __device__ void diag_ldlt(double* D, double* Li, int b, LdltShared& sh) {
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ blocked 64x64 factorization
+// diag_blocked: the same result as diag_ldlt (L in D, L^-1 in Li, pivots in
+// pv) with a much shorter critical path.  The block is split into 16x16
+// blocks; each diagonal block is factored by ONE warp entirely in registers
+// (lane i owns row i of the block and row i of its inverse; the pivot row is
+// broadcast with shuffles, so a pivot step is a shuffle + reciprocal + FMA
+// chain with no CTA barrier), and the TRSM of the rows below, the trailing
+// update and the off-diagonal blocks of L^-1 are DMMA work spread over the
+// CTA's 8 warps.  Rows/cols >= b must already hold the identity.
+constexpr int DB = 16;
+
+// 1/d to full double precision without the IEEE division subroutine:
+// MUFU.RCP64H seed + two Newton steps.
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Factor the 16x16 block at blk (lower part read, stride SD) with one warp:
+// L -> blk (zeros above the diagonal), L^-1 -> lblk, pivots -> piv[0..15].
+// Lanes 0..15 hold row i = lane of the working matrix, lanes 16..31 row
+// i = lane - 16 of the inverse V = U^-1 (U unit lower).  Step j broadcasts
+// row j of both through a double-buffered shared-memory row (the owners
+// store it, __syncwarp, every lane reads it with 128-bit broadcast loads):
+// ~20 shared-memory ops per pivot instead of 2 x 34 shuffles.
+struct Chol16Shared {
+  double row[2][2][DB];   // [buffer][half][column]
+  double col[2][DB];      // [buffer][row]: column j of the working matrix
+};
+
+__device__ __forceinline__ void chol16_warp(double* blk, double* lblk, double* piv, Chol16Shared& cs) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane & 15, half = lane >> 4;
+  double x[DB];
+#pragma unroll
+  for (int k = 0; k < DB; ++k) {
+    const double m = k <= i ? blk[i * SD + k] : blk[k * SD + i];   // full symmetric row i
+    x[k] = half ? (k == i ? 1.0 : 0.0) : m;
+  }
+#pragma unroll
+  for (int j = 0; j < DB; ++j) {
+    const int buf = j & 1;
+    if (i == j) {
+#pragma unroll
+      for (int k = 0; k < DB; k += 2)
+        *reinterpret_cast<double2*>(&cs.row[buf][half][k]) = make_double2(x[k], x[k + 1]);
+    }
+    if (!half) cs.col[buf][i] = x[j];
+    __syncwarp();
+    const double d = cs.row[buf][0][j];
+    const double lj = cs.col[buf][i] * fast_rcp(d);
+    const bool act = i > j;
+#pragma unroll
+    for (int k = 0; k < DB; k += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(&cs.row[buf][half][k]);
+      if (act && (half ? (k <= j) : (k > j))) x[k] = fma(-lj, t.x, x[k]);
+      if (act && (half ? (k + 1 <= j) : (k + 1 > j))) x[k + 1] = fma(-lj, t.y, x[k + 1]);
+    }
+    if (act && !half) x[j] = lj;           // multiplier l_ij; lane j keeps its pivot d_j in x[j]
+  }
+  double di = x[0];
+#pragma unroll
+  for (int k = 1; k < DB; ++k)
+    if (k == i) di = x[k];
+  if (!half) cs.col[0][i] = di;
+  __syncwarp();
+  di = cs.col[0][i];
+  const double sqi = sqrt(di), rsqi = fast_rcp(sqi);
+  if (!half) cs.col[1][i] = sqi;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < DB; ++k) {
+    if (!half) blk[i * SD + k] = k < i ? x[k] * cs.col[1][k] : (k == i ? sqi : 0.0);
+    else lblk[i * SD + k] = k <= i ? x[k] * rsqi : 0.0;
+  }
+  if (!half) piv[i] = di;
+  __syncwarp();
+}
+
+// out(8x8 tile at rows m0, cols n0) = sum_k A[m0+.][k] * B[n0+.][k], k < 16 (A, B smem, stride SD)
+__device__ __forceinline__ void tile8_nt16(double (&c)[2], const double* A, const double* B, int g, int tq) {
+  c[0] = c[1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < DB; kk += 4) dmma884(c, A[g * SD + kk + tq], B[g * SD + kk + tq]);
+}
+
+// 256 threads (8 warps).  D, Li: 64 x SD smem; pv: 64 doubles smem.
+__device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  for (int t = tid; t < PB * PB; t += blockDim.x) Li[(t / PB) * SD + t % PB] = 0.0;
+  __syncthreads();
+  PTRACE(16);
+#pragma unroll 1
+  for (int kb = 0; kb < PB / DB; ++kb) {
+    const int c = kb * DB;
+    if (warp == 0) chol16_warp(D + c * SD + c, Li + c * SD + c, pv + c, cs);
+    __syncthreads();
+    PTRACE(17 + 2 * kb);
+    const int R = PB - c - DB;                 // rows below the block
+    if (R == 0) break;
+    // TRSM: X = D[c+16:, c:c+16] <- X Linv_kk^T; 8x8 output tiles (R/8) x 2
+    const int nt = (R / 8) * 2;
+    double x[2][2];
+    int tt[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      tt[u] = warp + 8 * u;
+      if (tt[u] < nt) {
+        const int tm = tt[u] >> 1, tn = tt[u] & 1;
+        tile8_nt16(x[u], D + (c + DB + 8 * tm) * SD + c, Li + (c + 8 * tn) * SD + c, g, tq);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (tt[u] < nt) {
+        const int tm = tt[u] >> 1, tn = tt[u] & 1;
+        double* dst = D + (c + DB + 8 * tm + g) * SD + c + 8 * tn + 2 * tq;
+        dst[0] = x[u][0];
+        dst[1] = x[u][1];
+      }
+    __syncthreads();
+    // trailing update of the lower 8x8 tiles of D[c+16:, c+16:] (K = 16)
+    const int T = R / 8, ntile = T * (T + 1) / 2;
+    for (int t = warp; t < ntile; t += 8) {
+      int tm = 0;
+      while ((tm + 1) * (tm + 2) / 2 <= t) ++tm;
+      const int tn = t - tm * (tm + 1) / 2;
+      double cc[2];
+      tile8_nt16(cc, D + (c + DB + 8 * tm) * SD + c, D + (c + DB + 8 * tn) * SD + c, g, tq);
+      double* dst = D + (c + DB + 8 * tm + g) * SD + c + DB + 8 * tn + 2 * tq;
+      dst[0] -= cc[0];
+      dst[1] -= cc[1];
+    }
+    __syncthreads();
+    PTRACE(18 + 2 * kb);
+  }
+  PTRACE(25);
+  // off-diagonal 16x16 blocks of L^-1, by block diagonals dd = 1..3:
+  //   Linv_IJ = -Linv_II * (sum_{K=J}^{I-1} L_IK Linv_KJ),  I = J + dd
+#pragma unroll 1
+  for (int dd = 1; dd < PB / DB; ++dd) {
+    const int nblk = PB / DB - dd;             // blocks on this block diagonal
+    // phase 1: W_J = sum_K L_IK Linv_KJ (16x16 each, 4 8x8 tiles) -> registers, then smem scratch
+    double w[2][2];
+    int tt[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      tt[u] = warp + 8 * u;
+      w[u][0] = w[u][1] = 0.0;
+      if (tt[u] < nblk * 4) {
+        const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
+        // sum over K = J .. I-1 of L[I,K] (16x16 from D) * Linv[K,J] (16x16 from Li); k runs over K's 16 columns
+        for (int K = J; K < I; ++K) {
+#pragma unroll
+          for (int kk = 0; kk < DB; kk += 4) {
+            const double av = D[(I * DB + 8 * tm + g) * SD + K * DB + kk + tq];
+            const double bv = Li[(K * DB + kk + tq) * SD + J * DB + 8 * tn + g];
+            dmma884(w[u], av, bv);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // stash W in the (zero) upper part of Li: block (J, I) position holds W_J for pair (I, J)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (tt[u] < nblk * 4) {
+        const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
+        double* dst = Li + (J * DB + 8 * tm + g) * SD + I * DB + 8 * tn + 2 * tq;
+        dst[0] = w[u][0];
+        dst[1] = w[u][1];
+      }
+    __syncthreads();
+    // phase 2: Linv_IJ = -Linv_II W
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      w[u][0] = w[u][1] = 0.0;
+      if (tt[u] < nblk * 4) {
+        const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
+#pragma unroll
+        for (int kk = 0; kk < DB; kk += 4) {
+          const double av = Li[(I * DB + 8 * tm + g) * SD + I * DB + kk + tq];
+          const double bv = Li[(J * DB + kk + tq) * SD + I * DB + 8 * tn + g];
+          dmma884(w[u], av, bv);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (tt[u] < nblk * 4) {
+        const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
+        double* dst = Li + (I * DB + 8 * tm + g) * SD + J * DB + 8 * tn + 2 * tq;
+        dst[0] = -w[u][0];
+        dst[1] = -w[u][1];
+        double* scr = Li + (J * DB + 8 * tm + g) * SD + I * DB + 8 * tn + 2 * tq;   // clear the stash
+        scr[0] = scr[1] = 0.0;
+      }
+    __syncthreads();
+  }
+  PTRACE(26);
+}
+
 // First pivot j < b that is not > 0 (or NaN) -> atomicMin(npd[slot], p + j).  Called by warp 0.
 __device__ __forceinline__ void record_npd(const LdltShared& sh, int b, int p, int32_t* npd, int slot) {
   const int lane = threadIdx.x & 31;
@@ -242,17 +451,27 @@ __device__ __forceinline__ void record_npd(const LdltShared& sh, int b, int p, i
 
 // ------------------------------------------------------------------ stand-alone DIAG
 #ifndef H2G_DIAG_BS
-#define H2G_DIAG_BS 2
+#define H2G_DIAG_BS 0   // 0: diag_blocked (default); 2 / 4: diag_ldlt with that register block
 #endif
 constexpr int DIAG_BS = H2G_DIAG_BS;
-constexpr int DIAG_THREADS = (Ldlt<DIAG_BS>::NT + 31) / 32 * 32;
+constexpr int DIAG_THREADS = DIAG_BS == 0 ? 256 : (Ldlt<(DIAG_BS ? DIAG_BS : 2)>::NT + 31) / 32 * 32;
 
-__global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
+// factor the 64x64 block in smem (lower part, rows/cols >= b already identity)
+__device__ __forceinline__ void diag_factor(double* D, double* Li, int b, LdltShared& sh) {
+  if constexpr (DIAG_BS == 0) {
+    diag_blocked(D, Li, sh.pv, *reinterpret_cast<Chol16Shared*>(&sh.colX[0][0]));
+  } else {
+    diag_ldlt<(DIAG_BS ? DIAG_BS : 2)>(D, Li, b, sh);
+  }
+}
+
+__global__ void __launch_bounds__(DIAG_THREADS, 2) potrf_diag_kernel(const h2g_panel_desc* __restrict__ descs,
                                                                   int32_t* __restrict__ npd) {
   extern __shared__ __align__(16) double dsm[];
   double* D = dsm;
   double* Li = dsm + PB * SD;
   LdltShared& sh = *reinterpret_cast<LdltShared*>(dsm + 2 * PB * SD);
+  PTRACE(10);
   const h2g_panel_desc P = descs[blockIdx.x];
   const int p = P.p, b = P.b, ldh = P.ldh;
   double* H = P.H;
@@ -265,7 +484,11 @@ __global__ void __launch_bounds__(DIAG_THREADS) potrf_diag_kernel(const h2g_pane
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  diag_ldlt<DIAG_BS>(D, Li, b, sh);
+  if (threadIdx.x < PB && threadIdx.x >= b) D[threadIdx.x * SD + threadIdx.x] = 1.0;   // identity padding
+  __syncthreads();
+  PTRACE(11);
+  diag_factor(D, Li, b, sh);
+  PTRACE(12);
   if (threadIdx.x < 32) record_npd(sh, b, p, npd, P.npd_slot);
   for (int t = threadIdx.x; t < PB * PB; t += blockDim.x) {
     const int i = t / PB, x = t % PB;
@@ -306,7 +529,7 @@ __device__ __forceinline__ void panel_update_64(double (&acc)[4][2][2], const do
   }
 }
 
-__global__ void __launch_bounds__(DIAG_THREADS) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
+__global__ void __launch_bounds__(DIAG_THREADS, 2) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
                                                                  int32_t* __restrict__ npd) {
   extern __shared__ __align__(16) double csm[];
   double* S = csm;                  // PB x SD: X_{q-1}[p:p+b], then D
@@ -357,7 +580,11 @@ __global__ void __launch_bounds__(DIAG_THREADS) chol_diag_kernel(const h2g_chol_
       }
   }
   __syncthreads();
-  diag_ldlt<DIAG_BS>(S, Li, b, sh);
+  if (tid < PB && tid >= b) {   // identity padding beyond the panel width
+    for (int x = 0; x < PB; ++x) S[tid * SD + x] = (x == tid) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  diag_factor(S, Li, b, sh);
   if (tid < 32) record_npd(sh, b, p, npd, P.npd_slot);
   for (int t = tid; t < PB * PB; t += DIAG_THREADS) {
     const int i = t / PB, x = t % PB;

@@ -307,8 +307,9 @@ class FactorPlan:
 
         PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
         panel q-1 to block column q, factors the diagonal block and TRSMs the
-        rows below; REST(q) applies panel q to
-        everything right of block column q+1 (lower tiles of H).  RTRSM / RUPD
+        rows below; REST(q) applies panel q to the columns < r right of block
+        column q+1 (lower tiles of RR, all SR rows); the SS corner receives its
+        single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.  RTRSM / RUPD
         apply the panel to the V rows R = q_red (V = q_red L^-T), off the
         critical lane.  Returns (linv, loff, event after the last R update or
         None)."""
@@ -335,10 +336,14 @@ class FactorPlan:
                 descs.append((h, li, ni, W, ni, p, b, slot0 + i))
                 q0 = p + b                               # first column right of the panel
                 c0 = q0 + (min(W, ri - q0) if ri > q0 else 0)   # right of the next panel
-                if ni > c0:
+                if ri > c0:
+                    # columns c0 .. r only: the SS corner gets its single Schur update at the end
                     x = h + 8 * (c0 * ni + p)            # panel rows c0.. : H[c0:, p:p+b]
-                    rest.append((x, x, h + 8 * (c0 * ni + c0), ni - c0, ni - c0, b, ni, ni, ni,
+                    rest.append((x, x, h + 8 * (c0 * ni + c0), ri - c0, ri - c0, b, ni, ni, ni,
                                  nat.GEMM_LOWER, -1.0, 1.0))
+                    if ni > ri:                          # SR rows
+                        rest.append((h + 8 * (ri * ni + p), x, h + 8 * (ri * ni + c0), ni - ri, ri - c0, b,
+                                     ni, ni, ni, 0, -1.0, 1.0))
                 if Rp:
                     rr = Rp + 8 * int(qo[i])
                     rtrsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
@@ -374,6 +379,14 @@ class FactorPlan:
         last = [e for e in rest_ev if e is not None]
         if last:
             prog.wait(last[-1])                  # lane 1 is in order: the last REST covers all
+        # the single Schur update SS_ii -= L(s) L(s)^T with K = r (ulv_factor.py:236-241)
+        schur = []
+        for i in range(nb):
+            ri, ni = int(r[i]), int(n[i])
+            if mine[i] and ri > 0 and ni > ri:
+                ls = Hp + 8 * int(qo[i] + ri * ni)  # H[r:, 0:r]
+                schur.append((ls, ls, ls + 8 * ri, ni - ri, ni - ri, ri, ni, ni, ni, nat.GEMM_LOWER, -1.0, 1.0))
+        prog.gemm(0, 1, schur)
         return linv, loff, ev_v
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):

@@ -48,7 +48,7 @@ int main(int argc, char** argv) {
     h2g_chol_panel(dd, nbox, dmap, (int)map.size(), dnpd, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    long long tr[16]; cudaMemcpyFromSymbol(tr, h2g::g_panel_trace, sizeof(tr));
+    long long tr[32]; cudaMemcpyFromSymbol(tr, h2g::g_panel_trace, sizeof(tr));
     printf("chol_panel nbox %d n %d p %d row CTAs %zu: %.1f us | rows kernel cycles from start:", nbox, n, p, map.size(), ms * 1e3);
     for (int k = 1; k <= 5; ++k) printf(" %d:%lld", k, tr[k] - tr[0]);
     printf("\n");
@@ -59,7 +59,10 @@ int main(int argc, char** argv) {
     h2g_panel_potrf(dpd, nbox, dnpd, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    printf("potrf_diag nbox %d: %.1f us\n", nbox, ms * 1e3);
+    long long tr[32]; cudaMemcpyFromSymbol(tr, h2g::g_panel_trace, sizeof(tr));
+    printf("potrf_diag nbox %d: %.1f us | cycles from start: load %lld factor %lld [", nbox, ms * 1e3, tr[11] - tr[10], tr[12] - tr[11]);
+    for (int k = 16; k <= 26; ++k) printf(" %lld", tr[k] - tr[16]);
+    printf(" ]\n");
   }
   // check box 0: L_pp L_pp^T = D - X X^T (X = H[p:p+b, p-64:p]) and Linv L = I
   std::vector<double> Lp(4096), Li(4096);

@@ -1,9 +1,10 @@
 # microbenchmarks of the panel kernels + GPU tests + C2 bench (per-step dump)
 mkdir -p gpurun_out
 T=${1:-r01}
-for bs in 2 4; do
+for bs in 0 2; do
   for args in "1 256 64" "256 256 64" "256 256 0" "4096 256 64" "2 900 256"; do
-    ./tools/microbench/panel_bench_bs$bs $args | grep -v "^max" | tail -2
+    echo "== bs $bs args $args"
+    ./tools/microbench/panel_bench_bs$bs $args | tail -6
   done
 done > gpurun_out/${T}_panel_bench.txt 2>&1
 ./tools/microbench/diag_bench 256 >> gpurun_out/${T}_panel_bench.txt 2>&1
