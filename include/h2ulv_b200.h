@@ -123,6 +123,28 @@ int h2g_chol_panel_tiles(int n, int p, int b);
 int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map, int total_tiles,
                    int32_t* d_npd, void* stream);
 
+/* ---- left-looking row solve --------------------------------------------------
+ * For every 64-row chunk of every descriptor (one CTA each):
+ *   Xout[r, 0:b] = (Xin[r, 0:b] - sum_k A[r, k] Lb[c, k]) * Linv^T     (k < K)
+ * i.e. block column q of X = B L^-T once its columns 0..p-1 (A) are solved,
+ * with Lb = L[p:p+b, 0:K] and Linv the 64 x 64 inverse of the panel's
+ * diagonal block (ld 64).  Xin == NULL means the identity columns
+ * p0 .. p0+b-1 (X = L^-T itself).  Replaces the tri_solve of V_i = q_red L^-T
+ * (dense_core.py:69-81 in diag_trsm, ulv_factor.py:223-234).
+ */
+typedef struct h2g_rows_desc {
+  const double* A;     /* rows x K, ld lda */
+  const double* Lb;    /* b x K, ld ldlb */
+  const double* Xin;   /* rows x b, ld ldx (or NULL: identity columns p0..) */
+  double* Xout;        /* rows x b, ld ldx (may equal Xin) */
+  const double* Linv;  /* 64 x 64, ld 64 */
+  int32_t rows, b, K, p0;
+  int32_t lda, ldlb, ldx;
+  int32_t tile_start;  /* first CTA of this descriptor: ceil(rows / 64) CTAs each */
+} h2g_rows_desc;
+
+int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int total_tiles, void* stream);
+
 /* ---- block copy / gather ----------------------------------------------------
  * dst[r, c] = src(r, c) for an rows x cols block, where src(r, c) is
  *   mode 0: src[r*lds + c]            (copy)
@@ -156,8 +178,8 @@ int h2g_block_copy(const h2g_copy_desc* d_descs, const int32_t* d_tile_map,
  * rows [split, m) -> y2 (the basis transform of _transform_in,
  * ulv_solve.py:33-41, split = r).  Terms of output o are
  * d_terms[term_begin .. term_end).  With H2G_GEMV_PLUS the sum is added.
- * Each output is split into 256-row chunks, one CTA each (chunk_start =
- * running sum of ceil(m / 256)).
+ * Each output is split into 64-row chunks, one CTA each (chunk_start =
+ * running sum of ceil(m / 64)).
  * Replaces the per-box numpy products of _forward/_backward
  * (ulv_solve.py:98-113, 144-181).
  */
@@ -180,7 +202,7 @@ typedef struct h2g_gemv_out {
   int32_t split;     /* SPLIT only */
   int32_t term_begin, term_end;
   int32_t flags;
-  int32_t chunk_start; /* first 256-row chunk (CTA) of this output */
+  int32_t chunk_start; /* first 64-row chunk (CTA) of this output */
 } h2g_gemv_out;
 
 int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
@@ -280,6 +302,7 @@ enum {
   H2G_STEP_TRSV = 10,    /* descs = trsv descs, grid = w, arg = trans      */
   H2G_STEP_NOP = 12,     /* no kernel: carries a lane's event wait / record  */
   H2G_STEP_CHOL_PANEL = 13, /* descs/map = chol panel descs/tile map; npd = status */
+  H2G_STEP_TRSM_ROWS = 14,  /* descs/map = rows descs/tile map */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

@@ -688,6 +688,135 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
   PTRACE(5);
 }
 
+// ------------------------------------------------------------------ left-looking row solve
+// trsm_rows_kernel (h2g_trsm_rows): for one 64-row chunk of a descriptor
+//   Xout[rows, 0:b] = (Xin[rows, 0:b] - A[rows, 0:K] Lb[0:b, 0:K]^T) Linv^T
+// i.e. block column q of X = B L^-T given the already solved columns 0..p-1
+// (A) and the panel's row block of L (Lb), with the panel's 64x64 inverse.
+// Xin == NULL stands for the identity columns p0 .. p0+b (used to form
+// L^-T itself).  The K loop streams 64x32 slices of A and Lb through a
+// 2-stage cp.async pipeline; the TRSM with Linv runs on the accumulators.
+constexpr int TS_BK = 32;
+constexpr int TS_S = TS_BK + 4;   // 36 = 4 mod 16 doubles: conflict-free fragments
+
+__global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows_desc* __restrict__ descs,
+                                                                  const int32_t* __restrict__ tile_map) {
+  extern __shared__ __align__(16) double tsm[];
+  double* Li = tsm;                              // PB x SD
+  double* As = tsm + PB * SD;                    // 2 stages x (PB x TS_S)
+  double* Bs = As + 2 * PB * TS_S;               // 2 stages x (PB x TS_S)
+  double* Cs = As;                               // PB x SD after the K loop (aliases the stages)
+  const int pi = tile_map[blockIdx.x];
+  const h2g_rows_desc P = descs[pi];
+  const int chunk = blockIdx.x - P.tile_start;
+  const int r0 = PB * chunk;
+  const int nrows = min(PB, P.rows - r0);
+  const int b = P.b, K = P.K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;       // warp tile 32 x 16
+
+#pragma unroll 4
+  for (int t = tid; t < PB * PB; t += RW_THREADS) {
+    const int i = t / PB, x = t % PB;
+    cp_async8(Li + i * SD + x, P.Linv + (size_t)i * PB + x, true);
+  }
+  auto load_stage = [&](int st, int k0) {
+    double* as = As + st * PB * TS_S;
+    double* bs = Bs + st * PB * TS_S;
+#pragma unroll
+    for (int u = 0; u < (PB * TS_BK) / RW_THREADS; ++u) {
+      const int idx = tid + u * RW_THREADS;
+      const int m = idx / TS_BK, k = idx % TS_BK;
+      const bool va = m < nrows && k0 + k < K;
+      cp_async8(as + m * TS_S + k, va ? P.A + (size_t)(r0 + m) * P.lda + k0 + k : P.A, va);
+      const bool vb = m < b && k0 + k < K;
+      cp_async8(bs + m * TS_S + k, vb ? P.Lb + (size_t)m * P.ldlb + k0 + k : P.Lb, vb);
+    }
+  };
+  const int KT = (K + TS_BK - 1) / TS_BK;
+  if (KT > 0) load_stage(0, 0);
+  cp_async_commit();
+
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq + e;
+        double v = 0.0;
+        if (m < nrows && c < b)
+          v = P.Xin ? P.Xin[(size_t)(r0 + m) * P.ldx + c] : ((r0 + m == P.p0 + c) ? 1.0 : 0.0);
+        acc[i][j][e] = -v;
+      }
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* as = As + (kt & 1) * PB * TS_S;
+    const double* bs = Bs + (kt & 1) * PB * TS_S;
+#pragma unroll
+    for (int kk = 0; kk < TS_BK; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(wm * 32 + i * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // C = Xin - A Lb^T = -acc  ->  smem, then Xout = C Linv^T
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq;
+      Cs[m * SD + c] = -acc[i][j][0];
+      Cs[m * SD + c + 1] = -acc[i][j][1];
+    }
+  __syncthreads();
+  double out[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < PB; kk += 4) {
+    double af[4], bf[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = Cs[(wm * 32 + i * 8 + g) * SD + kk + tq];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) bf[j] = Li[(wn * 16 + j * 8 + g) * SD + kk + tq];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma884(out[i][j], af[i], bf[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = wm * 32 + i * 8 + g;
+    if (m >= nrows) continue;
+    double* dst = P.Xout + (size_t)(r0 + m) * P.ldx;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = wn * 16 + j * 8 + 2 * tq;
+      if (c < b) dst[c] = out[i][j][0];
+      if (c + 1 < b) dst[c + 1] = out[i][j][1];
+    }
+  }
+}
+
+constexpr size_t TS_SMEM = (PB * SD + 4 * PB * TS_S) * sizeof(double);
+
 constexpr size_t DIAG_SMEM = (2 * PB * SD) * sizeof(double) + sizeof(LdltShared);
 constexpr size_t RW_SMEM = (3 * PB * SD) * sizeof(double);
 
@@ -728,4 +857,16 @@ extern "C" int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, con
   if (rc || total_tiles <= 0) return rc;
   h2g::chol_rows_kernel<<<total_tiles, h2g::RW_THREADS, h2g::RW_SMEM, st>>>(d_descs, d_tile_map);
   return h2g_check_launch("chol_rows");
+}
+
+extern "C" int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int total_tiles, void* stream) {
+  if (total_tiles <= 0) return H2G_OK;
+  if (!d_descs || !d_tile_map) return h2g_set_error(H2G_EINVAL, "h2g_trsm_rows: null argument");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(h2g::trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::TS_SMEM);
+    attr = true;
+  }
+  h2g::trsm_rows_kernel<<<total_tiles, h2g::RW_THREADS, h2g::TS_SMEM, (cudaStream_t)stream>>>(d_descs, d_tile_map);
+  return h2g_check_launch("trsm_rows");
 }

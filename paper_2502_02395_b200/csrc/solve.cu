@@ -3,13 +3,13 @@
 // per sweep, so the kernels are built for memory-level parallelism: all
 // loads of a thread are independent and unrolled, rows of a transposed
 // operand are split across warps and reduced through shared memory, and a
-// large segment is split over several CTAs (one 256-row output chunk each).
+// large segment is split over several CTAs (one 64-row output chunk each).
 #include "common.cuh"
 
 namespace h2g {
 
-constexpr int GV_THREADS = 256;
-constexpr int GV_CHUNK = 256;   // output rows per CTA
+constexpr int GV_THREADS = 512;
+constexpr int GV_CHUNK = 64;    // output rows per CTA (small: many CTAs for memory-level parallelism)
 constexpr int GV_W = 4;         // RHS columns per pass
 
 __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) {
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_grouped_kernel(const h2g_gemv
           double s[GV_CHUNK / 32];
 #pragma unroll
           for (int t = 0; t < GV_CHUNK / 32; ++t) s[t] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
           for (int c = warp; c < K; c += NW) {
             const double xv = x[(size_t)c * w + j0 + j];
             const double* arow = A + (size_t)c * lda + r0;
@@ -114,10 +114,13 @@ __global__ void __launch_bounds__(GV_THREADS) gemv_grouped_kernel(const h2g_gemv
 //   trans = 0:  x_P <- Linv_q (x_P - L[P, <P] x_<P)       (forward)
 //   trans = 1:  x_P <- Linv_q^T (x_P - L[>P, P]^T x_>P)   (backward)
 constexpr int TB = 64;
-__global__ void __launch_bounds__(256) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
-                                                           int w) {
+constexpr int TR_THREADS = 512;
+constexpr int TR_WARPS = TR_THREADS / 32;
+constexpr int TR_RPW = TB / TR_WARPS;   // rows per warp in the forward GEMV (4)
+__global__ void __launch_bounds__(TR_THREADS) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
+                                                                  int w) {
   __shared__ double t[TB];
-  __shared__ double red[8][TB];
+  __shared__ double red[TR_WARPS][TB];
   const h2g_trsv_desc D = descs[blockIdx.x];
   const int n = D.n, ld = D.ldl;
   const double* __restrict__ L = D.L;
@@ -133,31 +136,45 @@ __global__ void __launch_bounds__(256) trsv_batched_kernel(const h2g_trsv_desc* 
       const int nb = min(TB, n - i0);
       const double* Lq = Li + (size_t)q * TB * TB;
       if (!trans) {
-        // t[r] = x[i0+r] - sum_{c < i0} L[i0+r][c] x[c]   (warp per row)
-        for (int r = warp; r < nb; r += 8) {
-          const double* lrow = L + (size_t)(i0 + r) * ld;
-          double s = 0.0;
-#pragma unroll 4
-          for (int c = lane; c < i0; c += 32) s += lrow[c] * x[(size_t)c * w + j];
+        // t[r] = x[i0+r] - sum_{c < i0} L[i0+r][c] x[c]: each warp owns TR_RPW rows, all loads independent
+        double s[TR_RPW];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) t[r] = x[(size_t)(i0 + r) * w + j] - s;
+        for (int u = 0; u < TR_RPW; ++u) s[u] = 0.0;
+#pragma unroll 2
+        for (int c = lane; c < i0; c += 32) {
+          const double xv = x[(size_t)c * w + j];
+#pragma unroll
+          for (int u = 0; u < TR_RPW; ++u) {
+            const int r = warp * TR_RPW + u;
+            if (r < nb) s[u] += L[(size_t)(i0 + r) * ld + c] * xv;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < TR_RPW; ++u) {
+          double v = s[u];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          const int r = warp * TR_RPW + u;
+          if (lane == 0 && r < nb) t[r] = x[(size_t)(i0 + r) * w + j] - v;
         }
         __syncthreads();
         // x[i0+r] = sum_c Linv[r][c] t[c]
-        for (int r = warp; r < nb; r += 8) {
-          double s = 0.0;
-          for (int c = lane; c <= r; c += 32) s += Lq[r * TB + c] * t[c];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) x[(size_t)(i0 + r) * w + j] = s;
+        for (int u = 0; u < TR_RPW; ++u) {
+          const int r = warp * TR_RPW + u;
+          double v = 0.0;
+          if (r < nb)
+            for (int c = lane; c <= r; c += 32) v += Lq[r * TB + c] * t[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0 && r < nb) x[(size_t)(i0 + r) * w + j] = v;
         }
         __syncthreads();
       } else {
         // t[c] = x[i0+c] - sum_{r >= i0+nb} L[r][i0+c] x[r]  (warps split r, lanes own c)
         double s0 = 0.0, s1 = 0.0;
-#pragma unroll 2
-        for (int r = i0 + nb + warp; r < n; r += 8) {
+#pragma unroll 4
+        for (int r = i0 + nb + warp; r < n; r += TR_WARPS) {
           const double xv = x[(size_t)r * w + j];
           const double* lrow = L + (size_t)r * ld + i0;
           if (lane < nb) s0 += lrow[lane] * xv;
@@ -169,13 +186,13 @@ __global__ void __launch_bounds__(256) trsv_batched_kernel(const h2g_trsv_desc* 
         if (tid < nb) {
           double v = 0.0;
 #pragma unroll
-          for (int qq = 0; qq < 8; ++qq) v += red[qq][tid];
+          for (int qq = 0; qq < TR_WARPS; ++qq) v += red[qq][tid];
           t[tid] = x[(size_t)(i0 + tid) * w + j] - v;
         }
         __syncthreads();
         // x[i0+c] = sum_r Linv[r][c] t[r]   (r >= c)
         double u0 = 0.0, u1 = 0.0;
-        for (int r = warp; r < nb; r += 8) {
+        for (int r = warp; r < nb; r += TR_WARPS) {
           const double tv = t[r];
           if (lane <= r) u0 += Lq[r * TB + lane] * tv;
           if (lane + 32 <= r) u1 += Lq[r * TB + lane + 32] * tv;
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(256) trsv_batched_kernel(const h2g_trsv_desc* 
         if (tid < nb) {
           double v = 0.0;
 #pragma unroll
-          for (int qq = 0; qq < 8; ++qq) v += red[qq][tid];
+          for (int qq = 0; qq < TR_WARPS; ++qq) v += red[qq][tid];
           x[(size_t)(i0 + tid) * w + j] = v;
         }
         __syncthreads();
@@ -208,6 +225,6 @@ extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2
 extern "C" int h2g_trsv_batched(const h2g_trsv_desc* d_descs, int count, int trans, int w, void* stream) {
   if (count <= 0) return H2G_OK;
   if (!d_descs || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_trsv_batched: bad argument");
-  h2g::trsv_batched_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(d_descs, trans, w);
+  h2g::trsv_batched_kernel<<<count, h2g::TR_THREADS, 0, (cudaStream_t)stream>>>(d_descs, trans, w);
   return h2g_check_launch("trsv_batched");
 }

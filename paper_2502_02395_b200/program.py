@@ -142,6 +142,24 @@ class Program:
                   self._blob(tmap) if tmap.size else -1, npd=npd_ptr, flops=fl)
         return int(tiles.sum())
 
+    def trsm_rows(self, descs):
+        """descs: list of (A, Lb, Xin, Xout, Linv, rows, b, K, p0, lda, ldlb, ldx): left-looking
+        block-column solve Xout = (Xin - A Lb^T) Linv^T, one CTA per 64-row chunk (h2g_trsm_rows)."""
+        descs = [d for d in descs if d[5] > 0 and d[6] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.ROWS_DT)
+        for name, col in zip(("A", "Lb", "Xin", "Xout", "Linv", "rows", "b", "K", "p0", "lda", "ldlb", "ldx"),
+                             zip(*descs)):
+            arr[name] = col
+        tiles = -(-arr["rows"].astype(np.int64) // nat.PANEL_WIDTH)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        m, b, k = arr["rows"].astype(np.int64), arr["b"].astype(np.int64), arr["K"].astype(np.int64)
+        self._add(nat.STEP["TRSM_ROWS"], len(descs), int(tiles.sum()), self._blob(arr), self._blob(tmap),
+                  flops=int((2 * m * b * k + m * b * b).sum()))
+        return int(tiles.sum())
+
     def copy(self, descs):
         """descs: list of (src, dst, rows, cols, lds, ldd, mode)."""
         rows = [d for d in descs if d[2] > 0 and d[3] > 0]
@@ -198,7 +216,7 @@ class Program:
         nbytes = 0
         for q, (y, y2, init, m, split, flags, tms) in enumerate(outs):
             oarr[q] = (y, y2, init, m, split, len(tl), len(tl) + len(tms), flags, chunks)
-            chunks += -(-int(m) // 256)
+            chunks += -(-int(m) // nat.GEMV_CHUNK)
             tl.extend(tms)
             nbytes += 8 * int(m) * sum(int(t[4]) for t in tms)
         tarr = np.zeros(max(len(tl), 1), dtype=nat.GEMV_TERM_DT)

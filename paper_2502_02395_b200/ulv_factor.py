@@ -12,11 +12,11 @@ on five lanes (CUDA streams joined by events; the whole factorization is one
 
   lane 2  GEMM NN  MO_ij[:, r_j:] = A_ij q_skel_j                     off_mul1, skeleton part
           GEMM TN  SS_ij = q_skel_i^T MO_ij[:, r_j:]                   off_mul2, skeleton part
-  lane 0  R <- Q (device copy); GEMM NN M_i = A_ii Q_i; TN H_i = Q_i^T M_i   diag_mul1/2 (189-200)
+  lane 0  GEMM NN M_i = A_ii Q_i; TN H_i = Q_i^T M_i                        diag_mul1/2 (189-200)
           for p in 0, 64, ...: PANEL chol(H[p:p+b,p:p+b]) + inverse; TRSM of the rows below;
                                NEXT = update of the next block column          partial Cholesky
   lane 1  REST = the remaining trailing update (lower tiles)             (217-241): H becomes
-  lane 4  V ride-along: R[:, :r] <- q_red L^-T panel by panel            [[L(r)],[L(s), SS - L(s)L(s)^T]]
+  lane 4  V ride-along: R[:, :r] <- q_red L^-T, block column by block column (left-looking)
   lane 3  (deferred, only the solve reads it)
           GEMM NN  MO_ij[:, :r_j] = A_ij V_j ; GEMM TN T_ij[:, :r_j] = Q_i^T MO  -> lr_off, L(s)_ij
           GEMM TN  L(s)_ji = (A_ij q_skel_j)^T V_i = (L(r)_ii^-1 RS_ij)^T        off_mirror (282-286)
@@ -214,8 +214,6 @@ class FactorPlan:
                 ev_ss = prog.event()
                 prog.record(ev_ss)
                 # ---- diagonal phase (lane 0 = the critical chain)
-                prog.lane = 4                   # R <- Q for the V ride-along, off the critical lane
-                prog.memcpy(Rp, qp, 8 * lay.qsize)
                 prog.lane = 0
                 prob = []
                 for i in range(nb):
@@ -230,7 +228,8 @@ class FactorPlan:
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
                          int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
                 prog.gemm(1, 0, prob)
-                B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine)
+                B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
+                                                                    Qp=qp)
                 if self.distributed_level(l):
                     # V_j of boxes owned elsewhere but coupled to mine by a near pair
                     prog = self._cut(prog, ("halo_v", l))
@@ -296,23 +295,25 @@ class FactorPlan:
         return Program(self.device)
 
     # ------------------------------------------------------------------ steps
-    def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None):
+    def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
         """Right-looking partial Cholesky of every box's H (and the V ride-along
         rows in R), panels of W = 64 columns, one fused kernel per panel on the
         critical lane:
 
           lane 0:  [wait REST(q-2)] -> PANEL(q) -> [wait REST(q-1)] -> PANEL(q+1) ...
           lane 1:          [wait PANEL(q)] -> REST(q)
-          lane 4:          [wait PANEL(q)] -> RTRSM(q) -> RUPD(q)
+          lane 4:          [wait PANEL(q)] -> ROWS_V(q)
 
         PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
         panel q-1 to block column q, factors the diagonal block and TRSMs the
         rows below; REST(q) applies panel q to the columns < r right of block
         column q+1 (lower tiles of RR, all SR rows); the SS corner receives its
-        single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.  RTRSM / RUPD
-        apply the panel to the V rows R = q_red (V = q_red L^-T), off the
-        critical lane.  Returns (linv, loff, event after the last R update or
-        None)."""
+        single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.
+        ROWS_V(q) (h2g_trsm_rows, left-looking) forms block column q of
+        R = Q_red L^-T = V from Q (Qp) and the solved columns < q, off the
+        critical lane; with Qp == 0 the ride-along is the identity and R
+        becomes L^-T (the root's explicit inverse for the solve).  Returns
+        (linv, loff, event after the last R column or None)."""
         nb = len(n)
         mine = np.ones(nb, dtype=bool) if mine is None else mine
         rmax = int(np.asarray(r)[mine].max()) if mine.any() else 0
@@ -325,7 +326,7 @@ class FactorPlan:
         lp = linv.data_ptr()
         rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
         for q, p in enumerate(range(0, rmax, W)):
-            descs, rest, rtrsm, rupd = [], [], [], []
+            descs, rest, rows = [], [], []
             for i in range(nb):
                 ri, ni = int(r[i]), int(n[i])
                 if ri <= p or not mine[i]:
@@ -346,10 +347,11 @@ class FactorPlan:
                                      ni, ni, ni, 0, -1.0, 1.0))
                 if Rp:
                     rr = Rp + 8 * int(qo[i])
-                    rtrsm.append((rr + 8 * p, li, rr + 8 * p, ni, b, b, ni, W, ni, 0, 1.0, 0.0))
-                    if ri - q0 > 0:
-                        pan = h + 8 * (q0 * ni + p)      # L[q0:r, p:p+b]
-                        rupd.append((rr + 8 * p, pan, rr + 8 * q0, ni, ri - q0, b, ni, ni, ni, 0, -1.0, 1.0))
+                    lb = h + 8 * (p * ni)                # L[p:p+b, 0:p]
+                    if Qp:                               # V = Q_red L^-T
+                        rows.append((rr, lb, Qp + 8 * int(qo[i] + p), rr + 8 * p, li, ni, b, p, 0, ni, ni, ni))
+                    else:                                # L^-T (upper: rows < p + b only)
+                        rows.append((rr, lb, 0, rr + 8 * p, li, p + b, b, p, p, ni, ni, ni))
             done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
             if done:
                 prog.wait(done[-1])              # block column q has all updates of panels <= q-2
@@ -364,11 +366,10 @@ class FactorPlan:
                 ev_rest = prog.event()
                 prog.record(ev_rest)
             rest_ev.append(ev_rest)
-            if rtrsm:
+            if rows:
                 prog.lane = 4
                 prog.wait(ev_fp)
-                prog.gemm(0, 1, rtrsm)
-                prog.gemm(0, 1, rupd)
+                prog.trsm_rows(rows)
             prog.lane = 0
         ev_v = None
         if Rp:
@@ -390,9 +391,12 @@ class FactorPlan:
         return linv, loff, ev_v
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
+        """Root: full Cholesky of the merged d x d block; the identity rides along so
+        that root_winv = L^-T (upper) turns the solve's root TRSVs into GEMVs."""
         assert d == ld
-        self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]),
-                                                            np.array([d]), slot)
+        self.root_winv = torch.zeros(max(d * d, 1), dtype=F64, device=self.device)
+        self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, self.root_winv.data_ptr(), np.array([0]),
+                                                            np.array([d]), np.array([d]), slot)
 
     def _merge_steps(self, prog, l, B, lists, dh2):
         lay = B.lay

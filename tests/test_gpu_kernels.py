@@ -1,0 +1,103 @@
+"""Kernel-level GPU checks of the Cholesky panel step and the left-looking row
+solve against numpy FP64 (the math of dense_core.cholesky / tri_solve,
+dense_core.py:51-81).  Tolerances are relative to the operand scale."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    from paper_2502_02395_b200 import _native as nat
+    from paper_2502_02395_b200.program import Program
+
+    nat.lib()
+    return torch, nat, Program
+
+
+def _spd(n, seed, shift=None):
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, n))
+    return g @ g.T + (shift if shift is not None else n) * np.eye(n)
+
+
+@pytest.mark.parametrize("n,p,b", [(256, 0, 64), (256, 64, 64), (200, 128, 40), (64, 0, 64), (70, 64, 6)])
+def test_chol_panel_step(env, n, p, b):
+    """PANEL(q) = previous-panel update of block column q + chol + TRSM of the rows below."""
+    torch, nat, Program = env
+    a = _spd(n, n + p + b)
+    lf = np.linalg.cholesky(a)
+    # H after panels < q-1 are complete and their REST updates applied:
+    # block column q still lacks the update of panel q-1.
+    h = a.copy()
+    if p > 0:
+        pp = p - 64
+        h[:, :p] = np.tril(lf[:, :p], 0) if p else h[:, :p]
+        s = lf[:, :pp] @ lf[:, :pp].T if pp > 0 else np.zeros((n, n))
+        h[p:, p:] = a[p:, p:] - s[p:, p:]
+    hd = torch.from_numpy(h.copy()).cuda()
+    linv = torch.zeros(64 * 64, dtype=torch.float64, device="cuda")
+    npd = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device="cuda")
+    prog = Program(torch.device("cuda"))
+    prog.chol_panel([(hd.data_ptr(), linv.data_ptr(), n, 64, n, p, b, 0)], npd.data_ptr())
+    prog.finalize().run()
+    torch.cuda.synchronize()
+    out = hd.cpu().numpy()
+    assert int(npd.item()) == 2 ** 31 - 1
+    scale = np.abs(lf).max()
+    np.testing.assert_allclose(np.tril(out[p:p + b, p:p + b]), lf[p:p + b, p:p + b], rtol=0, atol=RTOL * scale * 10)
+    if n > p + b:
+        np.testing.assert_allclose(out[p + b:, p:p + b], lf[p + b:, p:p + b], rtol=0, atol=RTOL * scale * 10)
+    li = linv.cpu().numpy().reshape(64, 64)[:b, :b]
+    np.testing.assert_allclose(li @ lf[p:p + b, p:p + b], np.eye(b), rtol=0, atol=1e-12)
+
+
+def test_chol_panel_reports_first_bad_pivot(env):
+    torch, nat, Program = env
+    n, bad = 96, 37
+    a = _spd(n, 5)
+    a[bad, bad] = -1.0e3                       # pivot 37 of the first panel turns negative
+    hd = torch.from_numpy(a).cuda()
+    linv = torch.zeros(64 * 64, dtype=torch.float64, device="cuda")
+    npd = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device="cuda")
+    prog = Program(torch.device("cuda"))
+    prog.chol_panel([(hd.data_ptr(), linv.data_ptr(), n, 64, n, 0, 64, 0)], npd.data_ptr())
+    prog.finalize().run()
+    torch.cuda.synchronize()
+    assert int(npd.item()) == bad
+
+
+@pytest.mark.parametrize("rows,b,K,ident", [(256, 64, 128, False), (100, 33, 64, False), (70, 64, 0, False),
+                                            (192, 64, 128, True)])
+def test_trsm_rows(env, rows, b, K, ident):
+    """Xout = (Xin - A Lb^T) Linv^T, Xin = identity columns p0.. when ident."""
+    torch, nat, Program = env
+    rng = np.random.default_rng(rows + b + K)
+    A = rng.standard_normal((rows, K))
+    Lb = rng.standard_normal((b, K))
+    ld = np.tril(rng.standard_normal((b, b))) + 4 * np.eye(b)
+    li = np.zeros((64, 64))
+    li[:b, :b] = np.linalg.inv(ld)
+    p0 = K
+    xin = np.zeros((rows, b))
+    if ident:
+        for c in range(b):
+            if p0 + c < rows:
+                xin[p0 + c, c] = 1.0
+    else:
+        xin = rng.standard_normal((rows, b))
+    ref = (xin - A @ Lb.T) @ li[:b, :b].T
+    t = lambda m: torch.from_numpy(np.ascontiguousarray(m)).cuda()
+    Ad, Lbd, Xd, Lid = t(A if K else np.zeros((rows, 1))), t(Lb if K else np.zeros((b, 1))), t(xin), t(li)
+    Xo = torch.zeros_like(Xd)
+    prog = Program(torch.device("cuda"))
+    prog.trsm_rows([(Ad.data_ptr(), Lbd.data_ptr(), 0 if ident else Xd.data_ptr(), Xo.data_ptr(), Lid.data_ptr(),
+                     rows, b, K, p0, max(K, 1), max(K, 1), b)])
+    prog.finalize().run()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(Xo.cpu().numpy(), ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
