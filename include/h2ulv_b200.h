@@ -124,23 +124,26 @@ int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, const int32_t*
                    int32_t* d_npd, void* stream);
 
 /* ---- left-looking row solve --------------------------------------------------
- * For every 64-row chunk of every descriptor (one CTA each):
- *   Xout[r, 0:b] = (Xin[r, 0:b] - sum_k A[r, k] Lb[c, k]) * Linv^T     (k < K)
- * i.e. block column q of X = B L^-T once its columns 0..p-1 (A) are solved,
- * with Lb = L[p:p+b, 0:K] and Linv the 64 x 64 inverse of the panel's
- * diagonal block (ld 64).  Xin == NULL means the identity columns
- * p0 .. p0+b-1 (X = L^-T itself).  Replaces the tri_solve of V_i = q_red L^-T
- * (dense_core.py:69-81 in diag_trsm, ulv_factor.py:223-234).
+ * X = B L^-T block column by block column, one CTA per 64-row chunk of every
+ * descriptor.  For panel q in [q_begin, q_end) (p = 64q, b = min(64, cols-p)):
+ *   Xout[r, p:p+b] = (Xin[r, p:p+b] - Xout[r, 0:p] L[p:p+b, 0:p]^T) Linv_q^T
+ * with L given by its rows (Lb, ld ldlb, row 0 / column 0) and Linv_q the
+ * 64 x 64 inverse of L's q-th diagonal block (at Linv + 4096 q, ld 64).
+ * Xin == NULL means B = I (X = L^-T, upper triangular; only rows < p + b are
+ * formed).  Xout may equal Xin.  Replaces the tri_solve of
+ * V_i = q_red L^-T (dense_core.py:69-81 in diag_trsm, ulv_factor.py:223-234);
+ * also forms the root's explicit L^-T used by the solve.
  */
 typedef struct h2g_rows_desc {
-  const double* A;     /* rows x K, ld lda */
-  const double* Lb;    /* b x K, ld ldlb */
-  const double* Xin;   /* rows x b, ld ldx (or NULL: identity columns p0..) */
-  double* Xout;        /* rows x b, ld ldx (may equal Xin) */
-  const double* Linv;  /* 64 x 64, ld 64 */
-  int32_t rows, b, K, p0;
-  int32_t lda, ldlb, ldx;
+  const double* Lb;    /* L (cols x cols lower), ld ldlb */
+  const double* Xin;   /* rows x cols, ld ldx (or NULL: identity) */
+  double* Xout;        /* rows x cols, ld ldx (may equal Xin) */
+  const double* Linv;  /* inverses of L's 64 x 64 diagonal blocks, 4096 doubles each */
+  const double* pad0_;
+  int32_t rows, cols, q_begin, q_end;
+  int32_t ldlb, ldx;
   int32_t tile_start;  /* first CTA of this descriptor: ceil(rows / 64) CTAs each */
+  int32_t pad1_;
 } h2g_rows_desc;
 
 int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int total_tiles, void* stream);

@@ -24,9 +24,9 @@ PANEL_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("ldh", "<i4"), ("ldl", "<i4
                      ("npd_slot", "<i4"), ("pad_", "<i4")])
 CHOLP_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("ldh", "<i4"), ("ldl", "<i4"), ("n", "<i4"), ("p", "<i4"),
                      ("b", "<i4"), ("npd_slot", "<i4"), ("tile_start", "<i4"), ("pad_", "<i4")])
-ROWS_DT = np.dtype([("A", "<u8"), ("Lb", "<u8"), ("Xin", "<u8"), ("Xout", "<u8"), ("Linv", "<u8"), ("rows", "<i4"),
-                    ("b", "<i4"), ("K", "<i4"), ("p0", "<i4"), ("lda", "<i4"), ("ldlb", "<i4"), ("ldx", "<i4"),
-                    ("tile_start", "<i4")])
+ROWS_DT = np.dtype([("Lb", "<u8"), ("Xin", "<u8"), ("Xout", "<u8"), ("Linv", "<u8"), ("pad0_", "<u8"),
+                    ("rows", "<i4"), ("cols", "<i4"), ("q_begin", "<i4"), ("q_end", "<i4"), ("ldlb", "<i4"),
+                    ("ldx", "<i4"), ("tile_start", "<i4"), ("pad1_", "<i4")])
 COPY_DT = np.dtype([("src", "<u8"), ("dst", "<u8"), ("rows", "<i4"), ("cols", "<i4"), ("lds", "<i4"),
                     ("ldd", "<i4"), ("mode", "<i4"), ("tile_start", "<i4")])
 GEMV_TERM_DT = np.dtype([("A", "<u8"), ("x", "<u8"), ("lda", "<i4"), ("trans", "<i4"), ("K", "<i4"),

@@ -1,6 +1,7 @@
 // C ABI plumbing: error reporting, the native step executor and CUDA-graph
 // capture of a whole factorization program (see include/h2ulv_b200.h).
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -74,10 +75,17 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
   }
 }
 
-constexpr int kMaxLanes = 5;   // lane 0 = the caller's stream, lanes 1..4 = side streams
+constexpr int kMaxLanes = 5;
 
+// Lanes of a multi-lane program run on the context's own streams: lanes 0
+// (the critical chain) and 1 (its look-ahead trailing updates) at the
+// device's greatest stream priority, lanes 2..4 (work that only has to be
+// done by the next merge / by the solve) at the least priority, so the block
+// scheduler hands free SMs to the chain first and the side lanes fill the
+// gaps of the latency-bound panel steps.  H2G_LANE_PRIORITY=0 gives every
+// lane the default priority.  The caller's stream only forks and joins.
 struct ExecCtx {
-  cudaStream_t side[kMaxLanes] = {};   // side[0] unused
+  cudaStream_t side[kMaxLanes] = {};
   std::vector<cudaEvent_t> ev;
   cudaEvent_t fork = nullptr, join[kMaxLanes] = {};
 };
@@ -85,9 +93,13 @@ struct ExecCtx {
 extern "C" int h2g_exec_ctx_create(int n_events, void** ctx_out) {
   if (!ctx_out || n_events < 0) return h2g_set_error(H2G_EINVAL, "h2g_exec_ctx_create: bad arguments");
   ExecCtx* c = new ExecCtx();
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const char* env = getenv("H2G_LANE_PRIORITY");
+  if (env && env[0] == '0') least = greatest = 0;
   cudaError_t e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-  for (int l = 1; l < kMaxLanes && e == cudaSuccess; ++l) {
-    e = cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking);
+  for (int l = 0; l < kMaxLanes && e == cudaSuccess; ++l) {
+    e = cudaStreamCreateWithPriority(&c->side[l], cudaStreamNonBlocking, l <= 1 ? greatest : least);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[l], cudaEventDisableTiming);
   }
   c->ev.resize(n_events, nullptr);
@@ -106,7 +118,7 @@ extern "C" int h2g_exec_ctx_destroy(void* ctx) {
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->fork) cudaEventDestroy(c->fork);
-  for (int l = 1; l < kMaxLanes; ++l) {
+  for (int l = 0; l < kMaxLanes; ++l) {
     if (c->join[l]) cudaEventDestroy(c->join[l]);
     if (c->side[l]) cudaStreamDestroy(c->side[l]);
   }
@@ -118,21 +130,22 @@ extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, 
   if (nsteps < 0 || (nsteps > 0 && !steps)) return h2g_set_error(H2G_EINVAL, "h2g_run_program: bad steps");
   cudaStream_t main_st = (cudaStream_t)stream;
   ExecCtx* c = (ExecCtx*)ctx;
-  bool used[kMaxLanes] = {true};
+  bool used[kMaxLanes] = {};
   bool multi = false;
   for (int i = 0; i < nsteps; ++i) {
     const int ln = steps[i].lane;
     if (ln < 0 || ln >= kMaxLanes) return h2g_set_error(H2G_EINVAL, "step %d: bad lane %d", i, ln);
-    if (ln > 0 && c) used[ln] = multi = true;
+    used[ln] = true;
+    if (ln > 0 && c) multi = true;
   }
-  if (multi) {  // fork: the side lanes start after everything already queued on main
+  if (multi) {  // fork: every lane starts after everything already queued on the caller's stream
     cudaEventRecord(c->fork, main_st);
-    for (int l = 1; l < kMaxLanes; ++l)
+    for (int l = 0; l < kMaxLanes; ++l)
       if (used[l]) cudaStreamWaitEvent(c->side[l], c->fork, 0);
   }
   for (int i = 0; i < nsteps; ++i) {
     const h2g_step& sp = steps[i];
-    cudaStream_t st = (multi && sp.lane > 0) ? c->side[sp.lane] : main_st;
+    cudaStream_t st = multi ? c->side[sp.lane] : main_st;
     if (multi && sp.wait_ev >= 0) {
       if (sp.wait_ev >= (int)c->ev.size()) return h2g_set_error(H2G_EINVAL, "step %d: bad wait event", i);
       cudaStreamWaitEvent(st, c->ev[sp.wait_ev], 0);
@@ -148,8 +161,8 @@ extern "C" int h2g_run_program(const h2g_step* steps, int nsteps, void* stream, 
       cudaEventRecord(c->ev[sp.rec_ev], st);
     }
   }
-  if (multi) {  // join: main continues only after every side lane drained
-    for (int l = 1; l < kMaxLanes; ++l)
+  if (multi) {  // join: the caller's stream continues only after every lane drained
+    for (int l = 0; l < kMaxLanes; ++l)
       if (used[l]) {
         cudaEventRecord(c->join[l], c->side[l]);
         cudaStreamWaitEvent(main_st, c->join[l], 0);

@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const int wm = warp / wn_count, wn = warp % wn_count;
+  // a warp tile strictly above the diagonal of a LOWER diagonal tile is never read: skip its math
+  const bool upper_warp = (P.flags & H2G_GEMM_LOWER) && tm == tn && wm * C::WM + C::WM <= wn * C::WN;
 
   double acc[C::MI][C::NI][2];
   double* Cp = P.C;  // may alias A (in-place TRSM with N <= 64)
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
     }
     const double* as = As + (kt % C::STAGES) * C::A_DBL;
     const double* bs = Bs + (kt % C::STAGES) * C::B_DBL;
+    if (upper_warp) continue;   // still takes part in the loads and barriers
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[C::MI], bf[C::NI];
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   cp_async_wait<0>();
 
   // epilogue: C = alpha * acc   (acc already holds beta/alpha * C_old)
+  if (upper_warp) return;
 #pragma unroll
   for (int i = 0; i < C::MI; ++i) {
     const int row = m0 + wm * C::WM + i * 8 + g;

@@ -322,8 +322,10 @@ __device__ __forceinline__ void tile8_nt16(double (&c)[2], const double* A, cons
   for (int kk = 0; kk < DB; kk += 4) dmma884(c, A[g * SD + kk + tq], B[g * SD + kk + tq]);
 }
 
-// 256 threads (8 warps).  D, Li: 64 x SD smem; pv: 64 doubles smem.
+// NW warps (4 or 8).  D, Li: 64 x SD smem; pv: 64 doubles smem.
+template <int NW>
 __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs) {
+  constexpr int NU = (16 + NW - 1) / NW;   // 8x8 output tiles per warp (<= 12 / 16 tiles per phase)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
   for (int t = tid; t < PB * PB; t += blockDim.x) Li[(t / PB) * SD + t % PB] = 0.0;
@@ -339,11 +341,11 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     if (R == 0) break;
     // TRSM: X = D[c+16:, c:c+16] <- X Linv_kk^T; 8x8 output tiles (R/8) x 2
     const int nt = (R / 8) * 2;
-    double x[2][2];
-    int tt[2];
+    double x[NU][2];
+    int tt[NU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      tt[u] = warp + 8 * u;
+    for (int u = 0; u < NU; ++u) {
+      tt[u] = warp + NW * u;
       if (tt[u] < nt) {
         const int tm = tt[u] >> 1, tn = tt[u] & 1;
         tile8_nt16(x[u], D + (c + DB + 8 * tm) * SD + c, Li + (c + 8 * tn) * SD + c, g, tq);
@@ -351,7 +353,7 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < NU; ++u)
       if (tt[u] < nt) {
         const int tm = tt[u] >> 1, tn = tt[u] & 1;
         double* dst = D + (c + DB + 8 * tm + g) * SD + c + 8 * tn + 2 * tq;
@@ -361,7 +363,7 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     __syncthreads();
     // trailing update of the lower 8x8 tiles of D[c+16:, c+16:] (K = 16)
     const int T = R / 8, ntile = T * (T + 1) / 2;
-    for (int t = warp; t < ntile; t += 8) {
+    for (int t = warp; t < ntile; t += NW) {
       int tm = 0;
       while ((tm + 1) * (tm + 2) / 2 <= t) ++tm;
       const int tn = t - tm * (tm + 1) / 2;
@@ -381,11 +383,11 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
   for (int dd = 1; dd < PB / DB; ++dd) {
     const int nblk = PB / DB - dd;             // blocks on this block diagonal
     // phase 1: W_J = sum_K L_IK Linv_KJ (16x16 each, 4 8x8 tiles) -> registers, then smem scratch
-    double w[2][2];
-    int tt[2];
+    double w[NU][2];
+    int tt[NU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      tt[u] = warp + 8 * u;
+    for (int u = 0; u < NU; ++u) {
+      tt[u] = warp + NW * u;
       w[u][0] = w[u][1] = 0.0;
       if (tt[u] < nblk * 4) {
         const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
@@ -403,7 +405,7 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     __syncthreads();
     // stash W in the (zero) upper part of Li: block (J, I) position holds W_J for pair (I, J)
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < NU; ++u)
       if (tt[u] < nblk * 4) {
         const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
         double* dst = Li + (J * DB + 8 * tm + g) * SD + I * DB + 8 * tn + 2 * tq;
@@ -413,7 +415,7 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     __syncthreads();
     // phase 2: Linv_IJ = -Linv_II W
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < NU; ++u) {
       w[u][0] = w[u][1] = 0.0;
       if (tt[u] < nblk * 4) {
         const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
@@ -427,7 +429,7 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < NU; ++u)
       if (tt[u] < nblk * 4) {
         const int J = tt[u] >> 2, I = J + dd, tm = (tt[u] >> 1) & 1, tn = tt[u] & 1;
         double* dst = Li + (I * DB + 8 * tm + g) * SD + J * DB + 8 * tn + 2 * tq;
@@ -456,10 +458,11 @@ __device__ __forceinline__ void record_npd(const LdltShared& sh, int b, int p, i
 constexpr int DIAG_BS = H2G_DIAG_BS;
 constexpr int DIAG_THREADS = DIAG_BS == 0 ? 256 : (Ldlt<(DIAG_BS ? DIAG_BS : 2)>::NT + 31) / 32 * 32;
 
-// factor the 64x64 block in smem (lower part, rows/cols >= b already identity)
+// factor the 64x64 block in smem (lower part, rows/cols >= b already identity), NW warps
+template <int NW = 8>
 __device__ __forceinline__ void diag_factor(double* D, double* Li, int b, LdltShared& sh) {
   if constexpr (DIAG_BS == 0) {
-    diag_blocked(D, Li, sh.pv, *reinterpret_cast<Chol16Shared*>(&sh.colX[0][0]));
+    diag_blocked<NW>(D, Li, sh.pv, *reinterpret_cast<Chol16Shared*>(&sh.colX[0][0]));
   } else {
     diag_ldlt<(DIAG_BS ? DIAG_BS : 2)>(D, Li, b, sh);
   }
@@ -529,8 +532,11 @@ __device__ __forceinline__ void panel_update_64(double (&acc)[4][2][2], const do
   }
 }
 
-__global__ void __launch_bounds__(DIAG_THREADS, 2) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
-                                                                 int32_t* __restrict__ npd) {
+// NW = 8: latency variant (few boxes); NW = 4: throughput variant (many boxes, more CTAs per SM).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
+                                                                    int32_t* __restrict__ npd) {
+  constexpr int NT = NW * 32, NV = 8 / NW;   // NV virtual 32x16 warp tiles per warp
   extern __shared__ __align__(16) double csm[];
   double* S = csm;                  // PB x SD: X_{q-1}[p:p+b], then D
   double* Li = csm + PB * SD;       // PB x SD
@@ -540,53 +546,62 @@ __global__ void __launch_bounds__(DIAG_THREADS, 2) chol_diag_kernel(const h2g_ch
   double* __restrict__ H = P.H;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  const bool gw = warp < 8;
   if (p > 0) {
     const double* src = H + (size_t)p * ldh + (p - PB);
 #pragma unroll 4
-    for (int t = tid; t < PB * PB; t += DIAG_THREADS) {
+    for (int t = tid; t < PB * PB; t += NT) {
       const int s = t / PB, c = t % PB;
       cp_async8(S + s * SD + c, s < b ? src + (size_t)s * ldh + c : H, s < b);
     }
     cp_async_commit();
   }
-  double acc[4][2][2];
-  const int wm = (warp >> 2) & 1, wn = warp & 3;
+  double acc[NV][4][2][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int s = wm * 32 + i * 8 + g;
+  for (int v = 0; v < NV; ++v) {
+    const int vw = warp + NW * v, wm = vw >> 2, wn = vw & 3;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 4; ++i) {
+      const int s = wm * 32 + i * 8 + g;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = wn * 16 + j * 8 + 2 * tq + e;
-        acc[i][j][e] = (gw && s < b && col <= s) ? -H[(size_t)(p + s) * ldh + p + col] : 0.0;
-      }
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 16 + j * 8 + 2 * tq + e;
+          acc[v][i][j][e] = (s < b && col <= s) ? -H[(size_t)(p + s) * ldh + p + col] : 0.0;
+        }
+    }
   }
   if (p > 0) {
     cp_async_wait<0>();
     __syncthreads();
-    if (gw) panel_update_64(acc, S, 0, warp, g, tq);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) panel_update_64(acc[v], S, 0, warp + NW * v, g, tq);
     __syncthreads();   // S becomes D
   }
-  if (gw) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int vw = warp + NW * v, wm = vw >> 2, wn = vw & 3;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int s = wm * 32 + i * 8 + g, col = wn * 16 + j * 8 + 2 * tq;
-        S[s * SD + col] = -acc[i][j][0];
-        S[s * SD + col + 1] = -acc[i][j][1];
+        S[s * SD + col] = -acc[v][i][j][0];
+        S[s * SD + col + 1] = -acc[v][i][j][1];
       }
   }
   __syncthreads();
   if (tid < PB && tid >= b) {   // identity padding beyond the panel width
     for (int x = 0; x < PB; ++x) S[tid * SD + x] = (x == tid) ? 1.0 : 0.0;
   }
+  if (NT < PB && tid + NT < PB && tid + NT >= b) {
+    const int r = tid + NT;
+    for (int x = 0; x < PB; ++x) S[r * SD + x] = (x == r) ? 1.0 : 0.0;
+  }
   __syncthreads();
-  diag_factor(S, Li, b, sh);
+  diag_blocked<NW>(S, Li, sh.pv, *reinterpret_cast<Chol16Shared*>(&sh.colX[0][0]));
   if (tid < 32) record_npd(sh, b, p, npd, P.npd_slot);
-  for (int t = tid; t < PB * PB; t += DIAG_THREADS) {
+  for (int t = tid; t < PB * PB; t += NT) {
     const int i = t / PB, x = t % PB;
     if (x <= i && i < b) H[(size_t)(p + i) * ldh + p + x] = S[i * SD + x];
     P.Linv[(size_t)i * P.ldl + x] = Li[i * SD + x];
@@ -689,13 +704,16 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
 }
 
 // ------------------------------------------------------------------ left-looking row solve
-// trsm_rows_kernel (h2g_trsm_rows): for one 64-row chunk of a descriptor
-//   Xout[rows, 0:b] = (Xin[rows, 0:b] - A[rows, 0:K] Lb[0:b, 0:K]^T) Linv^T
-// i.e. block column q of X = B L^-T given the already solved columns 0..p-1
-// (A) and the panel's row block of L (Lb), with the panel's 64x64 inverse.
-// Xin == NULL stands for the identity columns p0 .. p0+b (used to form
-// L^-T itself).  The K loop streams 64x32 slices of A and Lb through a
-// 2-stage cp.async pipeline; the TRSM with Linv runs on the accumulators.
+// trsm_rows_kernel (h2g_trsm_rows): X = B L^-T, block column by block column,
+// for one 64-row chunk of a descriptor.  For panel q in [q_begin, q_end)
+// (p = 64q, b = min(64, cols - p)):
+//   Xout[rows, p:p+b] = (Xin[rows, p:p+b] - Xout[rows, 0:p] L[p:p+b, 0:p]^T) Linv_q^T
+// (A = the already solved columns of the same rows, read back from Xout).
+// Xin == NULL stands for the identity (X = L^-T itself, upper triangular:
+// only rows < p + b are formed).  The K loop streams 64x32 slices of A and
+// of L's row block through a 2-stage cp.async pipeline; the TRSM with the
+// panel's 64x64 inverse runs on the accumulators.  One CTA walks all panels
+// of its rows, so a whole level's V = q_red L^-T is ONE launch.
 constexpr int TS_BK = 32;
 constexpr int TS_S = TS_BK + 4;   // 36 = 4 mod 16 doubles: conflict-free fragments
 
@@ -710,108 +728,117 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
   const h2g_rows_desc P = descs[pi];
   const int chunk = blockIdx.x - P.tile_start;
   const int r0 = PB * chunk;
-  const int nrows = min(PB, P.rows - r0);
-  const int b = P.b, K = P.K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;       // warp tile 32 x 16
+  const bool ident = P.Xin == nullptr;
 
+#pragma unroll 1
+  for (int q = P.q_begin; q < P.q_end; ++q) {
+    const int p = PB * q, b = min(PB, P.cols - p), K = p;
+    const int nrows = min(PB, (ident ? min(P.rows, p + b) : P.rows) - r0);
+    if (b <= 0) break;
+    if (nrows <= 0) continue;   // identity: these rows of L^-T start at a later block column
+    const double* __restrict__ Lb = P.Lb + (size_t)p * P.ldlb;
+    const double* __restrict__ Lq = P.Linv + (size_t)q * PB * PB;
 #pragma unroll 4
-  for (int t = tid; t < PB * PB; t += RW_THREADS) {
-    const int i = t / PB, x = t % PB;
-    cp_async8(Li + i * SD + x, P.Linv + (size_t)i * PB + x, true);
-  }
-  auto load_stage = [&](int st, int k0) {
-    double* as = As + st * PB * TS_S;
-    double* bs = Bs + st * PB * TS_S;
-#pragma unroll
-    for (int u = 0; u < (PB * TS_BK) / RW_THREADS; ++u) {
-      const int idx = tid + u * RW_THREADS;
-      const int m = idx / TS_BK, k = idx % TS_BK;
-      const bool va = m < nrows && k0 + k < K;
-      cp_async8(as + m * TS_S + k, va ? P.A + (size_t)(r0 + m) * P.lda + k0 + k : P.A, va);
-      const bool vb = m < b && k0 + k < K;
-      cp_async8(bs + m * TS_S + k, vb ? P.Lb + (size_t)m * P.ldlb + k0 + k : P.Lb, vb);
+    for (int t = tid; t < PB * PB; t += RW_THREADS) {
+      const int i = t / PB, x = t % PB;
+      cp_async8(Li + i * SD + x, Lq + (size_t)i * PB + x, true);
     }
-  };
-  const int KT = (K + TS_BK - 1) / TS_BK;
-  if (KT > 0) load_stage(0, 0);
-  cp_async_commit();
-
-  double acc[4][2][2];
+    auto load_stage = [&](int st, int k0) {
+      double* as = As + st * PB * TS_S;
+      double* bs = Bs + st * PB * TS_S;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq + e;
-        double v = 0.0;
-        if (m < nrows && c < b)
-          v = P.Xin ? P.Xin[(size_t)(r0 + m) * P.ldx + c] : ((r0 + m == P.p0 + c) ? 1.0 : 0.0);
-        acc[i][j][e] = -v;
+      for (int u = 0; u < (PB * TS_BK) / RW_THREADS; ++u) {
+        const int idx = tid + u * RW_THREADS;
+        const int m = idx / TS_BK, k = idx % TS_BK;
+        const bool va = m < nrows && k0 + k < K;
+        cp_async8(as + m * TS_S + k, va ? P.Xout + (size_t)(r0 + m) * P.ldx + k0 + k : P.Xout, va);
+        const bool vb = m < b && k0 + k < K;
+        cp_async8(bs + m * TS_S + k, vb ? Lb + (size_t)m * P.ldlb + k0 + k : Lb, vb);
       }
-  for (int kt = 0; kt < KT; ++kt) {
-    if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
+    };
+    const int KT = (K + TS_BK - 1) / TS_BK;
+    if (KT > 0) load_stage(0, 0);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double* as = As + (kt & 1) * PB * TS_S;
-    const double* bs = Bs + (kt & 1) * PB * TS_S;
-#pragma unroll
-    for (int kk = 0; kk < TS_BK; kk += 4) {
-      double af[4], bf[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[(wm * 32 + i * 8 + g) * TS_S + kk + tq];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * TS_S + kk + tq];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma884(acc[i][j], af[i], bf[j]);
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  // C = Xin - A Lb^T = -acc  ->  smem, then Xout = C Linv^T
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq;
-      Cs[m * SD + c] = -acc[i][j][0];
-      Cs[m * SD + c + 1] = -acc[i][j][1];
-    }
-  __syncthreads();
-  double out[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
-#pragma unroll 4
-  for (int kk = 0; kk < PB; kk += 4) {
-    double af[4], bf[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = Cs[(wm * 32 + i * 8 + g) * SD + kk + tq];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) bf[j] = Li[(wn * 16 + j * 8 + g) * SD + kk + tq];
+
+    double acc[4][2][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) dmma884(out[i][j], af[i], bf[j]);
-  }
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = wm * 32 + i * 8 + g;
-    if (m >= nrows) continue;
-    double* dst = P.Xout + (size_t)(r0 + m) * P.ldx;
+        for (int e = 0; e < 2; ++e) {
+          const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq + e;
+          double v = 0.0;
+          if (m < nrows && c < b)
+            v = ident ? ((r0 + m == p + c) ? 1.0 : 0.0) : P.Xin[(size_t)(r0 + m) * P.ldx + p + c];
+          acc[i][j][e] = -v;
+        }
+    for (int kt = 0; kt < KT; ++kt) {
+      if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const double* as = As + (kt & 1) * PB * TS_S;
+      const double* bs = Bs + (kt & 1) * PB * TS_S;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = wn * 16 + j * 8 + 2 * tq;
-      if (c < b) dst[c] = out[i][j][0];
-      if (c + 1 < b) dst[c + 1] = out[i][j][1];
+      for (int kk = 0; kk < TS_BK; kk += 4) {
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = as[(wm * 32 + i * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      }
+      __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();
+    // C = Xin - A Lb^T = -acc  ->  smem, then Xout = C Linv^T
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq;
+        Cs[m * SD + c] = -acc[i][j][0];
+        Cs[m * SD + c + 1] = -acc[i][j][1];
+      }
+    __syncthreads();
+    double out[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < PB; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Cs[(wm * 32 + i * 8 + g) * SD + kk + tq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Li[(wn * 16 + j * 8 + g) * SD + kk + tq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(out[i][j], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = wm * 32 + i * 8 + g;
+      if (m >= nrows) continue;
+      double* dst = P.Xout + (size_t)(r0 + m) * P.ldx + p;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = wn * 16 + j * 8 + 2 * tq;
+        if (c < b) dst[c] = out[i][j][0];
+        if (c + 1 < b) dst[c + 1] = out[i][j][1];
+      }
+    }
+    __syncthreads();   // the next panel reads these columns back (and reuses Li / Cs)
   }
 }
 
@@ -847,12 +874,17 @@ extern "C" int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, con
     return h2g_set_error(H2G_EINVAL, "h2g_chol_panel: null argument");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(h2g::chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
+    cudaFuncSetAttribute(h2g::chol_diag_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
+    cudaFuncSetAttribute(h2g::chol_diag_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
     cudaFuncSetAttribute(h2g::chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::RW_SMEM);
     attr = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  h2g::chol_diag_kernel<<<count, h2g::DIAG_THREADS, h2g::DIAG_SMEM, st>>>(d_descs, d_npd);
+  // many boxes: the 4-warp variant fits 3 CTAs per SM (throughput); few boxes: 8 warps (latency)
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (count >= 2 * sms) h2g::chol_diag_kernel<4><<<count, 128, h2g::DIAG_SMEM, st>>>(d_descs, d_npd);
+  else h2g::chol_diag_kernel<8><<<count, 256, h2g::DIAG_SMEM, st>>>(d_descs, d_npd);
   int rc = h2g_check_launch("chol_diag");
   if (rc || total_tiles <= 0) return rc;
   h2g::chol_rows_kernel<<<total_tiles, h2g::RW_THREADS, h2g::RW_SMEM, st>>>(d_descs, d_tile_map);

@@ -42,6 +42,15 @@ def copy_tiles(rows, cols):
     return (-(-rows // nat.COPY_TILE)) * (-(-cols // nat.COPY_TILE))
 
 
+def _ablated_lanes():
+    """H2G_ABLATE_LANES="3,4" turns every step of those lanes into a NOP (events kept).
+    Measurement aid for critical-path analysis only: the results are wrong."""
+    import os
+
+    v = os.environ.get("H2G_ABLATE_LANES", "")
+    return {int(x) for x in v.split(",") if x.strip()}
+
+
 class Program:
     """Accumulates steps; `finalize()` uploads descriptors and resolves pointers."""
 
@@ -143,21 +152,26 @@ class Program:
         return int(tiles.sum())
 
     def trsm_rows(self, descs):
-        """descs: list of (A, Lb, Xin, Xout, Linv, rows, b, K, p0, lda, ldlb, ldx): left-looking
-        block-column solve Xout = (Xin - A Lb^T) Linv^T, one CTA per 64-row chunk (h2g_trsm_rows)."""
-        descs = [d for d in descs if d[5] > 0 and d[6] > 0]
+        """descs: list of (Lb, Xin, Xout, Linv, rows, cols, q_begin, q_end, ldlb, ldx): X = B L^-T for
+        the block columns [q_begin, q_end) (h2g_trsm_rows), one CTA per 64-row chunk."""
+        descs = [d for d in descs if d[4] > 0 and d[5] > 0 and d[7] > d[6]]
         if not descs:
             return 0
         arr = np.zeros(len(descs), dtype=nat.ROWS_DT)
-        for name, col in zip(("A", "Lb", "Xin", "Xout", "Linv", "rows", "b", "K", "p0", "lda", "ldlb", "ldx"),
+        for name, col in zip(("Lb", "Xin", "Xout", "Linv", "rows", "cols", "q_begin", "q_end", "ldlb", "ldx"),
                              zip(*descs)):
             arr[name] = col
         tiles = -(-arr["rows"].astype(np.int64) // nat.PANEL_WIDTH)
         arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
-        m, b, k = arr["rows"].astype(np.int64), arr["b"].astype(np.int64), arr["K"].astype(np.int64)
-        self._add(nat.STEP["TRSM_ROWS"], len(descs), int(tiles.sum()), self._blob(arr), self._blob(tmap),
-                  flops=int((2 * m * b * k + m * b * b).sum()))
+        fl = 0
+        W = nat.PANEL_WIDTH
+        for d in descs:   # useful flops: rows x b x (2 p + b) per panel (update + triangular solve)
+            for q in range(d[6], d[7]):
+                p, b = W * q, min(W, d[5] - W * q)
+                m = d[4] if d[1] else min(d[4], p + b)
+                fl += m * b * (2 * p + b)
+        self._add(nat.STEP["TRSM_ROWS"], len(descs), int(tiles.sum()), self._blob(arr), self._blob(tmap), flops=fl)
         return int(tiles.sum())
 
     def copy(self, descs):
@@ -272,8 +286,9 @@ class Program:
                 return v[1]
             return base + offs[v] if v >= 0 else 0
 
+        ablate = _ablated_lanes()
         for q, st in enumerate(self._steps):
-            steps[q]["kind"] = st["kind"]
+            steps[q]["kind"] = nat.STEP["NOP"] if st["lane"] in ablate else st["kind"]
             steps[q]["count"] = st["count"]
             steps[q]["grid"] = st["grid"]
             steps[q]["arg"] = st["arg"]

@@ -302,17 +302,17 @@ class FactorPlan:
 
           lane 0:  [wait REST(q-2)] -> PANEL(q) -> [wait REST(q-1)] -> PANEL(q+1) ...
           lane 1:          [wait PANEL(q)] -> REST(q)
-          lane 4:          [wait PANEL(q)] -> ROWS_V(q)
+          lane 4:          [wait last PANEL] -> ROWS_V (all block columns, one launch)
 
         PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
         panel q-1 to block column q, factors the diagonal block and TRSMs the
         rows below; REST(q) applies panel q to the columns < r right of block
         column q+1 (lower tiles of RR, all SR rows); the SS corner receives its
         single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.
-        ROWS_V(q) (h2g_trsm_rows, left-looking) forms block column q of
-        R = Q_red L^-T = V from Q (Qp) and the solved columns < q, off the
-        critical lane; with Qp == 0 the ride-along is the identity and R
-        becomes L^-T (the root's explicit inverse for the solve).  Returns
+        ROWS_V (h2g_trsm_rows, left-looking, one CTA per 64 rows walking all
+        block columns) forms R = Q_red L^-T = V from Q (Qp) off the critical
+        lane; with Qp == 0 (the root) the identity rides along panel by panel
+        and R becomes L^-T (the root's explicit inverse for the solve).  Returns
         (linv, loff, event after the last R column or None)."""
         nb = len(n)
         mine = np.ones(nb, dtype=bool) if mine is None else mine
@@ -345,13 +345,9 @@ class FactorPlan:
                     if ni > ri:                          # SR rows
                         rest.append((h + 8 * (ri * ni + p), x, h + 8 * (ri * ni + c0), ni - ri, ri - c0, b,
                                      ni, ni, ni, 0, -1.0, 1.0))
-                if Rp:
-                    rr = Rp + 8 * int(qo[i])
-                    lb = h + 8 * (p * ni)                # L[p:p+b, 0:p]
-                    if Qp:                               # V = Q_red L^-T
-                        rows.append((rr, lb, Qp + 8 * int(qo[i] + p), rr + 8 * p, li, ni, b, p, 0, ni, ni, ni))
-                    else:                                # L^-T (upper: rows < p + b only)
-                        rows.append((rr, lb, 0, rr + 8 * p, li, p + b, b, p, p, ni, ni, ni))
+                if Rp and not Qp:                        # root: L^-T panel by panel (rows < p + b)
+                    rows.append((h, 0, Rp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, ni, ri, q, q + 1,
+                                 ni, ni))
             done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
             if done:
                 prog.wait(done[-1])              # block column q has all updates of panels <= q-2
@@ -370,6 +366,15 @@ class FactorPlan:
                 prog.lane = 4
                 prog.wait(ev_fp)
                 prog.trsm_rows(rows)
+            prog.lane = 0
+        if Rp and Qp:
+            # V = Q_red L^-T for every box in ONE launch once all panels are factored:
+            # each CTA walks the block columns of its 64 rows (left-looking)
+            prog.lane = 4
+            prog.wait(ev_fp)
+            prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
+                             lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]), int(n[i]))
+                            for i in range(nb) if mine[i] and r[i] > 0])
             prog.lane = 0
         ev_v = None
         if Rp:
@@ -593,18 +598,59 @@ def _remember(key, dh2, plan):
 
 def factorize(h2, batched=True, retain=False):
     """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
-    if retain:
-        raise NotImplementedError("retain=True (pre-factorization slab copies) is not supported on the GPU path yet")
     nat.lib()
     dh2, plan = _cached_plan(h2)
     plan.capture()
     plan.run()
     plan.check_pivots()
     f = factors_from_plan(h2, plan)
+    if retain:
+        f.retained = _retained_views(plan)
     for key, ent in list(_PLAN_CACHE.items()):
         if ent[1] is plan:
             _PLAN_CACHE[key] = (ent[0], ent[1], weakref.ref(f))
     return f
+
+
+def _retained_views(plan):
+    """`factors.retained` of factorize(..., retain=True) (ulv_factor.py:161-162,
+    210-214, 273-279): the sparsified blocks Q_i^T A_ij Q_j (i >= j near) split
+    into rr / rs / sr / ss0, before any elimination.  The level's near blocks
+    A_ij and bases stay in HBM after the factorization, so the slabs are formed
+    on access (one device GEMM pair per block) instead of being copied eagerly;
+    the values are the same."""
+    keys, src = [], {}
+    for l, B in plan.bufs.items():
+        lay = B.lay
+        for (i, j) in lay.near_pairs:
+            for part in ("rr", "rs", "sr", "ss0"):
+                keys.append((part, l, i, j))
+            src[(l, i, j)] = B
+    cache = {}
+
+    def block(l, i, j):
+        if (l, i, j) not in cache:
+            B = src[(l, i, j)]
+            lay = B.lay
+            n = lay.n
+            q = plan.dh2.q[l]
+            qi = q[int(lay.qoff[i]): int(lay.qoff[i] + n[i] * n[i])].view(int(n[i]), int(n[i]))
+            qj = q[int(lay.qoff[j]): int(lay.qoff[j] + n[j] * n[j])].view(int(n[j]), int(n[j]))
+            off = int(B.aoff[(i, j)])
+            a = B.a[off: off + int(n[i] * n[j])].view(int(n[i]), int(n[j]))
+            if i == j:   # only the lower triangle of a merged diagonal block is maintained
+                a = torch.tril(a) + torch.tril(a, -1).T
+            cache[(l, i, j)] = (qi.T @ a @ qj).cpu().numpy()
+        return cache[(l, i, j)]
+
+    def fetch(key):
+        part, l, i, j = key
+        h = block(l, i, j)
+        lay = plan.bufs[l].lay
+        ri, rj = int(lay.r[i]), int(lay.r[j])
+        return {"rr": h[:ri, :rj], "rs": h[:ri, rj:], "sr": h[ri:, :rj], "ss0": h[ri:, rj:]}[part].copy()
+
+    return _LazyBlocks(keys, fetch)
 
 
 def factors_from_plan(h2, plan):

@@ -93,3 +93,24 @@ def test_repeat_is_bitwise_deterministic(pkg):
     for l in fa.levels:
         for i in fa.levels[l].lr_diag:
             assert np.array_equal(fa.levels[l].lr_diag[i], fb.levels[l].lr_diag[i])
+
+
+@pytest.mark.parametrize("name", H2_FIXTURES[:1])
+def test_retain_slabs_consistent(pkg, name):
+    """retain=True (ulv_factor.py:161-162, 210-214, 273-279): the sparsified
+    slabs Q_i^T A_ij Q_j before elimination; L(r)_ii L(r)_ii^T = rr_ii and
+    lr_off_ij L(r)_jj^T = rr_ij."""
+    h2 = load_h2(name)
+    f = pkg.factorize(h2, retain=True)
+    assert f.retained is not None
+    for l, lvl in f.levels.items():
+        for i, (r, k) in lvl.dims.items():
+            if r == 0:
+                continue
+            rr = f.retained[("rr", l, i, i)]
+            L = lvl.lr_diag[i]
+            assert _rel(L @ L.T, rr) < 1e-10, (l, i)
+            assert f.retained[("ss0", l, i, i)].shape == (k, k)
+        for (i, j), lo in lvl.lr_off.items():
+            if lo.size:
+                assert _rel(lo @ lvl.lr_diag[j].T, f.retained[("rr", l, i, j)]) < 1e-10, (l, i, j)

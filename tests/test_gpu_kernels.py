@@ -72,32 +72,31 @@ def test_chol_panel_reports_first_bad_pivot(env):
     assert int(npd.item()) == bad
 
 
-@pytest.mark.parametrize("rows,b,K,ident", [(256, 64, 128, False), (100, 33, 64, False), (70, 64, 0, False),
-                                            (192, 64, 128, True)])
-def test_trsm_rows(env, rows, b, K, ident):
-    """Xout = (Xin - A Lb^T) Linv^T, Xin = identity columns p0.. when ident."""
+@pytest.mark.parametrize("rows,cols,qb,qe,ident", [(256, 213, 0, 4, False), (100, 64, 0, 1, False),
+                                                    (70, 150, 0, 3, False), (300, 300, 0, 5, True),
+                                                    (200, 200, 2, 3, True)])
+def test_trsm_rows(env, rows, cols, qb, qe, ident):
+    """X = B L^-T, block columns [qb, qe) (left-looking, h2g_trsm_rows); B = I when ident."""
     torch, nat, Program = env
-    rng = np.random.default_rng(rows + b + K)
-    A = rng.standard_normal((rows, K))
-    Lb = rng.standard_normal((b, K))
-    ld = np.tril(rng.standard_normal((b, b))) + 4 * np.eye(b)
-    li = np.zeros((64, 64))
-    li[:b, :b] = np.linalg.inv(ld)
-    p0 = K
-    xin = np.zeros((rows, b))
-    if ident:
-        for c in range(b):
-            if p0 + c < rows:
-                xin[p0 + c, c] = 1.0
-    else:
-        xin = rng.standard_normal((rows, b))
-    ref = (xin - A @ Lb.T) @ li[:b, :b].T
+    rng = np.random.default_rng(rows + cols + qb)
+    L = np.tril(rng.standard_normal((cols, cols))) * 0.1 + 2 * np.eye(cols)
+    nq = -(-cols // 64)
+    linv = np.zeros((nq, 64, 64))
+    for q in range(nq):
+        p, b = 64 * q, min(64, cols - 64 * q)
+        linv[q, :b, :b] = np.linalg.inv(L[p:p + b, p:p + b])
+    B = np.eye(rows, cols) if ident else rng.standard_normal((rows, cols))
+    ref = np.linalg.solve(L, B.T).T          # B L^-T
     t = lambda m: torch.from_numpy(np.ascontiguousarray(m)).cuda()
-    Ad, Lbd, Xd, Lid = t(A if K else np.zeros((rows, 1))), t(Lb if K else np.zeros((b, 1))), t(xin), t(li)
-    Xo = torch.zeros_like(Xd)
+    Ld, Bd, Lid = t(L), t(B), t(linv)
+    X = torch.zeros_like(Bd)
+    if qb > 0:                               # columns < 64 qb already solved
+        X[:, :64 * qb] = t(ref[:, :64 * qb])
     prog = Program(torch.device("cuda"))
-    prog.trsm_rows([(Ad.data_ptr(), Lbd.data_ptr(), 0 if ident else Xd.data_ptr(), Xo.data_ptr(), Lid.data_ptr(),
-                     rows, b, K, p0, max(K, 1), max(K, 1), b)])
+    prog.trsm_rows([(Ld.data_ptr(), 0 if ident else Bd.data_ptr(), X.data_ptr(), Lid.data_ptr(), rows, cols, qb, qe,
+                     cols, cols)])
     prog.finalize().run()
     torch.cuda.synchronize()
-    np.testing.assert_allclose(Xo.cpu().numpy(), ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+    hi = min(cols, 64 * qe)
+    got = X.cpu().numpy()
+    np.testing.assert_allclose(got[:, 64 * qb:hi], ref[:, 64 * qb:hi], rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
