@@ -36,6 +36,19 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
+// Row of lower-triangular tile t (t = i(i+1)/2 + j, j <= i) without FP64 math.
+__device__ __forceinline__ int tri_row(int t) {
+  int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  return i;
+}
+
+// Sign flip of a double on the integer pipe (keeps the FP64 pipe free for DMMA).
+__device__ __forceinline__ double neg_int(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
 // Largest index p in [0, n) with starts[p] <= x (starts ascending).
 __device__ __forceinline__ int upper_index(const int32_t* starts_strided, int stride_ints, int n, int x) {
   int lo = 0, hi = n - 1;

@@ -54,9 +54,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   int t = tile - P.tile_start;
   int tm, tn;
   if (P.flags & H2G_GEMM_LOWER) {
-    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((i + 1) * (i + 2) / 2 <= t) ++i;
-    while (i * (i + 1) / 2 > t) --i;
+    const int i = tri_row(t);
     tm = i;
     tn = t - i * (i + 1) / 2;
   } else {
@@ -82,7 +80,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   const int ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
   // preload beta/alpha * C so the epilogue is a pure store
-  const double cscale = (beta != 0.0 && alpha != 0.0) ? beta / alpha : 0.0;
+  // C preload scale beta/alpha: the common +-1 cases stay off the FP64 pipe (it is the DMMA pipe)
+  const int cmode = (beta == 0.0 || alpha == 0.0) ? 0 : beta == alpha ? 1 : beta == -alpha ? 2 : 3;
+  const double cscale = cmode == 3 ? beta / alpha : 1.0;
 #pragma unroll
   for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -90,12 +90,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       const int row = m0 + wm * C::WM + i * 8 + g;
       const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double v = 0.0;
-        if (cscale != 0.0 && row < M && col + e < N) v = cscale * Cp[(size_t)row * ldc + col + e];
-        acc[i][j][e] = v;
-      }
+      for (int e = 0; e < 2; ++e) acc[i][j][e] = (cmode && row < M && col + e < N) ? Cp[(size_t)row * ldc + col + e] : 0.0;
     }
+  if (cmode == 2) {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        acc[i][j][0] = neg_int(acc[i][j][0]);
+        acc[i][j][1] = neg_int(acc[i][j][1]);
+      }
+  } else if (cmode == 3) {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        acc[i][j][0] *= cscale;
+        acc[i][j][1] *= cscale;
+      }
+  }
 
   auto load_stage = [&](int stage, int k0) {
     double* as = As + stage * C::A_DBL;
@@ -171,8 +184,41 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
   cp_async_wait<0>();
 
-  // epilogue: C = alpha * acc   (acc already holds beta/alpha * C_old)
+  // epilogue: C = alpha * acc   (acc already holds beta/alpha * C_old); alpha = +-1 stays off the FP64 pipe
   if (upper_warp) return;
+  if (alpha == 0.0) {  // degenerate: C = beta * C
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int row = m0 + wm * C::WM + i * 8 + g;
+      if (row >= M) continue;
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
+        double* cp = Cp + (size_t)row * ldc + col;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (col + e < N) cp[e] = beta * cp[e];
+      }
+    }
+    return;
+  }
+  if (alpha == -1.0) {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        acc[i][j][0] = neg_int(acc[i][j][0]);
+        acc[i][j][1] = neg_int(acc[i][j][1]);
+      }
+  } else if (alpha != 1.0) {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        acc[i][j][0] *= alpha;
+        acc[i][j][1] *= alpha;
+      }
+  }
 #pragma unroll
   for (int i = 0; i < C::MI; ++i) {
     const int row = m0 + wm * C::WM + i * 8 + g;
@@ -181,21 +227,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
     for (int j = 0; j < C::NI; ++j) {
       const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
       double* cp = Cp + (size_t)row * ldc + col;
-      if (alpha == 0.0) {  // degenerate: C = beta * C
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (col + e < N) cp[e] = beta * cp[e];
-        continue;
+      if (col + 1 < N) {
+        cp[0] = acc[i][j][0];
+        cp[1] = acc[i][j][1];
+      } else if (col < N) {
+        cp[0] = acc[i][j][0];
       }
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (col + e < N) cp[e] = alpha * acc[i][j][e];
     }
   }
 }
 
-// Same tiling with the m16n8k16 FP64 MMA (one instruction per 16x8x16 block):
-// warp tile 32x32 = 2 x 4 MMAs per 16-deep k step.
 template <class C, bool TA, bool TB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_kernel(const h2g_gemm_problem* __restrict__ probs,
                                                                       const int32_t* __restrict__ tile_map) {
@@ -211,9 +252,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_ke
   int t = tile - P.tile_start;
   int tm, tn;
   if (P.flags & H2G_GEMM_LOWER) {
-    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((i + 1) * (i + 2) / 2 <= t) ++i;
-    while (i * (i + 1) / 2 > t) --i;
+    const int i = tri_row(t);
     tm = i;
     tn = t - i * (i + 1) / 2;
   } else {
@@ -236,7 +275,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_ke
   double* Cp = P.C;
   const int ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
-  const double cscale = (beta != 0.0 && alpha != 0.0) ? beta / alpha : 0.0;
+  const int cmode = (beta == 0.0 || alpha == 0.0) ? 0 : beta == alpha ? 1 : beta == -alpha ? 2 : 3;
+  const double cscale = cmode == 3 ? beta / alpha : 1.0;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -246,7 +286,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_ke
         const int row = m0 + wm * 32 + i * 16 + g + 8 * (e >> 1);
         const int col = n0 + wn * 32 + j * 8 + 2 * tq + (e & 1);
         double v = 0.0;
-        if (cscale != 0.0 && row < M && col < N) v = cscale * Cp[(size_t)row * ldc + col];
+        if (cmode && row < M && col < N) {
+          v = Cp[(size_t)row * ldc + col];
+          v = cmode == 1 ? v : cmode == 2 ? neg_int(v) : cscale * v;
+        }
         acc[i][j][e] = v;
       }
 
@@ -341,8 +384,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_ke
           continue;
         }
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (col + e < N) cp[e] = alpha * acc[i][j][2 * h + e];
+        for (int e = 0; e < 2; ++e) {
+          const double a = acc[i][j][2 * h + e];
+          if (col + e < N) cp[e] = alpha == 1.0 ? a : alpha == -1.0 ? neg_int(a) : alpha * a;
+        }
       }
     }
 }

@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(con
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = wn * 16 + j * 8 + 2 * tq + e;
-          acc[v][i][j][e] = (s < b && col <= s) ? -H[(size_t)(p + s) * ldh + p + col] : 0.0;
+          acc[v][i][j][e] = (s < b && col <= s) ? neg_int(H[(size_t)(p + s) * ldh + p + col]) : 0.0;
         }
     }
   }
@@ -586,8 +586,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(con
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int s = wm * 32 + i * 8 + g, col = wn * 16 + j * 8 + 2 * tq;
-        S[s * SD + col] = -acc[v][i][j][0];
-        S[s * SD + col + 1] = -acc[v][i][j][1];
+        S[s * SD + col] = neg_int(acc[v][i][j][0]);
+        S[s * SD + col + 1] = neg_int(acc[v][i][j][1]);
       }
   }
   __syncthreads();
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = wn * 16 + j * 8 + 2 * tq + e;
-        acc[i][j][e] = (c < nrows && col < b) ? -H[(size_t)(row0 + c) * ldh + p + col] : 0.0;
+        acc[i][j][e] = (c < nrows && col < b) ? neg_int(H[(size_t)(row0 + c) * ldh + p + col]) : 0.0;
       }
   }
   PTRACE(1);
@@ -665,8 +665,8 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int c = wm * 32 + i * 8 + g, col = wn * 16 + j * 8 + 2 * tq;
-      C[c * SD + col] = -acc[i][j][0];
-      C[c * SD + col + 1] = -acc[i][j][1];
+      C[c * SD + col] = neg_int(acc[i][j][0]);
+      C[c * SD + col + 1] = neg_int(acc[i][j][1]);
     }
   __syncthreads();
   // X_c <- C L_pp^-T
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
           double v = 0.0;
           if (m < nrows && c < b)
             v = ident ? ((r0 + m == p + c) ? 1.0 : 0.0) : P.Xin[(size_t)(r0 + m) * P.ldx + p + c];
-          acc[i][j][e] = -v;
+          acc[i][j][e] = neg_int(v);
         }
     for (int kt = 0; kt < KT; ++kt) {
       if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
@@ -805,8 +805,8 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq;
-        Cs[m * SD + c] = -acc[i][j][0];
-        Cs[m * SD + c + 1] = -acc[i][j][1];
+        Cs[m * SD + c] = neg_int(acc[i][j][0]);
+        Cs[m * SD + c + 1] = neg_int(acc[i][j][1]);
       }
     __syncthreads();
     double out[4][2][2];
