@@ -453,6 +453,7 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   if (tile_cfg == 2) return h2g::dispatch<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 3) return h2g::dispatch_k16<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 4) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 6) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg != 0) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d", tile_cfg);
   return h2g::dispatch<h2g::Cfg64>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
 }

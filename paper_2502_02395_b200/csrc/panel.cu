@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
 #pragma unroll
     for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
 #pragma unroll 4
-  for (int kk = 0; kk < PB; kk += 4) {
+  for (int kk = 0; kk < 16 * (wn + 1); kk += 4) {   // Linv[n][k] = 0 for k > n
     double af[4], bf[2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) af[i] = C[(wm * 32 + i * 8 + g) * SD + kk + tq];
@@ -815,7 +815,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
 #pragma unroll
       for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
 #pragma unroll 4
-    for (int kk = 0; kk < PB; kk += 4) {
+    for (int kk = 0; kk < 16 * (wn + 1); kk += 4) {   // Linv[n][k] = 0 for k > n
       double af[4], bf[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = Cs[(wm * 32 + i * 8 + g) * SD + kk + tq];

@@ -26,13 +26,15 @@ def gemm_tiles(m, n, flags=0, cfg=0):
     return (-(-m // t)) * (-(-n // t))
 
 
-def choose_tile_cfg(ms, ns, flags, sms=148):
+def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False):
     """Tile configuration of a grouped GEMM launch.
 
-    Measured on B200 (tools/gemm_bench.py, profiles/): the 64x64 2-stage
-    variant at 4 CTAs/SM (cfg 2) beats both the 3-stage 64x64 (cfg 0) and the
-    128x128 tile (cfg 1, 1 CTA/SM at ~240 registers) for every shape on this
-    path, from the K = 64 Cholesky updates to 900^3 transforms."""
+    Measured on B200 (tools/gemm_bench.py, profiles/r01_gemm_tile_configs*.jsonl):
+    the 64x64 2-stage DMMA.8x8x4 variant at 4 CTAs/SM (cfg 2) is the fastest for
+    the NN / TN transforms (30 TFLOP/s on 4096 x 256^3).  The 3-stage
+    m16n8k16 variant at 3 CTAs/SM (cfg 6) is 7-13% faster on isolated K = 64
+    NT updates but made the whole factorization slower in place (C2 8.52 ->
+    8.56 ms, M1 29.1 -> 29.3 ms), so every launch uses cfg 2."""
     return 2
 
 
@@ -104,7 +106,7 @@ class Program:
         cols = list(zip(*rows))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
             arr[name] = col
-        cfg = choose_tile_cfg(arr["M"], arr["N"], arr["flags"]) if tile_cfg is None else tile_cfg
+        cfg = choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b)) if tile_cfg is None else tile_cfg
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
                          dtype=np.int64)
         starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])
