@@ -424,7 +424,21 @@ def _attach_host_views(h2, dh2, choice, lqs):
 
 def h2_matvec(h2, x):
     """y = A x through the hierarchical representation, tree order
-    (h2_build.py:232-282).  Host numpy: measurement support for residuals."""
+    (h2_build.py:232-282).  On the GPU (one grouped GEMV per level and pass,
+    matvec_device.MatvecPlan) when the operands are in HBM (our construct);
+    otherwise the reference's host algorithm."""
+    if getattr(h2, "_device", None) is not None:
+        from .matvec_device import device_matvec
+
+        xm = np.asarray(x, dtype=np.float64)
+        if xm.reshape(xm.shape[0], -1).shape[0] != h2.count:
+            raise ValueError("length mismatch")
+        return device_matvec(h2, xm)
+    return h2_matvec_host(h2, x)
+
+
+def h2_matvec_host(h2, x):
+    """The reference's host H² matvec (h2_build.py:232-282), numpy."""
     x = np.asarray(x, dtype=np.float64)
     vec = x.ndim == 1
     xm = x.reshape(h2.count, -1)

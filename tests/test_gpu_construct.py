@@ -111,3 +111,23 @@ def test_many_boxes_multi_panel_matches_oracle(pkg):
     b = np.random.default_rng(1).standard_normal(h2.count)
     x, xo = pkg.solve(f, b), orc.solve(of, b)
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-9
+
+
+@pytest.mark.parametrize("family,shape", [("laplace", "cube"), ("yukawa", "sphere")])
+def test_device_matvec_matches_host(pkg, family, shape):
+    """GPU H2 matvec (matvec_device.MatvecPlan) == the reference's host algorithm
+    (h2_build.py:232-282) on the same operands, vector and multi-RHS."""
+    from paper_2502_02395_b200.h2_build import h2_matvec_host
+
+    gen = pkg.gen_uniform_cube if shape == "cube" else pkg.gen_sphere_surface
+    cloud = gen(4096, seed=3)
+    tree = pkg.build_tree(cloud, 128)
+    lists = pkg.build_interaction_lists(tree, 1.0)
+    cfg = pkg.BuildConfig(eta=1.0, leaf_max=128, tol=1e-8, s_far=256, s_near=256)
+    h2 = pkg.construct(pkg.KernelSpec(family=family, diagonal_shift=1e4), tree, lists, cfg, cloud)
+    rng = np.random.default_rng(0)
+    for x in (rng.standard_normal(cloud.count), rng.standard_normal((cloud.count, 3))):
+        y = pkg.h2_matvec(h2, x)
+        yh = h2_matvec_host(h2, x)
+        assert y.shape == yh.shape
+        assert np.linalg.norm(y - yh) / np.linalg.norm(yh) < 1e-13
