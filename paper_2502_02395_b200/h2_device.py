@@ -10,7 +10,8 @@ Layout in HBM (all FP64, row-major, one allocation per level and kind):
   root_a    the single block when the tree has depth 0.
 
 `DeviceH2.from_host(h2)` uploads a numpy H2Matrix (the reference's, or a
-host-materialized one) through one pinned staging buffer per kind;
+host-materialized one) through one reusable pinned staging buffer (bases as
+contiguous q_red / q_skel, interleaved into q_full on the device);
 `h2_build.construct` produces a DeviceH2 directly on the GPU.
 """
 
@@ -50,9 +51,11 @@ def _run_tasks(tasks):
 
 
 def _fill_q(host, off, basis, n, k):
-    blk = host[off:off + n * n].reshape(n, n)
-    blk[:, :n - k] = basis.q_red
-    blk[:, n - k:] = basis.q_skel
+    """q_red then q_skel, each contiguous (fast memcpy); the GPU interleaves
+    them into the row-major q_full = [q_red | q_skel] (one block-copy launch)."""
+    r = n - k
+    host[off:off + n * r].reshape(n, r)[...] = basis.q_red
+    host[off + n * r:off + n * n].reshape(n, k)[...] = basis.q_skel
 
 
 def _fill_flat(host, off, arr):
@@ -97,6 +100,25 @@ class LevelLayout:
             acc += int(self.k[i] * self.k[j])
         self.soff = soff
         self.ssize = acc
+
+
+def _q_interleave(levels, q, device):
+    """Device staging for the bases (q_red, q_skel contiguous per box) and the
+    block-copy program that forms q_full = [q_red | q_skel] row-major in q[l]."""
+    from .program import Program
+
+    qsplit = {l: torch.empty(max(lay.qsize, 1), dtype=F64, device=device) for l, lay in levels.items()}
+    prog = Program(device)
+    descs = []
+    for l, lay in levels.items():
+        sp, qp = qsplit[l].data_ptr(), q[l].data_ptr()
+        for i in range(lay.nb):
+            n, k = int(lay.n[i]), int(lay.k[i])
+            r, o = n - k, int(lay.qoff[i])
+            descs.append((sp + 8 * o, qp + 8 * o, n, r, r, n, 0))
+            descs.append((sp + 8 * (o + n * r), qp + 8 * (o + r), n, k, k, n, 0))
+    prog.copy(descs)
+    return qsplit, prog.finalize()
 
 
 class DeviceH2:
@@ -166,16 +188,18 @@ class DeviceH2:
         host_t, host = _staging(off)
         if into is not None:
             q, s, leaf_a = into.q, into.s, into.leaf_a
+            qsplit, qprog = into._qsplit, into._qprog
         else:
             q = {l: torch.empty(lay.qsize, dtype=F64, device=device) for l, lay in levels.items()}
             s = {l: torch.empty(max(lay.ssize, 1), dtype=F64, device=device) for l, lay in levels.items()}
             leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
+            qsplit, qprog = _q_interleave(levels, q, device)
         # chunks of ~4M doubles inside one region: gathered by the thread pool, each
         # DMA'd to HBM as soon as it is complete (gather and H2D overlap)
         chunks = []
         for kind, l, base, size in regions:
             lay = levels[l]
-            dst = q[l] if kind == "q" else s[l] if kind == "s" else leaf_a
+            dst = qsplit[l] if kind == "q" else s[l] if kind == "s" else leaf_a
             if kind == "q":
                 items = [(int(lay.qoff[i]), int(lay.n[i] * lay.n[i]),
                           (_fill_q, host, base + int(lay.qoff[i]), h2.bases[(l, i)], int(lay.n[i]), int(lay.k[i])))
@@ -199,8 +223,13 @@ class DeviceH2:
         for (dst, base, c0, c1, _), fu in zip(chunks, futs):
             fu.result()
             dst[c0:c1].copy_(host_t[base + c0:base + c1], non_blocking=True)
+        qprog.run()                                       # [q_red | q_skel] rows, on the device
         torch.cuda.current_stream(device).synchronize()  # staging buffer is reused by the next upload
-        return into if into is not None else cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
+        if into is not None:
+            return into
+        out = cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
+        out._qsplit, out._qprog = qsplit, qprog
+        return out
 
     def ptr_q(self, l, i, col=0):
         lay = self.levels[l]
