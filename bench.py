@@ -314,7 +314,7 @@ def main():
     if os.environ.get("BENCH_DUMP"):
         with open(os.environ["BENCH_DUMP"], "w") as fh:
             json.dump([{"kind": names[int(kd)], "flops": int(fl), "bytes": int(by), "ms": float(t),
-                        "count": int(st["count"]), "grid": int(st["grid"])}
+                        "count": int(st["count"]), "grid": int(st["grid"]), "lane": int(st["lane"])}
                        for (kd, fl, by), t, st in zip(work, step_ms, steps_arr)], fh)
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     traffic = traffic_note = None
