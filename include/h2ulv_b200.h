@@ -248,7 +248,7 @@ typedef struct h2g_qr_panel_desc {
   int32_t p, b;
 } h2g_qr_panel_desc;
 
-int h2g_qr_panel(const h2g_qr_panel_desc* d_descs, int count, void* stream);
+int h2g_qr_panel(const h2g_qr_panel_desc* d_descs, int count, int max_rows, void* stream);  /* max_rows >= max(n - p): panels that fit are factored in shared memory */
 
 /* h2g_basis_finish: given Q (n x n, explicit) and the factored Z (R in the
  * upper triangle), apply the sign convention of id_basis

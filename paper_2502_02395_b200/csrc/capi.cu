@@ -54,7 +54,7 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
       return H2G_OK;
     }
     case H2G_STEP_QR_PANEL:
-      return h2g_qr_panel((const h2g_qr_panel_desc*)s.descs, s.count, st);
+      return h2g_qr_panel((const h2g_qr_panel_desc*)s.descs, s.count, s.arg, st);
     case H2G_STEP_BASIS:
       return h2g_basis_finish((const h2g_basis_desc*)s.descs, s.count, st);
     case H2G_STEP_GEMV:

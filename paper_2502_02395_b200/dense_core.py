@@ -51,6 +51,81 @@ class SkeletonChoice:
     rank: int
 
 
+_GEQP3_LWORK = {}
+_TRTRS = {"fn": None, "tried": False}
+
+
+def _scipy_trtrs():
+    """scipy's own LAPACK dtrtrs (the routine scipy.linalg.solve_triangular calls) via
+    ctypes, which drops the GIL for the call; None if the library is not found."""
+    if not _TRTRS["tried"]:
+        _TRTRS["tried"] = True
+        import ctypes
+        import glob
+        import os
+
+        libs = glob.glob(os.path.join(os.path.dirname(os.path.dirname(scipy.__file__)), "scipy.libs",
+                                      "libscipy_openblas*.so"))
+        for path in libs:
+            try:
+                fn = ctypes.CDLL(path).scipy_dtrtrs_
+            except (OSError, AttributeError):
+                continue
+            fn.restype = None
+            _TRTRS["fn"] = fn
+            break
+    return _TRTRS["fn"]
+
+
+def solve_triangular(a, b, lower):
+    """scipy.linalg.solve_triangular(a, b, lower=lower) bit for bit (same dtrtrs call on
+    the same operands), with the GIL released; falls back to scipy when the library
+    symbol is unavailable."""
+    fn = _scipy_trtrs()
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if fn is None or a.ndim != 2 or b.ndim not in (1, 2) or a.shape[0] == 0 or b.size == 0:
+        return scipy.linalg.solve_triangular(a, b, lower=lower)
+    import ctypes
+
+    n = a.shape[0]
+    vec = b.ndim == 1
+    bf = np.array(b.reshape(n, -1), dtype=np.float64, order="F", copy=True)
+    nrhs = bf.shape[1]
+    if a.flags.f_contiguous:
+        af, uplo, trans = a, (b"L" if lower else b"U"), b"N"
+    else:   # the C buffer read as Fortran is a^T: solve a^T^T x = b (scipy's own choice)
+        af, uplo, trans = np.ascontiguousarray(a), (b"U" if lower else b"L"), b"T"
+    info = ctypes.c_int(0)
+    c = lambda v: ctypes.byref(ctypes.c_char(v))
+    i = lambda v: ctypes.byref(ctypes.c_int(v))
+    fn(c(uplo), c(trans), c(b"N"), i(n), i(nrhs), af.ctypes.data_as(ctypes.c_void_p), i(n),
+       bf.ctypes.data_as(ctypes.c_void_p), i(n), ctypes.byref(info))
+    if info.value > 0:
+        raise np.linalg.LinAlgError(f"singular matrix: resolution failed at diagonal {info.value - 1}")
+    if info.value < 0:
+        raise ValueError(f"dtrtrs: illegal argument {-info.value}")
+    return bf[:, 0] if vec else bf
+
+
+def _pivoted_qr_r(at):
+    """(R, piv) of scipy.linalg.qr(at, pivoting=True, mode="economic"), bit for bit
+    (the same dgeqp3 call with the same optimal workspace on the same Fortran-ordered
+    operand), through the raw LAPACK wrapper, which releases the GIL — so the
+    skeleton pass's thread pool runs the QRs in parallel (scipy.linalg.qr holds it)."""
+    at = np.asfortranarray(at, dtype=np.float64)
+    m, n = at.shape
+    lw = _GEQP3_LWORK.get((m, n))
+    if lw is None:
+        lw = int(scipy.linalg.lapack.dgeqp3(at, lwork=-1)[3][0])
+        _GEQP3_LWORK[(m, n)] = lw
+    qr, jpvt, _, _, info = scipy.linalg.lapack.dgeqp3(at, lwork=lw)
+    if info < 0:
+        raise ValueError(f"dgeqp3: illegal argument {-info}")
+    k = min(m, n)
+    return np.triu(qr[:k]), jpvt - 1
+
+
 def skeleton_selection(samples, rank=None, tol=None):
     """Column-pivoted QR of samples^T -> (skeleton, T, k).
 
@@ -65,7 +140,7 @@ def skeleton_selection(samples, rank=None, tol=None):
     n, m = a.shape
     if m < 1:
         raise ValueError("need at least one sample column")
-    _, r, piv = scipy.linalg.qr(a.T, pivoting=True, mode="economic")
+    r, piv = _pivoted_qr_r(a.T)
     diag = np.abs(np.diag(r))
     if diag.size == 0 or diag[0] == 0.0:
         k = 0
@@ -82,7 +157,7 @@ def skeleton_selection(samples, rank=None, tol=None):
     t = np.zeros((n, k))
     t[lead] = np.eye(k)
     if n > k:
-        t[piv[k:]] = scipy.linalg.solve_triangular(r[:k, :k], r[:k, k:], lower=False).T
+        t[piv[k:]] = solve_triangular(r[:k, :k], r[:k, k:], lower=False).T
     return SkeletonChoice(skeleton=lead[order].astype(np.int64), t=t[:, order], rank=k)
 
 

@@ -31,7 +31,7 @@ import torch
 from . import _native as nat
 from . import kernels
 from .basis_qr import LevelQR
-from .dense_core import BasisDecomposition, skeleton_selection
+from .dense_core import BasisDecomposition, skeleton_selection, solve_triangular
 from .errors import CoincidentPointsError, SingularTriangularError, StructureError
 from .h2_device import DeviceH2, LevelLayout
 from .program import Program
@@ -141,7 +141,7 @@ def gauss_seidel_solve(a, b, sweeps):
     strict_upper = a - lower
     x = np.zeros_like(b)
     for _ in range(sweeps):
-        x = scipy.linalg.solve_triangular(lower, b - strict_upper @ x, lower=True)
+        x = solve_triangular(lower, b - strict_upper @ x, lower=True)
     return x
 
 

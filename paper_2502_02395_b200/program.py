@@ -208,7 +208,8 @@ class Program:
         arr = np.zeros(len(descs), dtype=nat.QRP_DT)
         for name, col in zip(("Z", "V", "tau", "T", "n", "ldz", "p", "b"), zip(*descs)):
             arr[name] = col
-        self._add(nat.STEP["QR_PANEL"], len(descs), len(descs), self._blob(arr))
+        max_rows = int((arr["n"].astype(np.int64) - arr["p"]).max())
+        self._add(nat.STEP["QR_PANEL"], len(descs), len(descs), self._blob(arr), arg=max_rows)
         return len(descs)
 
     def basis(self, descs):
