@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 F64 = torch.float64
-_STAGING = {"buf": None}
+_STAGING = {"buf": None, "done": None}
 _POOL = {"pool": None}
 
 
@@ -103,22 +103,25 @@ class LevelLayout:
 
 
 def _q_interleave(levels, q, device):
-    """Device staging for the bases (q_red, q_skel contiguous per box) and the
-    block-copy program that forms q_full = [q_red | q_skel] row-major in q[l]."""
+    """Device staging for the bases (q_red, q_skel contiguous per box) and, per
+    level, the block-copy program that forms q_full = [q_red | q_skel] row-major
+    in q[l]."""
     from .program import Program
 
     qsplit = {l: torch.empty(max(lay.qsize, 1), dtype=F64, device=device) for l, lay in levels.items()}
-    prog = Program(device)
-    descs = []
+    progs = {}
     for l, lay in levels.items():
+        prog = Program(device)
+        descs = []
         sp, qp = qsplit[l].data_ptr(), q[l].data_ptr()
         for i in range(lay.nb):
             n, k = int(lay.n[i]), int(lay.k[i])
             r, o = n - k, int(lay.qoff[i])
             descs.append((sp + 8 * o, qp + 8 * o, n, r, r, n, 0))
             descs.append((sp + 8 * (o + n * r), qp + 8 * (o + r), n, k, k, n, 0))
-    prog.copy(descs)
-    return qsplit, prog.finalize()
+        prog.copy(descs)
+        progs[l] = prog.finalize()
+    return qsplit, progs
 
 
 class DeviceH2:
@@ -152,12 +155,36 @@ class DeviceH2:
         return _signature(self.depth, self.count, self.levels)
 
     @classmethod
-    def from_host(cls, h2, device=None, into=None):
+    def allocate_for_host(cls, h2, device=None):
+        """Device buffers (and the q interleave programs) for the structure of the
+        numpy H2Matrix `h2`, without uploading anything."""
+        device = torch.device(device or "cuda")
+        depth = h2.tree.depth
+        levels = cls.layouts_from_host(h2)
+        leaf = levels[depth]
+        aoff, asize = {}, 0
+        for (i, j) in leaf.near_pairs:
+            aoff[(i, j)] = asize
+            asize += int(leaf.n[i] * leaf.n[j])
+        q = {l: torch.empty(lay.qsize, dtype=F64, device=device) for l, lay in levels.items()}
+        s = {l: torch.empty(max(lay.ssize, 1), dtype=F64, device=device) for l, lay in levels.items()}
+        leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
+        out = cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
+        out._qsplit, out._qprog = _q_interleave(levels, q, device)
+        return out
+
+    @classmethod
+    def from_host(cls, h2, device=None, into=None, on_level=None, stream=None):
         """Upload the numpy arrays of `h2` (bases, leaf near blocks, couplings).
 
         The blocks are gathered in parallel (numpy releases the GIL) into one
-        reusable pinned staging buffer, then copied to HBM asynchronously.  With
-        `into` (a DeviceH2 of the same structure) its device buffers are reused.
+        reusable pinned staging buffer and copied to HBM asynchronously, level
+        by level from the leaves up (leaf near blocks with the leaf level).
+        With `into` (a DeviceH2 of the same structure) its device buffers are
+        reused.  With `stream` the copies run there and, once level l is
+        complete on that stream, `on_level(l, event)` lets the caller queue the
+        compute that needs it (the factorization of level l overlaps the upload
+        of the levels above).
         """
         device = torch.device(device or "cuda")
         depth = h2.tree.depth
@@ -165,36 +192,27 @@ class DeviceH2:
             a = np.ascontiguousarray(h2.near_blocks[(0, 0, 0)], dtype=np.float64)
             root_a = torch.from_numpy(a).to(device)
             return cls(device, 0, h2.count, {}, {}, {}, None, {}, root_a=root_a)
-        levels = into.levels if into is not None else cls.layouts_from_host(h2)
-        leaf = levels[depth]
-        if into is not None:
-            aoff = into.aoff
-            asize = int(into.leaf_a.numel())
-        else:
-            aoff, asize = {}, 0
-            for (i, j) in leaf.near_pairs:
-                aoff[(i, j)] = asize
-                asize += int(leaf.n[i] * leaf.n[j])
-        # staging layout: [q levels][s levels][leaf near blocks]
+        if into is None:
+            into = cls.allocate_for_host(h2, device)
+        levels, leaf, aoff = into.levels, into.levels[depth], into.aoff
+        asize = int(into.leaf_a.numel())
+        q, s, leaf_a, qsplit, qprog = into.q, into.s, into.leaf_a, into._qsplit, into._qprog
+        # staging layout by level, leaves first: [q_L][s_L][a][q_L-1][s_L-1] ... [q_1][s_1]
         regions, off = [], 0
-        for l, lay in levels.items():
+        for l in range(depth, 0, -1):
+            lay = levels[l]
             regions.append(("q", l, off, lay.qsize))
             off += lay.qsize
-        for l, lay in levels.items():
             regions.append(("s", l, off, max(lay.ssize, 1)))
             off += max(lay.ssize, 1)
-        regions.append(("a", depth, off, max(asize, 1)))
-        off += max(asize, 1)
+            if l == depth:
+                regions.append(("a", depth, off, max(asize, 1)))
+                off += max(asize, 1)
+        prev = _STAGING.get("done")
+        if prev is not None:
+            prev.synchronize()                 # the staging buffer is still being read by the last upload
         host_t, host = _staging(off)
-        if into is not None:
-            q, s, leaf_a = into.q, into.s, into.leaf_a
-            qsplit, qprog = into._qsplit, into._qprog
-        else:
-            q = {l: torch.empty(lay.qsize, dtype=F64, device=device) for l, lay in levels.items()}
-            s = {l: torch.empty(max(lay.ssize, 1), dtype=F64, device=device) for l, lay in levels.items()}
-            leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
-            qsplit, qprog = _q_interleave(levels, q, device)
-        # chunks of ~4M doubles inside one region: gathered by the thread pool, each
+        # chunks of ~0.5M doubles inside one region: gathered by the thread pool, each
         # DMA'd to HBM as soon as it is complete (gather and H2D overlap)
         chunks = []
         for kind, l, base, size in regions:
@@ -213,23 +231,33 @@ class DeviceH2:
             cur, c0, c1 = [], 0, 0
             for o, sz, task in items:
                 if cur and (o + sz) - c0 > _CHUNK:
-                    chunks.append((dst, base, c0, c1, cur))
+                    chunks.append((l, dst, base, c0, c1, cur))
                     cur, c0 = [], o
                 cur.append(task)
                 c1 = o + sz
             if cur:
-                chunks.append((dst, base, c0, c1, cur))
-        futs = [_pool().submit(_run_tasks, ch[4]) for ch in chunks]
-        for (dst, base, c0, c1, _), fu in zip(chunks, futs):
-            fu.result()
-            dst[c0:c1].copy_(host_t[base + c0:base + c1], non_blocking=True)
-        qprog.run()                                       # [q_red | q_skel] rows, on the device
-        torch.cuda.current_stream(device).synchronize()  # staging buffer is reused by the next upload
-        if into is not None:
-            return into
-        out = cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
-        out._qsplit, out._qprog = qsplit, qprog
-        return out
+                chunks.append((l, dst, base, c0, c1, cur))
+        last_of = {}
+        for idx, ch in enumerate(chunks):
+            last_of[ch[0]] = idx
+        st = stream if stream is not None else torch.cuda.current_stream(device)
+        futs = [_pool().submit(_run_tasks, ch[5]) for ch in chunks]
+        with torch.cuda.stream(st):
+            for idx, ((l, dst, base, c0, c1, _), fu) in enumerate(zip(chunks, futs)):
+                fu.result()
+                dst[c0:c1].copy_(host_t[base + c0:base + c1], non_blocking=True)
+                if last_of.get(l) == idx:
+                    qprog[l].run(st)             # [q_red | q_skel] rows of level l, on the device
+                    if on_level is not None:
+                        ev = torch.cuda.Event()
+                        ev.record(st)
+                        on_level(l, ev)
+        done = torch.cuda.Event()
+        done.record(st)
+        _STAGING["done"] = done
+        if stream is None:
+            done.synchronize()
+        return into
 
     def ptr_q(self, l, i, col=0):
         lay = self.levels[l]

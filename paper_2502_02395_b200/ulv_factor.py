@@ -133,7 +133,7 @@ class FactorPlan:
     (l >= log2 P) and everything above; the program is cut into segments
     with collective exchanges in between (distributed.py)."""
 
-    def __init__(self, dh2: DeviceH2, lists, part=None, comm=None):
+    def __init__(self, dh2: DeviceH2, lists, part=None, comm=None, level_cuts=False):
         self.dh2 = dh2
         self.depth = dh2.depth
         self.part = part
@@ -167,6 +167,10 @@ class FactorPlan:
             a_buf, a_off = dh2.leaf_a, dh2.aoff
             merge_ev = None
             for l in range(depth, 0, -1):
+                if level_cuts:
+                    # streamed upload: level l's segment starts once its operands landed
+                    prog = self._cut(prog, ("upload", l))
+                    merge_ev = None
                 lay = dh2.levels[l]
                 B = _LevelBuffers()
                 self.bufs[l] = B
@@ -473,6 +477,41 @@ class FactorPlan:
 
         run_segments(self, stream)
 
+    def launch_streamed(self):
+        """Incremental launcher for a plan built with level_cuts: returns
+        (on_level, finish).  on_level(l, event) — called by DeviceH2.from_host
+        when level l's operands are on their way — queues every segment up to
+        and including level l's after a wait on `event`; finish() queues the
+        rest (the root)."""
+        stream = torch.cuda.current_stream(self.device)
+        segs = self.segments
+        state = {"i": 0}
+
+        def on_level(level, event):
+            waited = False
+            while state["i"] < len(segs):
+                seg = segs[state["i"]]
+                if isinstance(seg, Program):
+                    seg.launch(stream)
+                elif seg[0] == "upload" and seg[1] == level and not waited:
+                    stream.wait_event(event)
+                    waited = True
+                elif seg[0] == "upload":
+                    return              # a later level: wait for its upload
+                else:
+                    raise ValueError(f"streamed launch does not support the exchange {seg}")
+                state["i"] += 1
+
+        def finish():
+            while state["i"] < len(segs):
+                seg = segs[state["i"]]
+                if not isinstance(seg, Program):
+                    raise RuntimeError(f"streamed launch: level {seg} was never uploaded")
+                seg.launch(stream)
+                state["i"] += 1
+
+        return on_level, finish
+
     def capture(self):
         """CUDA-graph every program segment (collectives stay outside)."""
         for seg in self.segments:
@@ -596,12 +635,51 @@ def _remember(key, dh2, plan):
     _PLAN_CACHE[key] = (dh2, plan, None)
 
 
+_UPLOAD_STREAM = {}
+
+
+def _upload_stream(device):
+    st = _UPLOAD_STREAM.get(device)
+    if st is None:
+        st = torch.cuda.Stream(device=device)
+        _UPLOAD_STREAM[device] = st
+    return st
+
+
+def _factorize_streamed(h2):
+    """Host-resident H2 (the reference's numpy data model): the upload runs level
+    by level from the leaves up on a copy stream, and each level's factorization
+    segment is queued as soon as its operands are in flight, so the GPU factors
+    level l while the host gathers and copies the levels above.  The symbolic
+    part (layout, descriptors, per-level CUDA graphs) is cached per structure."""
+    levels = DeviceH2.layouts_from_host(h2)
+    from .h2_device import _signature
+
+    key = ("stream", _signature(h2.tree.depth, h2.count, levels))
+    ent = _PLAN_CACHE.get(key)
+    if ent is not None and (ent[2] is None or ent[2]() is None):
+        dh2, plan = ent[0], ent[1]
+    else:
+        dh2 = DeviceH2.allocate_for_host(h2)
+        plan = FactorPlan(dh2, h2.lists, level_cuts=True)
+        plan.capture()
+        _remember(key, dh2, plan)
+    torch.cuda.current_stream(dh2.device).wait_stream(_upload_stream(dh2.device))
+    on_level, finish = plan.launch_streamed()
+    DeviceH2.from_host(h2, into=dh2, on_level=on_level, stream=_upload_stream(dh2.device))
+    finish()
+    return dh2, plan
+
+
 def factorize(h2, batched=True, retain=False):
     """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
     nat.lib()
-    dh2, plan = _cached_plan(h2)
-    plan.capture()
-    plan.run()
+    if getattr(h2, "_device", None) is None and h2.tree.depth > 0:
+        dh2, plan = _factorize_streamed(h2)
+    else:
+        dh2, plan = _cached_plan(h2)
+        plan.capture()
+        plan.run()
     plan.check_pivots()
     f = factors_from_plan(h2, plan)
     if retain:
