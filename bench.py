@@ -11,7 +11,8 @@ not part of the reference metric).
                 HBM, whole program replayed as one CUDA graph
   e2e           the same metric through the public API with HOST buffers:
                 factorize(h2 of numpy blocks) + solve(b) -> x on the host,
-                all host<->device copies inside the timed region
+                all host<->device copies inside the timed region (the upload
+                streams level by level and overlaps the factorization)
   roofline      dominant kernel = grouped FP64 DMMA GEMM; achieved flops over
                 its CUDA-event time inside an instrumented pass of K steps
   cpu_baseline  the CPU oracle port (oracle/h2ulv_oracle.py) on the host cores
@@ -377,9 +378,10 @@ def main():
     e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
            "d2h_bytes_per_step": int(xe.nbytes + plan.npd.numel() * 4), "seconds_per_step": e2e_s,
            "includes": "factorize(h2 of host numpy blocks): parallel pinned gather + H2D of bases / leaf near "
-                       "blocks / couplings, graph-replayed factorization, pivot-status D2H; solve(b): H2D b, "
-                       "forward/backward graphs, D2H x. The symbolic part (layout, descriptors, CUDA graph) "
-                       "is cached per structure, the numeric upload is redone every step"}
+                       "blocks / couplings level by level on a copy stream, each level's factorization graph "
+                       "queued behind its level's copies (upload and factorization overlap), pivot-status D2H; "
+                       "solve(b): H2D b, forward/backward graphs, D2H x. The symbolic part (layout, descriptors, "
+                       "CUDA graphs) is cached per structure, the numeric upload is redone every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -39,6 +39,8 @@ using Cfg64 = GemmCfg<64, 64, 2, 2, 1, 3>;      // 3 CTAs/SM (smem-bound), 3 sta
 using Cfg128 = GemmCfg<128, 128, 2, 4, 1, 3>;
 using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // 4 CTAs/SM, <= 128 registers, 2 stages
 using Cfg64k3 = GemmCfg<64, 64, 2, 2, 3, 3>;    // 3 CTAs/SM, 3 stages (m16n8k16 path)
+using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // experiment: 3 CTAs/SM (170 registers), 2 stages
+using Cfg64m2 = GemmCfg<64, 64, 2, 2, 2, 3>;    // experiment: 2 CTAs/SM (255 registers), 3 stages
 
 template <class C, bool TA, bool TB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
@@ -454,6 +456,8 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   if (tile_cfg == 3) return h2g::dispatch_k16<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 4) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 6) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 7) return h2g::dispatch<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 8) return h2g::dispatch<h2g::Cfg64m2>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg != 0) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d", tile_cfg);
   return h2g::dispatch<h2g::Cfg64>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
 }

@@ -98,6 +98,12 @@ def _stratified(pools, budget, rng):
     nonempty = [p for p in pools if len(p)]
     if budget == 0 or budget >= total:
         return np.concatenate(nonempty) if nonempty else np.zeros(0, dtype=np.int64)
+    # When the budget is below the pool count, the round-robin stops inside its first
+    # pass and only takes element 0 of the first `budget` pools; the permutations of
+    # the later pools are drawn after those from a generator used nowhere else, so
+    # skipping them leaves the result bit-identical (at N = 1M: 512 of 4095 per box).
+    if budget <= len(nonempty):
+        nonempty = nonempty[:budget]
     shuffled = [p[rng.permutation(len(p))] for p in nonempty]
     picked = []
     depth = 0

@@ -26,7 +26,7 @@ def gemm_tiles(m, n, flags=0, cfg=0):
     return (-(-m // t)) * (-(-n // t))
 
 
-def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False):
+def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False, ks=None):
     """Tile configuration of a grouped GEMM launch.
 
     Measured on B200 (tools/gemm_bench.py, profiles/r01_gemm_tile_configs*.jsonl):
@@ -34,7 +34,11 @@ def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False):
     the NN / TN transforms (30 TFLOP/s on 4096 x 256^3).  The 3-stage
     m16n8k16 variant at 3 CTAs/SM (cfg 6) is 7-13% faster on isolated K = 64
     NT updates but made the whole factorization slower in place (C2 8.52 ->
-    8.56 ms, M1 29.1 -> 29.3 ms), so every launch uses cfg 2."""
+    8.56 ms, M1 29.1 -> 29.3 ms).  The 2-stage m8n8k4 kernel at 3 CTAs/SM
+    (cfg 7, <= 170 registers) is 12-18% faster on the K <= 64 NT trailing
+    updates (profiles/r01_gemm_tile_configs_3.jsonl); those launches use it."""
+    if trans_b and ks is not None and len(ks) and int(np.max(ks)) <= 64:
+        return 7
     return 2
 
 
@@ -106,7 +110,8 @@ class Program:
         cols = list(zip(*rows))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
             arr[name] = col
-        cfg = choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b)) if tile_cfg is None else tile_cfg
+        cfg = (choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b), ks=arr["K"])
+               if tile_cfg is None else tile_cfg)
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
                          dtype=np.int64)
         starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])

@@ -113,3 +113,41 @@ def test_flop_model_reproduces_reference(name):
     for l, phases in want["levels"].items():
         for ph, ent in phases.items():
             assert got["levels"][int(l)][ph] == ent, (l, ph)
+
+
+def test_stratified_sampling_matches_reference_algorithm():
+    """h2_build._stratified skips the permutations of pools the round-robin never
+    reaches (budget < pool count); the draw must stay bit-identical to the
+    reference's _stratified (h2_build.py:77-96), restated here literally."""
+    from paper_2502_02395_b200.h2_build import _stratified
+
+    def reference(pools, budget, rng):
+        total = sum(len(p) for p in pools)
+        nonempty = [p for p in pools if len(p)]
+        if budget == 0 or budget >= total:
+            return np.concatenate(nonempty) if nonempty else np.zeros(0, dtype=np.int64)
+        shuffled = [p[rng.permutation(len(p))] for p in nonempty]
+        picked, depth = [], 0
+        while len(picked) < budget:
+            live = False
+            for p in shuffled:
+                if depth < len(p):
+                    picked.append(p[depth])
+                    live = True
+                    if len(picked) == budget:
+                        break
+            depth += 1
+            if not live:
+                break
+        return np.sort(np.asarray(picked, dtype=np.int64))
+
+    g = np.random.default_rng(0)
+    for trial in range(200):
+        sizes = g.integers(0, 40, size=int(g.integers(1, 600)))
+        starts = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+        pools = [np.arange(s0, s0 + sz, dtype=np.int64) for s0, sz in zip(starts, sizes)]
+        budget = int(g.integers(0, 700))
+        seed = np.random.SeedSequence((trial, 3, 7))
+        a = reference(pools, budget, np.random.default_rng(seed))
+        b = _stratified(pools, budget, np.random.default_rng(np.random.SeedSequence((trial, 3, 7))))
+        assert np.array_equal(a, b), trial
