@@ -131,3 +131,18 @@ def test_device_matvec_matches_host(pkg, family, shape):
         yh = h2_matvec_host(h2, x)
         assert y.shape == yh.shape
         assert np.linalg.norm(y - yh) / np.linalg.norm(yh) < 1e-13
+
+
+def test_c2_full_size_flops_and_residual(pkg):
+    """BASELINE.json configs[1] (C2, N = 65536, sampled 512/512, shift 1e5) at full
+    size: the reference's flop report exactly and the solve residual (reference
+    h2_matvec definition, cli.py:199-205) within 10x the reference's residual."""
+    m = meta("c2")
+    h2 = _build(pkg, "cube", 65536, 256, "laplace", 1e5, tol=1e-8, s_far=512, s_near=512)
+    f = pkg.factorize(h2)
+    assert f.flops["total_true"] == m["flops"]["total_true"]
+    b = np.random.default_rng(1).standard_normal(65536)
+    x = pkg.solve(f, b)
+    perm = h2.cloud.perm
+    res = np.linalg.norm(pkg.h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b)
+    assert res <= 10 * m["residual"], res
