@@ -717,13 +717,17 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
 constexpr int TS_BK = 32;
 constexpr int TS_S = TS_BK + 4;   // 36 = 4 mod 16 doubles: conflict-free fragments
 
-__global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows_desc* __restrict__ descs,
+// Shared memory: two stage regions of 2 x (64 x TS_S) doubles each.  The K loop
+// ping-pongs between them; the panel's 64x64 inverse is prefetched into the
+// region the loop no longer needs (that of tile KT) during the last tile, and
+// the accumulators go to the other region after the loop — 74 KB per CTA,
+// 3 CTAs per SM.
+constexpr int TS_REGION = 2 * PB * TS_S;   // doubles per stage region (>= PB * SD)
+static_assert(TS_REGION >= PB * SD, "a stage region must hold a 64 x SD block");
+
+__global__ void __launch_bounds__(RW_THREADS, 3) trsm_rows_kernel(const h2g_rows_desc* __restrict__ descs,
                                                                   const int32_t* __restrict__ tile_map) {
   extern __shared__ __align__(16) double tsm[];
-  double* Li = tsm;                              // PB x SD
-  double* As = tsm + PB * SD;                    // 2 stages x (PB x TS_S)
-  double* Bs = As + 2 * PB * TS_S;               // 2 stages x (PB x TS_S)
-  double* Cs = As;                               // PB x SD after the K loop (aliases the stages)
   const int pi = tile_map[blockIdx.x];
   const h2g_rows_desc P = descs[pi];
   const int chunk = blockIdx.x - P.tile_start;
@@ -741,14 +745,19 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
     if (nrows <= 0) continue;   // identity: these rows of L^-T start at a later block column
     const double* __restrict__ Lb = P.Lb + (size_t)p * P.ldlb;
     const double* __restrict__ Lq = P.Linv + (size_t)q * PB * PB;
+    const int KT = (K + TS_BK - 1) / TS_BK;
+    double* Li = tsm + (KT & 1) * TS_REGION;          // the region tile KT would use
+    double* Cs = tsm + ((KT + 1) & 1) * TS_REGION;    // the region of the last tile
+    auto load_li = [&]() {
 #pragma unroll 4
-    for (int t = tid; t < PB * PB; t += RW_THREADS) {
-      const int i = t / PB, x = t % PB;
-      cp_async8(Li + i * SD + x, Lq + (size_t)i * PB + x, true);
-    }
+      for (int t = tid; t < PB * PB; t += RW_THREADS) {
+        const int i = t / PB, x = t % PB;
+        cp_async8(Li + i * SD + x, Lq + (size_t)i * PB + x, true);
+      }
+    };
     auto load_stage = [&](int st, int k0) {
-      double* as = As + st * PB * TS_S;
-      double* bs = Bs + st * PB * TS_S;
+      double* as = tsm + st * TS_REGION;
+      double* bs = as + PB * TS_S;
 #pragma unroll
       for (int u = 0; u < (PB * TS_BK) / RW_THREADS; ++u) {
         const int idx = tid + u * RW_THREADS;
@@ -759,8 +768,8 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
         cp_async8(bs + m * TS_S + k, vb ? Lb + (size_t)m * P.ldlb + k0 + k : Lb, vb);
       }
     };
-    const int KT = (K + TS_BK - 1) / TS_BK;
     if (KT > 0) load_stage(0, 0);
+    else load_li();
     cp_async_commit();
 
     double acc[4][2][2];
@@ -778,11 +787,12 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
         }
     for (int kt = 0; kt < KT; ++kt) {
       if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
+      else load_li();                                  // overlaps the last tile's math
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
-      const double* as = As + (kt & 1) * PB * TS_S;
-      const double* bs = Bs + (kt & 1) * PB * TS_S;
+      const double* as = tsm + (kt & 1) * TS_REGION;
+      const double* bs = as + PB * TS_S;
 #pragma unroll
       for (int kk = 0; kk < TS_BK; kk += 4) {
         double af[4], bf[2];
@@ -838,11 +848,11 @@ __global__ void __launch_bounds__(RW_THREADS, 2) trsm_rows_kernel(const h2g_rows
         if (c + 1 < b) dst[c + 1] = out[i][j][1];
       }
     }
-    __syncthreads();   // the next panel reads these columns back (and reuses Li / Cs)
+    __syncthreads();   // the next panel reads these columns back (and reuses the regions)
   }
 }
 
-constexpr size_t TS_SMEM = (PB * SD + 4 * PB * TS_S) * sizeof(double);
+constexpr size_t TS_SMEM = (2 * TS_REGION) * sizeof(double);
 
 constexpr size_t DIAG_SMEM = (2 * PB * SD) * sizeof(double) + sizeof(LdltShared);
 constexpr size_t RW_SMEM = (3 * PB * SD) * sizeof(double);
