@@ -122,6 +122,15 @@ typedef struct h2g_chol_panel_desc {
 int h2g_chol_panel_tiles(int n, int p, int b);
 int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map, int total_tiles,
                    int32_t* d_npd, void* stream);
+/* The same step; with d_sync (2 * count + 2 zeroed int32, left zeroed) and
+ * count <= h2g_chol_panel_fused_max() (default 128, env H2G_PANEL_FUSED_MAX)
+ * it is ONE launch: each CTA takes a ticket, the first `count` factor the
+ * diagonal blocks and publish L_pp^-1 through a per-box flag, the rest are
+ * the row chunks, which apply the previous panel while the diagonal block is
+ * being factored and wait for the flag only before their TRSM. */
+int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map, int total_tiles,
+                        int32_t* d_npd, int32_t* d_sync, void* stream);
+int h2g_chol_panel_fused_max(void);
 
 /* ---- left-looking row solve --------------------------------------------------
  * X = B L^-T block column by block column, one CTA per 64-row chunk of every

@@ -65,7 +65,8 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
       return h2g_kernel_blocks((const h2g_kblock_desc*)s.descs, s.map, s.grid, (const double*)s.aux, s.arg,
                                s.d0, s.d1, (int64_t*)s.npd, st);
     case H2G_STEP_CHOL_PANEL:
-      return h2g_chol_panel((const h2g_chol_panel_desc*)s.descs, s.count, s.map, s.grid, s.npd, st);
+      return h2g_chol_panel_sync((const h2g_chol_panel_desc*)s.descs, s.count, s.map, s.grid, s.npd,
+                                 (int32_t*)s.aux, st);
     case H2G_STEP_TRSM_ROWS:
       return h2g_trsm_rows((const h2g_rows_desc*)s.descs, s.map, s.grid, st);
     case H2G_STEP_NOP:

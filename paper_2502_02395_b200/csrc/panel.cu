@@ -534,14 +534,11 @@ __device__ __forceinline__ void panel_update_64(double (&acc)[4][2][2], const do
 
 // NW = 8: latency variant (few boxes); NW = 4: throughput variant (many boxes, more CTAs per SM).
 template <int NW>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
-                                                                    int32_t* __restrict__ npd) {
+__device__ __forceinline__ void chol_diag_body(const h2g_chol_panel_desc& P, double* csm, int32_t* __restrict__ npd) {
   constexpr int NT = NW * 32, NV = 8 / NW;   // NV virtual 32x16 warp tiles per warp
-  extern __shared__ __align__(16) double csm[];
   double* S = csm;                  // PB x SD: X_{q-1}[p:p+b], then D
   double* Li = csm + PB * SD;       // PB x SD
   LdltShared& sh = *reinterpret_cast<LdltShared*>(csm + 2 * PB * SD);
-  const h2g_chol_panel_desc P = descs[blockIdx.x];
   const int p = P.p, b = P.b, ldh = P.ldh;
   double* __restrict__ H = P.H;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -608,14 +605,36 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(con
   }
 }
 
-__global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol_panel_desc* __restrict__ descs,
-                                                                  const int32_t* __restrict__ tile_map) {
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 3) chol_diag_kernel(const h2g_chol_panel_desc* __restrict__ descs,
+                                                                    int32_t* __restrict__ npd) {
   extern __shared__ __align__(16) double csm[];
+  const h2g_chol_panel_desc P = descs[blockIdx.x];
+  chol_diag_body<NW>(P, csm, npd);
+}
+
+__device__ __forceinline__ int chol_row_chunks(const h2g_chol_panel_desc& P) {
+  const int below = P.n - P.p - P.b;
+  return below > 0 ? (below + PB - 1) / PB : 0;
+}
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// FUSED: the diag CTA of the same launch publishes L_pp^-1 through *flag; the
+// chunk loads and applies the previous panel first, then waits for it.  The
+// last chunk of the box to pass the flag resets flag and counter for the next launch.
+template <bool FUSED>
+__device__ __forceinline__ void chol_rows_body(const h2g_chol_panel_desc& P, int chunk, double* csm,
+                                               int32_t* flag = nullptr, int32_t* cnt = nullptr) {
   double* S = csm;                  // 2PB x SD: X_{q-1}[p:p+b] (B), X_{q-1}[chunk] (A), then C
   double* Li = csm + 2 * PB * SD;   // PB x SD: L_pp^-1
-  const int pi = tile_map[blockIdx.x];
-  const h2g_chol_panel_desc P = descs[pi];
-  const int chunk = blockIdx.x - P.tile_start;
   const int p = P.p, b = P.b, n = P.n, ldh = P.ldh;
   double* __restrict__ H = P.H;
   const int row0 = p + b + PB * chunk;
@@ -623,12 +642,23 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
   PTRACE(0);
-  // L_pp^-1 and (p > 0) the previous panel's rows, all copies in flight at once
+  auto load_li = [&]() {
+    if (FUSED) {   // published by the diag CTA during this launch: bypass L1
 #pragma unroll 4
-  for (int t = tid; t < PB * PB; t += RW_THREADS) {
-    const int i = t / PB, x = t % PB;
-    cp_async8(Li + i * SD + x, P.Linv + (size_t)i * P.ldl + x, true);
-  }
+      for (int t = tid; t < PB * PB / 2; t += RW_THREADS) {
+        const int i = t / (PB / 2), x = 2 * (t % (PB / 2));
+        cp_async16_cg(Li + i * SD + x, P.Linv + (size_t)i * P.ldl + x);
+      }
+    } else {
+#pragma unroll 4
+      for (int t = tid; t < PB * PB; t += RW_THREADS) {
+        const int i = t / PB, x = t % PB;
+        cp_async8(Li + i * SD + x, P.Linv + (size_t)i * P.ldl + x, true);
+      }
+    }
+  };
+  // L_pp^-1 and (p > 0) the previous panel's rows, all copies in flight at once
+  if (!FUSED) load_li();
   if (p > 0) {
     const int k0 = p - PB;
 #pragma unroll 4
@@ -668,7 +698,23 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
       C[c * SD + col] = neg_int(acc[i][j][0]);
       C[c * SD + col + 1] = neg_int(acc[i][j][1]);
     }
-  __syncthreads();
+  if (FUSED) {
+    if (tid == 0) {
+      while (ld_acquire(flag) == 0) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    load_li();
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(cnt, 1) == chol_row_chunks(P) - 1) {
+      *cnt = 0;
+      *flag = 0;
+    }
+  } else {
+    __syncthreads();
+  }
   // X_c <- C L_pp^-T
   double out[4][2][2];
 #pragma unroll
@@ -701,6 +747,52 @@ __global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol
     }
   }
   PTRACE(5);
+}
+
+__global__ void __launch_bounds__(RW_THREADS, 2) chol_rows_kernel(const h2g_chol_panel_desc* __restrict__ descs,
+                                                                  const int32_t* __restrict__ tile_map) {
+  extern __shared__ __align__(16) double csm[];
+  const int pi = tile_map[blockIdx.x];
+  const h2g_chol_panel_desc P = descs[pi];
+  chol_rows_body<false>(P, blockIdx.x - P.tile_start, csm);
+}
+
+// One launch for the whole panel step (few boxes: the step is latency-bound).
+// Each CTA takes a ticket: tickets < count factor box `ticket`'s diagonal
+// block, the rest are row chunks.  A chunk only waits for diag CTAs that
+// already hold their ticket (they are running and wait for nothing), so
+// there is no dependence on the hardware's CTA dispatch order.
+// sync: [0] ticket counter, [1] finished CTAs, [2, 2+count) flags,
+// [2+count, 2+2count) per-box chunk counters; all zero between launches.
+__global__ void __launch_bounds__(RW_THREADS, 2) chol_panel_fused_kernel(const h2g_chol_panel_desc* __restrict__ descs,
+                                                                         const int32_t* __restrict__ tile_map,
+                                                                         int32_t* __restrict__ npd,
+                                                                         int32_t* __restrict__ sync, int count,
+                                                                         int total) {
+  extern __shared__ __align__(16) double csm[];
+  __shared__ int ticket;
+  if (threadIdx.x == 0) ticket = atomicAdd(&sync[0], 1);
+  __syncthreads();
+  const int t = ticket;
+  int32_t* flag = sync + 2;
+  int32_t* cnt = sync + 2 + count;
+  if (t < count) {
+    const h2g_chol_panel_desc P = descs[t];
+    chol_diag_body<8>(P, csm, npd);
+    __syncthreads();
+    if (threadIdx.x == 0 && chol_row_chunks(P) > 0) {
+      __threadfence();
+      st_release(flag + t, 1);
+    }
+  } else {
+    const int pi = tile_map[t - count];
+    const h2g_chol_panel_desc P = descs[pi];
+    chol_rows_body<true>(P, t - count - P.tile_start, csm, flag + pi, cnt + pi);
+  }
+  if (threadIdx.x == 0 && atomicAdd(&sync[1], 1) == total - 1) {
+    sync[0] = 0;
+    sync[1] = 0;
+  }
 }
 
 // ------------------------------------------------------------------ left-looking row solve
@@ -856,6 +948,7 @@ constexpr size_t TS_SMEM = (2 * TS_REGION) * sizeof(double);
 
 constexpr size_t DIAG_SMEM = (2 * PB * SD) * sizeof(double) + sizeof(LdltShared);
 constexpr size_t RW_SMEM = (3 * PB * SD) * sizeof(double);
+constexpr size_t FUSED_SMEM = RW_SMEM > DIAG_SMEM ? RW_SMEM : DIAG_SMEM;
 
 }  // namespace h2g
 
@@ -877,8 +970,22 @@ extern "C" int h2g_chol_panel_tiles(int n, int p, int b) {
   return below > 0 ? (below + h2g::PB - 1) / h2g::PB : 0;
 }
 
+extern "C" int h2g_chol_panel_fused_max(void) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("H2G_PANEL_FUSED_MAX");
+    v = e ? atoi(e) : 128;
+  }
+  return v;
+}
+
 extern "C" int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map,
                               int total_tiles, int32_t* d_npd, void* stream) {
+  return h2g_chol_panel_sync(d_descs, count, d_tile_map, total_tiles, d_npd, nullptr, stream);
+}
+
+extern "C" int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count, const int32_t* d_tile_map,
+                                   int total_tiles, int32_t* d_npd, int32_t* d_sync, void* stream) {
   if (count <= 0) return H2G_OK;
   if (!d_descs || !d_npd || (total_tiles > 0 && !d_tile_map))
     return h2g_set_error(H2G_EINVAL, "h2g_chol_panel: null argument");
@@ -887,9 +994,16 @@ extern "C" int h2g_chol_panel(const h2g_chol_panel_desc* d_descs, int count, con
     cudaFuncSetAttribute(h2g::chol_diag_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
     cudaFuncSetAttribute(h2g::chol_diag_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
     cudaFuncSetAttribute(h2g::chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::RW_SMEM);
+    cudaFuncSetAttribute(h2g::chol_panel_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)h2g::FUSED_SMEM);
     attr = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (d_sync && total_tiles > 0 && count <= h2g_chol_panel_fused_max()) {
+    h2g::chol_panel_fused_kernel<<<count + total_tiles, h2g::RW_THREADS, h2g::FUSED_SMEM, st>>>(
+        d_descs, d_tile_map, d_npd, d_sync, count, count + total_tiles);
+    return h2g_check_launch("chol_panel_fused");
+  }
   // many boxes: the 4-warp variant fits 3 CTAs per SM (throughput); few boxes: 8 warps (latency)
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);

@@ -68,6 +68,7 @@ class Program:
         self.steps = None
         self.graph = None
         self.kernel_launches = 0
+        self._keep = []       # device buffers the steps point into (CHOL_PANEL sync words)
         self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
         self.lane = 0         # lane of the steps added next (0: caller's stream, 1..4: side streams)
         self.n_events = 0
@@ -154,8 +155,11 @@ class Program:
         # useful flops: previous-panel update of block column p (K = 64) + chol + TRSM of the rows below
         upd = np.where(arr["p"] > 0, (b64 * (b64 + 1) + 2 * below * b64) * nat.PANEL_WIDTH, 0)
         fl = int((upd + b64 ** 3 // 3 + below * b64 * b64).sum())
+        # ticket / flag words of the one-launch variant (h2g_chol_panel_sync), zero between launches
+        sync = torch.zeros(2 * len(descs) + 2, dtype=torch.int32, device=self.device)
+        self._keep.append(sync)
         self._add(nat.STEP["CHOL_PANEL"], len(descs), int(tiles.sum()), self._blob(arr),
-                  self._blob(tmap) if tmap.size else -1, npd=npd_ptr, flops=fl)
+                  self._blob(tmap) if tmap.size else -1, npd=npd_ptr, aux=sync.data_ptr(), flops=fl)
         return int(tiles.sum())
 
     def trsm_rows(self, descs):
@@ -311,7 +315,9 @@ class Program:
             steps[q]["rec_ev"] = st["rec"]
         self.steps = steps
         # CHOL_PANEL issues a diag kernel plus, when rows lie below the panel, a row-chunk kernel
-        self.kernel_launches = int(sum((2 if st["kind"] == nat.STEP["CHOL_PANEL"] and st["grid"] > 0 else 1)
+        fused_max = nat.lib().h2g_chol_panel_fused_max()
+        self.kernel_launches = int(sum((2 if st["kind"] == nat.STEP["CHOL_PANEL"] and st["grid"] > 0
+                                        and st["count"] > fused_max else 1)
                                        for st in self._steps
                                        if st["kind"] not in (nat.STEP["MEMCPY"], nat.STEP["NOP"])))
         if any(st["lane"] for st in self._steps):

@@ -100,3 +100,41 @@ def test_trsm_rows(env, rows, cols, qb, qe, ident):
     hi = min(cols, 64 * qe)
     got = X.cpu().numpy()
     np.testing.assert_allclose(got[:, 64 * qb:hi], ref[:, 64 * qb:hi], rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("nbox", [100, 200])
+def test_chol_panel_many_boxes_rerun(env, nbox):
+    """nbox <= h2g_chol_panel_fused_max(): the one-launch ticket/flag variant; above: two kernels.
+    The program runs three times to check the sync words are left zeroed between launches."""
+    torch, nat, Program = env
+    n, p, b = 200, 64, 64
+    rng = np.random.default_rng(nbox)
+    hs, lfs = [], []
+    for _ in range(nbox):
+        g = rng.standard_normal((n, n))
+        a = g @ g.T + n * np.eye(n)
+        lf = np.linalg.cholesky(a)
+        h = a.copy()
+        h[:, :p] = np.tril(lf[:, :p])
+        h[p:, p:] = a[p:, p:]                  # the panel before p is the first one: nothing applied yet
+        hs.append(h)
+        lfs.append(lf)
+    h0 = torch.from_numpy(np.stack(hs)).cuda()
+    hd = h0.clone()
+    linv = torch.zeros(nbox, 64 * 64, dtype=torch.float64, device="cuda")
+    npd = torch.full((nbox,), 2 ** 31 - 1, dtype=torch.int32, device="cuda")
+    prog = Program(torch.device("cuda"))
+    prog.chol_panel([(hd[i].data_ptr(), linv[i].data_ptr(), n, 64, n, p, b, i) for i in range(nbox)],
+                    npd.data_ptr())
+    prog = prog.finalize()
+    for _ in range(3):
+        hd.copy_(h0)
+        prog.run()
+        torch.cuda.synchronize()
+        out = hd.cpu().numpy()
+        assert (npd.cpu().numpy() == 2 ** 31 - 1).all()
+        for i in range(0, nbox, 17):
+            lf = lfs[i]
+            tol = RTOL * np.abs(lf).max() * 10
+            np.testing.assert_allclose(np.tril(out[i, p:p + b, p:p + b]), lf[p:p + b, p:p + b], rtol=0, atol=tol)
+            np.testing.assert_allclose(out[i, p + b:, p:p + b], lf[p + b:, p:p + b], rtol=0, atol=tol)
