@@ -285,6 +285,7 @@ def main():
     # ---- roofline: per-step CUDA events over K instrumented (eager) factorizations
     per_kind = {}
     work = [w for pg in progs for w in pg.work]
+    exec_fl = [x for pg in progs for x in pg.exec_flops]
     steps_arr = np.concatenate([pg.steps for pg in progs])
     step_ms = np.zeros(len(steps_arr))
     for _ in range(args.steps):
@@ -314,9 +315,9 @@ def main():
     eager_ms = float(step_ms.sum())
     if os.environ.get("BENCH_DUMP"):
         with open(os.environ["BENCH_DUMP"], "w") as fh:
-            json.dump([{"kind": names[int(kd)], "flops": int(fl), "bytes": int(by), "ms": float(t),
-                        "count": int(st["count"]), "grid": int(st["grid"]), "lane": int(st["lane"])}
-                       for (kd, fl, by), t, st in zip(work, step_ms, steps_arr)], fh)
+            json.dump([{"kind": names[int(kd)], "flops": int(fl), "exec_flops": int(ex), "bytes": int(by),
+                        "ms": float(t), "count": int(st["count"]), "grid": int(st["grid"]), "lane": int(st["lane"])}
+                       for (kd, fl, by), ex, t, st in zip(work, exec_fl, step_ms, steps_arr)], fh)
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     traffic = traffic_note = None
     tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")

@@ -29,7 +29,10 @@ _POOL = {"pool": None}
 
 def _pool():
     if _POOL["pool"] is None:
-        _POOL["pool"] = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+        # measured on the B200 box (16 host cores; tools/upload_overlap.py, tools/ab_e2e.sh):
+        # 8 gather threads leave the DMA engine enough host memory bandwidth, 16 do not
+        n = int(os.environ.get("H2G_UPLOAD_THREADS", "8"))
+        _POOL["pool"] = ThreadPoolExecutor(max_workers=max(1, min(n, os.cpu_count() or 1)))
     return _POOL["pool"]
 
 
@@ -42,7 +45,8 @@ def _staging(n_doubles):
     return buf, buf.numpy()
 
 
-_CHUNK = 1 << 19   # doubles per upload chunk (4 MB): the first H2D starts after ~1 ms of gather
+# doubles per upload chunk (default 16 MB: C2 end to end 31 ms vs 39 ms with 4 MB chunks and 16 threads)
+_CHUNK = int(os.environ.get("H2G_UPLOAD_CHUNK", str(1 << 21)))
 
 
 def _run_tasks(tasks):

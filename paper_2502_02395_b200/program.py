@@ -70,6 +70,7 @@ class Program:
         self.kernel_launches = 0
         self._keep = []       # device buffers the steps point into (CHOL_PANEL sync words)
         self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
+        self.exec_flops = []  # per step: DMMA flops the tiles execute (GEMM: padded to whole tiles)
         self.lane = 0         # lane of the steps added next (0: caller's stream, 1..4: side streams)
         self.n_events = 0
         self.ctx = None
@@ -82,8 +83,9 @@ class Program:
         return len(self._blobs) - 1
 
     def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0, flops=0, nbytes=0,
-             wait=-1, rec=-1):
+             wait=-1, rec=-1, exec_flops=None):
         self.work.append((kind, int(flops), int(nbytes)))
+        self.exec_flops.append(int(flops if exec_flops is None else exec_flops))
         self._steps.append(dict(kind=kind, count=int(count), grid=int(grid), descs=descs, map=map_, npd=npd,
                                 arg=int(arg), aux=aux, d0=float(d0), d1=float(d1), lane=self.lane,
                                 wait=int(wait), rec=int(rec)))
@@ -124,7 +126,9 @@ class Program:
         m64, n64, k64 = arr["M"].astype(np.int64), arr["N"].astype(np.int64), arr["K"].astype(np.int64)
         lower = (arr["flags"] & nat.GEMM_LOWER) != 0
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
-        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg)
+        t = nat.GEMM_TILE[cfg]
+        ex = int((tiles * 2 * t * 64 * (-(-k64 // 16) * 16)).sum())
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex)
         return total
 
     def panel(self, descs, npd_ptr):
