@@ -53,7 +53,7 @@ STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "PANEL": 4, "COP
 GEMM_LOWER = 1
 GEMV_PLUS = 1
 GEMV_SPLIT = 2
-GEMM_TILE = (64, 128, 64, 64, 64, 64, 64, 64, 64)  # tile edge per tile_cfg (cfg 6 = cfg 4; 7, 8 experiments)
+GEMM_TILE = (64, 128, 64, 64, 64, 64, 64, 64, 64, 32)  # tile edge per tile_cfg (cfg 6 = cfg 4; 7, 8 experiments)
 COPY_TILE = 32
 PANEL_WIDTH = 64
 GEMV_CHUNK = 64    # output rows per CTA of h2g_gemv_grouped (csrc/solve.cu GV_CHUNK)

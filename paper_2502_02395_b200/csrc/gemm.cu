@@ -41,6 +41,7 @@ using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // 4 CTAs/SM, <= 128 registers, 
 using Cfg64k3 = GemmCfg<64, 64, 2, 2, 3, 3>;    // 3 CTAs/SM, 3 stages (m16n8k16 path)
 using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // experiment: 3 CTAs/SM (170 registers), 2 stages
 using Cfg64m2 = GemmCfg<64, 64, 2, 2, 2, 3>;    // experiment: 2 CTAs/SM (255 registers), 3 stages
+using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // small / ragged problems: 32x32 tiles, 6 CTAs/SM
 
 template <class C, bool TA, bool TB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
@@ -438,7 +439,7 @@ static int dispatch(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, c
 
 extern "C" int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg) {
   if (M <= 0 || N <= 0) return 0;
-  const int T = tile_cfg == 1 ? 128 : 64;   // cfg 0, 2, 3, 4: 64x64 tiles
+  const int T = tile_cfg == 1 ? 128 : tile_cfg == 9 ? 32 : 64;   // cfg 9: 32x32, the others 64x64
   if (flags & H2G_GEMM_LOWER) {
     int t = (M + T - 1) / T;
     return t * (t + 1) / 2;
@@ -458,6 +459,7 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   if (tile_cfg == 6) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 7) return h2g::dispatch<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 8) return h2g::dispatch<h2g::Cfg64m2>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  if (tile_cfg == 9) return h2g::dispatch<h2g::Cfg32>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg != 0) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d", tile_cfg);
   return h2g::dispatch<h2g::Cfg64>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
 }

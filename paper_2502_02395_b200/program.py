@@ -38,8 +38,24 @@ def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False, ks=None):
     (cfg 7, <= 170 registers) is 12-18% faster on the K <= 64 NT trailing
     updates (profiles/r01_gemm_tile_configs_3.jsonl); those launches use it."""
     if trans_b and ks is not None and len(ks) and int(np.max(ks)) <= 64:
+        # ragged small updates (REST of the partial Cholesky): 32x32 tiles when 64x64
+        # tiles would execute much more padding
+        if _TILE32_RATIO > 0:
+            ex64 = sum(gemm_tiles(m, n, f, 7) for m, n, f in zip(ms, ns, flags)) * 4
+            ex32 = sum(gemm_tiles(m, n, f, 9) for m, n, f in zip(ms, ns, flags))
+            if ex64 > _TILE32_RATIO * ex32:
+                return 9
         return 7
+    if _TILE32_ALL > 0:
+        ex64 = sum(gemm_tiles(m, n, f, 2) for m, n, f in zip(ms, ns, flags)) * 4
+        ex32 = sum(gemm_tiles(m, n, f, 9) for m, n, f in zip(ms, ns, flags))
+        if ex64 > _TILE32_ALL * ex32:
+            return 9
     return 2
+
+
+_TILE32_RATIO = float(__import__("os").environ.get("H2G_TILE32_RATIO", "1.5"))
+_TILE32_ALL = float(__import__("os").environ.get("H2G_TILE32_ALL", "0"))
 
 
 def copy_tiles(rows, cols):

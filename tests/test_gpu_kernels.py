@@ -138,3 +138,35 @@ def test_chol_panel_many_boxes_rerun(env, nbox):
             tol = RTOL * np.abs(lf).max() * 10
             np.testing.assert_allclose(np.tril(out[i, p:p + b, p:p + b]), lf[p:p + b, p:p + b], rtol=0, atol=tol)
             np.testing.assert_allclose(out[i, p + b:, p:p + b], lf[p + b:, p:p + b], rtol=0, atol=tol)
+
+
+@pytest.mark.parametrize("cfg", [2, 7, 9])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+def test_gemm_grouped_configs(env, cfg, ta, tb):
+    """Grouped C = alpha op(A) op(B) + beta C over ragged problems (h2g_gemm_grouped), every tile
+    configuration the planner picks; LOWER problems only write the lower triangle."""
+    torch, nat, Program = env
+    rng = np.random.default_rng(10 * cfg + 2 * ta + tb)
+    shapes = [(85, 85, 64, True), (43, 85, 64, False), (200, 37, 130, False), (96, 96, 21, True), (5, 70, 3, False)]
+    hold, probs, refs = [], [], []
+    for (m, n, k, lower) in shapes:
+        a = rng.standard_normal((k, m) if ta else (m, k))
+        b = rng.standard_normal((n, k) if tb else (k, n))
+        c = rng.standard_normal((m, n))
+        alpha, beta = -1.0, 1.0
+        ref = alpha * (a.T if ta else a) @ (b.T if tb else b) + beta * c
+        t = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (a, b, c)]
+        hold.append(t)
+        probs.append((t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), m, n, k, a.shape[1], b.shape[1], n,
+                      nat.GEMM_LOWER if lower else 0, alpha, beta))
+        refs.append(ref)
+    prog = Program(torch.device("cuda"))
+    prog.gemm(ta, tb, probs, tile_cfg=cfg)
+    prog.finalize().run()
+    torch.cuda.synchronize()
+    for t, ref, (m, n, k, lower) in zip(hold, refs, shapes):
+        got = t[2].cpu().numpy()
+        if lower:   # tiles above the diagonal are left alone; inside diagonal tiles only i >= j is specified
+            keep = np.tril(np.ones((m, n), dtype=bool))
+            got, ref = np.where(keep, got, 0.0), np.where(keep, ref, 0.0)
+        np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
