@@ -721,8 +721,9 @@ __device__ __forceinline__ void chol_rows_body(const h2g_chol_panel_desc& P, int
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+  const int kend = wn * 16 < b ? min(16 * (wn + 1), (b + 3) & ~3) : 0;   // Linv[n][k] = 0 for k > n, k >= b
 #pragma unroll 4
-  for (int kk = 0; kk < 16 * (wn + 1); kk += 4) {   // Linv[n][k] = 0 for k > n
+  for (int kk = 0; kk < kend; kk += 4) {
     double af[4], bf[2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) af[i] = C[(wm * 32 + i * 8 + g) * SD + kk + tq];
@@ -838,6 +839,7 @@ __global__ void __launch_bounds__(RW_THREADS, 3) trsm_rows_kernel(const h2g_rows
     const double* __restrict__ Lb = P.Lb + (size_t)p * P.ldlb;
     const double* __restrict__ Lq = P.Linv + (size_t)q * PB * PB;
     const int KT = (K + TS_BK - 1) / TS_BK;
+    const bool wact = wn * 16 < b;
     double* Li = tsm + (KT & 1) * TS_REGION;          // the region tile KT would use
     double* Cs = tsm + ((KT + 1) & 1) * TS_REGION;    // the region of the last tile
     auto load_li = [&]() {
@@ -886,7 +888,7 @@ __global__ void __launch_bounds__(RW_THREADS, 3) trsm_rows_kernel(const h2g_rows
       const double* as = tsm + (kt & 1) * TS_REGION;
       const double* bs = as + PB * TS_S;
 #pragma unroll
-      for (int kk = 0; kk < TS_BK; kk += 4) {
+      for (int kk = 0; kk < (wact ? TS_BK : 0); kk += 4) {   // columns >= b of a partial panel: no math
         double af[4], bf[2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) af[i] = as[(wm * 32 + i * 8 + g) * TS_S + kk + tq];
@@ -916,8 +918,9 @@ __global__ void __launch_bounds__(RW_THREADS, 3) trsm_rows_kernel(const h2g_rows
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+    const int kend = wact ? min(16 * (wn + 1), (b + 3) & ~3) : 0;   // Linv[n][k] = 0 for k > n and k >= b
 #pragma unroll 4
-    for (int kk = 0; kk < 16 * (wn + 1); kk += 4) {   // Linv[n][k] = 0 for k > n
+    for (int kk = 0; kk < kend; kk += 4) {
       double af[4], bf[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = Cs[(wm * 32 + i * 8 + g) * SD + kk + tq];
