@@ -186,7 +186,7 @@ def run_reference(args, c, key):
     res = orc.residual(h2, orc.solve(f, b), b)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
             "config": {"workload": workload_name(key, c), "flops_per_step": flops, "residual": res},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": th, "kind": "port",
                              "sample": f"full factorization of {key.upper()} per step (oracle/h2ulv_oracle.py, "
@@ -400,7 +400,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "strong" if world > 1 else "weak",
+                "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
                 "config": {"workload": workload_name(args.config, c),
                            "parallelism": (f"sharded{world}: boxes of levels >= log2 P split by contiguous leaf "
