@@ -163,7 +163,7 @@ int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int t
  *   mode 1: src[c*lds + r]            (transpose)
  *   mode 2: src[max(r,c)*lds + min(r,c)]  (symmetric from the lower half)
  *   mode 3: (r == c) ? 1 : 0              (identity fill; src unused)
- * 32x32 tiles; d_tile_map[t] = descriptor of tile t.
+ * 64x64 tiles; d_tile_map[t] = descriptor of tile t.
  * Replaces: merge_level / inject_couplings (ulv_factor.py:108-132, 289-303)
  * — the 2x2 assembly of child SS blocks (and far couplings) into the parent
  * near blocks.

@@ -54,7 +54,7 @@ GEMM_LOWER = 1
 GEMV_PLUS = 1
 GEMV_SPLIT = 2
 GEMM_TILE = (64, 128, 64, 64, 64, 64, 64, 64, 64, 32)  # tile edge per tile_cfg (cfg 6 = cfg 4; 7, 8 experiments)
-COPY_TILE = 32
+COPY_TILE = 64
 PANEL_WIDTH = 64
 GEMV_CHUNK = 64    # output rows per CTA of h2g_gemv_grouped (csrc/solve.cu GV_CHUNK)
 QR_PANEL_WIDTH = 32

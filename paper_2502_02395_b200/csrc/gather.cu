@@ -5,18 +5,22 @@
 // after the Schur update (only its lower half is maintained on the GPU ->
 // mode 2), stored off-diagonal SS of near pairs or far couplings (mode 0),
 // and their transposes when ci < cj (mode 1).  One launch moves a whole
-// level; 32x32 tiles are staged through shared memory so both the read and
+// level; 64x64 tiles are staged through shared memory so both the read and
 // the write are coalesced for the transposed quadrants.  HBM-bound.
 #include "common.cuh"
 
 namespace h2g {
 
-constexpr int CT = 32;
+// 64x64 tiles, 256 threads (32 x 8): every thread moves 16 elements and issues
+// all its loads before its stores (a CTA per 32x32 tile spent most of its
+// time on the descriptor chain: 3.4 TB/s on the merges).
+constexpr int CT = 64;
+constexpr int CR = CT / 8;   // rows per thread
+constexpr int CC = CT / 32;  // columns per thread
 
 __global__ void __launch_bounds__(256) block_copy_kernel(const h2g_copy_desc* __restrict__ descs,
                                                          const int32_t* __restrict__ tile_map) {
   __shared__ double tileA[CT][CT + 1];
-  __shared__ double tileB[CT][CT + 1];
   const h2g_copy_desc D = descs[tile_map[blockIdx.x]];
   const int t = blockIdx.x - D.tile_start;
   const int ntc = (D.cols + CT - 1) / CT;
@@ -24,47 +28,58 @@ __global__ void __launch_bounds__(256) block_copy_kernel(const h2g_copy_desc* __
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const double* __restrict__ src = D.src;
   double* __restrict__ dst = D.dst;
-  const int lds = D.lds, ldd = D.ldd;
+  const int lds = D.lds, ldd = D.ldd, rows = D.rows, cols = D.cols;
   int mode = D.mode;
   if (mode == 2) {
     if (r0 >= c0 + CT) mode = 0;          // tile strictly below the diagonal
     else if (c0 >= r0 + CT) mode = 1;     // strictly above: mirror
   }
+  double v[CR][CC];
   if (mode == 3) {  // identity fill (src unused)
-    for (int rr = ty; rr < CT; rr += 8) {
-      int r = r0 + rr, c = c0 + tx;
-      if (r < D.rows && c < D.cols) dst[(size_t)r * ldd + c] = (r == c) ? 1.0 : 0.0;
-    }
+#pragma unroll
+    for (int i = 0; i < CR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        const int r = r0 + ty + 8 * i, c = c0 + tx + 32 * j;
+        if (r < rows && c < cols) dst[(size_t)r * ldd + c] = (r == c) ? 1.0 : 0.0;
+      }
     return;
   }
-  if (mode == 0) {
-    for (int rr = ty; rr < CT; rr += 8) {
-      int r = r0 + rr, c = c0 + tx;
-      if (r < D.rows && c < D.cols) dst[(size_t)r * ldd + c] = src[(size_t)r * lds + c];
+  if (mode != 1) {  // direct orientation: src[r][c]
+#pragma unroll
+    for (int i = 0; i < CR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        const int r = r0 + ty + 8 * i, c = c0 + tx + 32 * j;
+        v[i][j] = (r < rows && c < cols && (mode == 0 || r >= c)) ? src[(size_t)r * lds + c] : 0.0;
+      }
+  }
+  if (mode != 0) {
+    // tileA[a][b] = src[c0 + a][r0 + b]   (rows of the transposed source)
+#pragma unroll
+    for (int i = 0; i < CR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        const int a = ty + 8 * i, bb = tx + 32 * j;
+        const int sr = c0 + a, sc = r0 + bb;
+        if (sr < cols && sc < rows && (mode == 1 || sr > sc)) tileA[a][bb] = src[(size_t)sr * lds + sc];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < CR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        const int rr = ty + 8 * i, cc = tx + 32 * j;
+        if (mode == 1 || r0 + rr < c0 + cc) v[i][j] = tileA[cc][rr];   // src[c][r]
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < CR; ++i)
+#pragma unroll
+    for (int j = 0; j < CC; ++j) {
+      const int r = r0 + ty + 8 * i, c = c0 + tx + 32 * j;
+      if (r < rows && c < cols) dst[(size_t)r * ldd + c] = v[i][j];
     }
-    return;
-  }
-  // tileA[a][b] = src[(c0+a)][r0+b]   (rows of the transposed source)
-  for (int a = ty; a < CT; a += 8) {
-    int sr = c0 + a, sc = r0 + tx;
-    if (sr < D.cols && sc < D.rows) tileA[a][tx] = src[(size_t)sr * lds + sc];
-  }
-  if (mode == 2) {  // diagonal tile: also the direct orientation
-    for (int a = ty; a < CT; a += 8) {
-      int sr = r0 + a, sc = c0 + tx;
-      if (sr < D.rows && sc < D.cols) tileB[a][tx] = src[(size_t)sr * lds + sc];
-    }
-  }
-  __syncthreads();
-  for (int rr = ty; rr < CT; rr += 8) {
-    int r = r0 + rr, c = c0 + tx;
-    if (r < D.rows && c < D.cols) {
-      double v;
-      if (mode == 1 || r < c) v = tileA[tx][rr];   // src[c][r]
-      else v = tileB[rr][tx];                      // src[r][c]
-      dst[(size_t)r * ldd + c] = v;
-    }
-  }
 }
 
 }  // namespace h2g

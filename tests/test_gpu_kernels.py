@@ -170,3 +170,39 @@ def test_gemm_grouped_configs(env, cfg, ta, tb):
             keep = np.tril(np.ones((m, n), dtype=bool))
             got, ref = np.where(keep, got, 0.0), np.where(keep, ref, 0.0)
         np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (45, 70), (64, 64), (130, 97), (200, 200)])
+def test_block_copy_modes(env, rows, cols):
+    """h2g_block_copy: copy / transpose / symmetric-from-lower / identity into a strided
+    destination, bit-exact (the merge of child Schur blocks, ulv_factor.py:115-132)."""
+    torch, nat, Program = env
+    rng = np.random.default_rng(rows * 1000 + cols)
+    src = rng.standard_normal((max(rows, cols) + 3, max(rows, cols) + 5))
+    lds = src.shape[1]
+    s = torch.from_numpy(src).cuda()
+    outs, refs = [], []
+    prog = Program(torch.device("cuda"))
+    descs = []
+    for mode in (0, 1, 2, 3):
+        r, c = (rows, rows) if mode == 2 else (rows, cols)
+        ldd = c + 7
+        d = torch.full((r, ldd), 7.0, dtype=torch.float64, device="cuda")
+        ref = np.full((r, ldd), 7.0)
+        if mode == 0:
+            ref[:, :c] = src[:r, :c]
+        elif mode == 1:
+            ref[:, :c] = src[:c, :r].T
+        elif mode == 2:
+            low = np.tril(src[:r, :r])
+            ref[:, :c] = low + np.tril(low, -1).T
+        else:
+            ref[:, :c] = np.eye(r, c)
+        descs.append((s.data_ptr(), d.data_ptr(), r, c, lds, ldd, mode))
+        outs.append(d)
+        refs.append(ref)
+    prog.copy(descs)
+    prog.finalize().run()
+    torch.cuda.synchronize()
+    for d, ref in zip(outs, refs):
+        np.testing.assert_array_equal(d.cpu().numpy(), ref)
