@@ -22,7 +22,7 @@ __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) 
 }
 
 // y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t
-__global__ void __launch_bounds__(GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
+__global__ void __launch_bounds__(GV_THREADS, 4) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
                                                                   const h2g_gemv_term* __restrict__ terms, int w) {
   __shared__ double acc[GV_CHUNK * GV_W];
   __shared__ double red[GV_THREADS / 32][GV_CHUNK];
