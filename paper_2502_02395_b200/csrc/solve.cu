@@ -117,7 +117,7 @@ constexpr int TB = 64;
 constexpr int TR_THREADS = 512;
 constexpr int TR_WARPS = TR_THREADS / 32;
 constexpr int TR_RPW = TB / TR_WARPS;   // rows per warp in the forward GEMV (4)
-__global__ void __launch_bounds__(TR_THREADS) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
+__global__ void __launch_bounds__(TR_THREADS, 4) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
                                                                   int w) {
   __shared__ double t[TB];
   __shared__ double red[TR_WARPS][TB];
