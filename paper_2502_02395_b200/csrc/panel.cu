@@ -248,10 +248,12 @@ constexpr int DB = 16;
 __device__ __forceinline__ double fast_rcp(double d) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
+  // r(1 + e)(1 + e^2) with e = 1 - d r: the second Newton step's residual is
+  // e^2, formed beside the first step -> three dependent FP64 ops after the seed
+  const double e = fma(-d, r, 1.0);
+  const double e2 = e * e;
   r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
+  return fma(r, e2, r);
 }
 
 // Factor the 16x16 block at blk (lower part read, stride SD) with one warp:
