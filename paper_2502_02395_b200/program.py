@@ -9,6 +9,7 @@ planner/executor (dense_core.plan_batches / run_plan, dense_core.py:229-284).
 """
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -56,8 +57,8 @@ def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False, ks=None):
     return 2
 
 
-_TILE32_RATIO = float(__import__("os").environ.get("H2G_TILE32_RATIO", "1.5"))
-_TILE32_ALL = float(__import__("os").environ.get("H2G_TILE32_ALL", "1.5"))
+_TILE32_RATIO = float(os.environ.get("H2G_TILE32_RATIO", "1.5"))
+_TILE32_ALL = float(os.environ.get("H2G_TILE32_ALL", "1.5"))
 
 
 def copy_tiles(rows, cols):
@@ -69,8 +70,6 @@ def copy_tiles(rows, cols):
 def _ablated_lanes():
     """H2G_ABLATE_LANES="3,4" turns every step of those lanes into a NOP (events kept).
     Measurement aid for critical-path analysis only: the results are wrong."""
-    import os
-
     v = os.environ.get("H2G_ABLATE_LANES", "")
     return {int(x) for x in v.split(",") if x.strip()}
 
