@@ -158,13 +158,39 @@ def versions():
             "reference": "h2ulv " + h2ulv.__version__ + " (/root/reference/pkg)"}
 
 
+def skeleton_sha_per_level(h2):
+    """sha256 of each level's concatenated box-local skeletons (to localise a mismatch)."""
+    out = {}
+    for l in range(h2.tree.depth, 0, -1):
+        sk = [h2.bases[(l, i)].skeleton for i in range(2 ** l)]
+        out[str(l)] = sha(np.concatenate(sk).astype(np.int64) if sk else np.zeros(0, np.int64),
+                          np.array([len(s) for s in sk], np.int64))
+    return out
+
+
 def make_structure_fixture(name, shape, n, leaf, family, shift, cfg_kw, store_arrays):
     k, cloud, tree, lists, cfg, h2, tbuild = build(shape, n, leaf, family, shift, cfg_kw)
     rng_arr, centers, radii = tree_arrays(tree)
     near, far = list_arrays(lists)
     skel_keys, ranks, skel_local, skel_global = skeleton_arrays(h2)
     t0 = time.perf_counter()
-    f = ulv_factor.factorize(h2)
+    try:
+        f = ulv_factor.factorize(h2)
+    except h2ulv.errors.NotPositiveDefiniteError as e:
+        # the reference's breakdown contract (dense_core.py:60-63): record where it failed
+        meta = {"name": name, "config": config_echo(shape, n, leaf, family, shift, cfg_kw),
+                "depth": tree.depth,
+                "sha": {"perm": sha(cloud.perm), "box_ranges": sha(rng_arr), "near": sha(near),
+                        "far": sha(far), "ranks": sha(ranks), "skeleton_local": sha(skel_local),
+                        "skeleton_global": sha(skel_global)},
+                "skeleton_sha_per_level": skeleton_sha_per_level(h2),
+                "npd": {"pivot": int(e.pivot), "level": int(e.level), "box": int(e.box)},
+                "factor_seconds": time.perf_counter() - t0, "construct_seconds": tbuild}
+        meta.update(versions())
+        with open(os.path.join(HERE, name + ".json"), "w") as fh:
+            json.dump(meta, fh, indent=1)
+        print(name, "NPD", meta["npd"], "build s", round(tbuild, 2))
+        return
     tf = time.perf_counter() - t0
     b = np.random.default_rng(1).standard_normal(n)
     t0 = time.perf_counter()
@@ -177,6 +203,7 @@ def make_structure_fixture(name, shape, n, leaf, family, shift, cfg_kw, store_ar
                     "box_ranges": sha(rng_arr), "near": sha(near), "far": sha(far),
                     "ranks": sha(ranks), "skeleton_local": sha(skel_local),
                     "skeleton_global": sha(skel_global)},
+            "skeleton_sha_per_level": skeleton_sha_per_level(h2),
             "counts": {"near": int(len(near)), "far": int(len(far)), "skeleton": int(len(skel_local))},
             "flops": flop_table(f.flops), "audit": f.audit, "residual": res,
             "factor_seconds": tf, "solve_seconds": ts, "construct_seconds": tbuild,
@@ -227,6 +254,20 @@ FIXTURES = {
     "c1": lambda: make_structure_fixture("c1", "cube", 4096, 256, "laplace", 1e3, {"tol": 1e-8}, True),
     "c2": lambda: make_structure_fixture("c2", "cube", 65536, 256, "laplace", 1e5,
                                          {"tol": 1e-8, "s_far": 512, "s_near": 512}, False),
+    # BASELINE.json configs[2] (C3) and the metric configuration (M1, N = 2^20) + its tolerance sweep (C5, P = 1)
+    "c3": lambda: make_structure_fixture("c3", "sphere", 262144, 256, "yukawa", 1e5,
+                                         {"tol": 1e-8, "s_far": 512, "s_near": 512}, False),
+    "m1": lambda: make_structure_fixture("m1", "cube", 1048576, 256, "laplace", 2e6,
+                                         {"tol": 1e-8, "s_far": 512, "s_near": 512}, False),
+    "m1_tol6": lambda: make_structure_fixture("m1_tol6", "cube", 1048576, 256, "laplace", 2e6,
+                                              {"tol": 1e-6, "s_far": 512, "s_near": 512}, False),
+    "m1_tol10": lambda: make_structure_fixture("m1_tol10", "cube", 1048576, 256, "laplace", 2e6,
+                                               {"tol": 1e-10, "s_far": 512, "s_near": 512}, False),
+    # BASELINE.md §3 breakdown edges: the reference raises NotPositiveDefiniteError(pivot, level, box)
+    "c2_npd": lambda: make_structure_fixture("c2_npd", "cube", 65536, 256, "laplace", 1e3,
+                                             {"tol": 1e-8, "s_far": 512, "s_near": 512}, False),
+    "sphere65k_npd": lambda: make_structure_fixture("sphere65k_npd", "sphere", 65536, 256, "yukawa", 1e3,
+                                                    {"tol": 1e-8, "s_far": 512, "s_near": 512}, False),
 }
 
 if __name__ == "__main__":
