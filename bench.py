@@ -1,28 +1,36 @@
 """H²-ULV factorization benchmark (BASELINE.json metric) — one JSON line.
 
 A "step" is one complete H²-ULV factorization (all levels + root) of the
-configuration named by `--config` (default C2 = BASELINE.json configs[1]:
-Laplace-3D, N = 65536 uniform-cube points, leaf 256, tol 1e-8, shift 1e5,
-512/512 sampling).  The H² matrix is built once (untimed; construction is
-not part of the reference metric).
+configuration named by `--config` (default M1 = the metric's configuration:
+Laplace-3D, N = 1 048 576 uniform-cube points, leaf 256, tol 1e-8, shift
+2e6 (1e5 breaks down at the root), 512/512 sampling; it
+fits one B200).  The H² matrix is built once (untimed; construction is not
+part of the reference metric).
 
   value         factorization GFLOP/s = reference flop model total_true
                 (dense_core.flop_count) / device time, operands resident in
                 HBM, whole program replayed as one CUDA graph
   e2e           the same metric through the public API with HOST buffers:
-                factorize(h2 of numpy blocks) + solve(b) -> x on the host,
-                all host<->device copies inside the timed region (the upload
-                streams level by level and overlaps the factorization)
+                factorize(h2 of numpy blocks in pinned host memory) +
+                solve(b) -> x on the host, all host<->device copies inside the
+                timed region (the upload streams level by level and overlaps
+                the factorization)
   roofline      dominant kernel = grouped FP64 DMMA GEMM; achieved flops over
                 its CUDA-event time inside an instrumented pass of K steps
-  cpu_baseline  the CPU oracle port (oracle/h2ulv_oracle.py) on the host cores
+  solve         device-timed forward + backward sweeps, GB/s of the SURVEY
+                §8(d) algorithmic solve bytes
+  cpu_baseline  the CPU oracle port (oracle/h2ulv_oracle.py) on the host cores,
+                on a bounded sample: the diagonal sub-hierarchy under one box of
+                level L0 = max(0, depth - 9) (1/8 of the leaves at N = 1M)
 
 Multi-GPU (`torchrun ... bench.py --gpus N`): ONE factorization sharded over
 the ranks (distributed.py: boxes of the levels >= log2 N split by contiguous
 leaf ranges, NCCL all_gather of halo / boundary blocks, top levels replicated);
 strong scaling, time = max over ranks.
 `--impl reference` times the CPU oracle port (the reference is pure Python and
-does not travel to the GPU box) on rank 0 only.
+does not travel to the GPU box) on rank 0 only; each step factors one sampled
+sub-hierarchy (the sample rotates over the 2^L0 subtrees), the warm-up steps
+choose the BLAS thread count.
 """
 
 import argparse
@@ -39,6 +47,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "H²-ULV factorization time (s) and GFLOP/s at N=1M, 1/2/4/8 B200; solve residual"
+
+
+def _measured_hbm():
+    """MEASURED_PEAKS.json hbm_gbs (driver-written, this pool's B200s); 6547.2 = its round-2 value."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6547.2
+
+
+HBM_PEAK_GBS = _measured_hbm()
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak, profiles/r01_fp64_peak.txt (no FP64 entry in MEASURED_PEAKS.json)
 
 CONFIGS = {
@@ -136,16 +156,105 @@ def h2d_bytes(h2):
     return nb
 
 
-def cpu_oracle_time(h2_host, threads):
-    from threadpoolctl import threadpool_limits
+def sample_level(depth):
+    """Level whose boxes root the CPU samples: one sample = 2^-(L0) of the leaves."""
+    return max(0, depth - 9)
 
+
+def sub_hierarchy(hh, L0, g):
+    """The diagonal sub-hierarchy of a host H² under box g of level L0, as a
+    standalone H² of depth D - L0 (box i of level l -> box i - g 2^(l-L0) of
+    level l - L0): its leaf near blocks, bases and couplings, with the near /
+    far pairs whose both boxes lie in the subtree.  Its factorization is the
+    share of the full factorization's work that this subtree does (cross-
+    subtree near pairs and the levels above L0 excluded); the flop report of
+    the oracle counts exactly that work."""
+    from types import SimpleNamespace
+
+    D = hh.tree.depth
+    d = D - L0
+    near, far = [set() for _ in range(d + 1)], [set() for _ in range(d + 1)]
+    bases, nblk, cpl = {}, {}, {}
+    for s_ in range(d, -1, -1):
+        l = s_ + L0
+        lo, hi = g << s_, (g + 1) << s_
+        near[s_] = {(i - lo, j - lo) for (i, j) in hh.lists.near[l] if lo <= i < hi and lo <= j < hi}
+        far[s_] = {(i - lo, j - lo) for (i, j) in hh.lists.far[l] if lo <= i < hi and lo <= j < hi}
+        if s_ == 0:
+            near[0], far[0] = {(0, 0)}, set()
+            continue
+        for i in range(lo, hi):
+            bases[(s_, i - lo)] = hh.bases[(l, i)]
+        for (i, j) in far[s_]:
+            if i > j:
+                cpl[(s_, i, j)] = hh.couplings[(l, i + lo, j + lo)]
+    lo = g << d
+    for (i, j) in near[d]:
+        if i >= j:
+            nblk[(d, i, j)] = hh.near_blocks[(D, i + lo, j + lo)]
+    tree = SimpleNamespace(depth=d)
+    lists = SimpleNamespace(near=near, far=far)
+    return SimpleNamespace(tree=tree, lists=lists, bases=bases, near_blocks=nblk, couplings=cpl)
+
+
+class OracleSampler:
+    """Times the CPU oracle port's factorize on the sub-hierarchies of a host H²."""
+
+    def __init__(self, hh):
+        self.hh = hh
+        self.L0 = sample_level(hh.tree.depth)
+        self.count = 2 ** self.L0
+        self.subs = {}
+
+    def sub(self, g):
+        g %= self.count
+        if g not in self.subs:
+            self.subs[g] = sub_hierarchy(self.hh, self.L0, g) if self.L0 else self.hh
+        return self.subs[g]
+
+    def run(self, g, threads):
+        from threadpoolctl import threadpool_limits
+
+        from oracle import h2ulv_oracle as orc
+
+        sub = self.sub(g)
+        with threadpool_limits(limits=threads):
+            t0 = time.perf_counter()
+            f = orc.factorize(sub)
+            dt = time.perf_counter() - t0
+        return dt, int(f.flops["total_true"])
+
+    def describe(self, key):
+        if self.L0 == 0:
+            return f"one full {key.upper()} factorization per step"
+        return (f"{key.upper()}: per step the diagonal sub-hierarchy under one level-{self.L0} box "
+                f"(1/{self.count} of the leaves, levels {self.hh.tree.depth}..{self.L0 + 1} + its Cholesky at "
+                f"level {self.L0}; cross-subtree near pairs excluded), rotating over the {self.count} boxes")
+
+
+def thread_candidates():
+    cores = os.cpu_count() or 1
+    return sorted({1, min(8, cores), cores})
+
+
+def reference_h2(pkg, c):
+    """Host (numpy) H² for the CPU arm: the GPU construct (skeletons bit-exact vs the
+    reference, tests/test_gpu_fullsize.py) when a GPU is present, else the oracle's own."""
+    import torch
+
+    kernel, cloud, tree, lists, cfg = build_problem(pkg, c)
+    if torch.cuda.is_available():
+        h2 = pkg.construct(kernel, tree, lists, cfg, cloud, device=torch.device("cuda", 0))
+        hh = host_copy(pkg, h2)
+        del h2
+        from paper_2502_02395_b200.ulv_factor import clear_cache
+
+        clear_cache()
+        torch.cuda.empty_cache()
+        return hh, "paper_2502_02395_b200.construct (GPU), downloaded to numpy"
     from oracle import h2ulv_oracle as orc
 
-    with threadpool_limits(limits=threads):
-        t0 = time.perf_counter()
-        f = orc.factorize(h2_host)
-        dt = time.perf_counter() - t0
-    return dt, f.flops["total_true"]
+    return orc.construct(kernel, tree, lists, cfg, cloud), "oracle construct (CPU)"
 
 
 def run_reference(args, c, key):
@@ -154,54 +263,62 @@ def run_reference(args, c, key):
     if rank != 0:
         return
     import paper_2502_02395_b200 as pkg
-    from threadpoolctl import threadpool_limits
 
-    from oracle import h2ulv_oracle as orc
-
-    kernel, cloud, tree, lists, cfg = build_problem(pkg, c)
-    h2 = orc.construct(kernel, tree, lists, cfg, cloud)
-    cores = os.cpu_count()
-    threads = sorted({1, min(8, cores), cores})
-    best = None
-    for th in threads:  # nproc and 1 BLAS thread (and 8), keep the fastest
-        with threadpool_limits(limits=th):
-            t0 = time.perf_counter()
-            orc.factorize(h2)
-            dt = time.perf_counter() - t0
-        if best is None or dt < best[0]:
-            best = (dt, th)
-    th = best[1]
-    times = []
-    with threadpool_limits(limits=th):
-        for s in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            f = orc.factorize(h2)
-            dt = time.perf_counter() - t0
-            if s >= args.warmup:
-                times.append(dt)
-    flops = f.flops["total_true"]
-    ms = 1e3 * float(np.mean(times))
-    val = flops / (ms * 1e-3) / 1e9
-    b = np.random.default_rng(1).standard_normal(c["n"])
-    res = orc.residual(h2, orc.solve(f, b), b)
+    hh, src = reference_h2(pkg, c)
+    smp = OracleSampler(hh)
+    cands = thread_candidates()
+    # warm-up steps double as the BLAS thread sweep (1, 8 and nproc threads)
+    rates = {}
+    for w in range(args.warmup):
+        th = cands[w % len(cands)]
+        dt, fl = smp.run(w, th)
+        rates.setdefault(th, []).append(fl / dt)
+    for th in cands:
+        if th not in rates:
+            dt, fl = smp.run(0, th)
+            rates[th] = [fl / dt]
+    th = max(rates, key=lambda t: max(rates[t]))
+    tot_t = tot_f = 0.0
+    for st in range(args.steps):
+        dt, fl = smp.run(args.warmup + st, th)
+        tot_t += dt
+        tot_f += fl
+    val = tot_f / tot_t / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
-            "config": {"workload": workload_name(key, c), "flops_per_step": flops, "residual": res},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (uniform cube, seed 0)" if c["shape"] == "cube" else "synthetic (sphere, seed 0)",
+            "config": {"workload": workload_name(key, c), "flops_per_step": tot_f / args.steps,
+                       "sample": smp.describe(key), "h2_source": src},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": th, "kind": "port",
-                             "sample": f"full factorization of {key.upper()} per step (oracle/h2ulv_oracle.py, "
-                                       f"OpenBLAS threads={th}, host has {cores} cores)"},
+                             "sample": smp.describe(key) + f"; oracle/h2ulv_oracle.py, OpenBLAS threads={th} "
+                                       f"(best of {cands} over the warm-up steps), host has {os.cpu_count()} cores"},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def solve_bytes(plan):
+    """SURVEY §8(d) algorithmic bytes of one solve (w = 1; every basis / factor
+    block read once per sweep): 2*8*[sum n^2 + sum r(r+1)/2 + sum_{near i>j} r_i r_j
+    + sum_{near (a,b)} k_a r_b] + 2*8*d(d+1)/2."""
+    tot = 0
+    for l, B in plan.bufs.items():
+        lay = B.lay
+        n, k, r = lay.n.astype(np.int64), lay.k.astype(np.int64), lay.r.astype(np.int64)
+        tot += int((n * n).sum() + (r * (r + 1) // 2).sum() + (k * r).sum())
+        for (i, j) in lay.off_pairs:
+            tot += int(r[i] * r[j] + k[i] * r[j] + k[j] * r[i])
+    d = plan.root_dim
+    return 16 * tot + 16 * (d * (d + 1) // 2)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="m1", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -354,21 +471,45 @@ def main():
     ts0 = time.perf_counter()
     for _ in range(3):
         x = solve_fn(f, b)
-    solve_ms = (time.perf_counter() - ts0) / 3 * 1e3
+    solve_ms = (time.perf_counter() - ts0) / 3 * 1e3     # host wall, incl. b / x transfers
     perm = cloud.perm
     res = float(np.linalg.norm(h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b))
+    solve = None
+    if world == 1:
+        # device-timed forward + backward sweeps (graph replays), operands in HBM
+        from paper_2502_02395_b200.ulv_solve import _plan_for
 
-    # ---- e2e through the public API with host buffers
-    h2_host = host_copy(pkg, h2)
+        sp = _plan_for(f, 1, "parallel")
+        for _ in range(3):
+            sp.run_forward(stream)
+            sp.run_backward(stream)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            sp.run_forward(stream)
+            sp.run_backward(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        s_ms = e0.elapsed_time(e1) / args.steps
+        sb = solve_bytes(plan)
+        solve = {"ms": s_ms, "algorithmic_bytes": sb, "gbs": sb / (s_ms * 1e-3) / 1e9,
+                 "hbm_peak_gbs": HBM_PEAK_GBS, "frac": sb / (s_ms * 1e-3) / 1e9 / HBM_PEAK_GBS,
+                 "note": "SURVEY §8(d) bytes (w = 1): every basis / factor block read once per sweep; "
+                         "forward + backward CUDA graphs replayed back to back, CUDA events"}
+
+    # ---- e2e through the public API with host buffers (the H² blocks in pinned host memory)
+    from paper_2502_02395_b200.h2_build import to_pinned_host
+
+    h2_host = to_pinned_host(h2)
     hb = h2d_bytes(h2_host) + b.nbytes
     e2e_times = []
-    for s in range(1 + args.e2e_steps):
+    for s_ in range(1 + args.e2e_steps):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         fe = factor_fn(h2_host)
         xe = solve_fn(fe, b)
         torch.cuda.synchronize(dev)
-        if s:
+        if s_:
             e2e_times.append(time.perf_counter() - t0)
         del fe
     e2e_s = float(np.mean(e2e_times))
@@ -378,40 +519,43 @@ def main():
         e2e_s = float(t.item())
     e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
            "d2h_bytes_per_step": int(xe.nbytes + plan.npd.numel() * 4), "seconds_per_step": e2e_s,
-           "includes": "factorize(h2 of host numpy blocks): parallel pinned gather + H2D of bases / leaf near "
-                       "blocks / couplings level by level on a copy stream, each level's factorization graph "
-                       "queued behind its level's copies (upload and factorization overlap), pivot-status D2H; "
-                       "solve(b): H2D b, forward/backward graphs, D2H x. The symbolic part (layout, descriptors, "
-                       "CUDA graphs) is cached per structure, the numeric upload is redone every step"}
+           "includes": "factorize(h2): the reference's numpy H2Matrix data model, its blocks in one pinned host "
+                       "buffer (to_pinned_host); H2D of bases / leaf near blocks / couplings level by level on a "
+                       "copy stream, each level's factorization graph queued behind its level's copies (upload "
+                       "and factorization overlap), pivot-status D2H; solve(b): H2D b, forward/backward graphs, "
+                       "D2H x. The symbolic part (layout, descriptors, CUDA graphs) is cached per structure, the "
+                       "numeric upload is redone every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
+        smp = OracleSampler(host_copy(pkg, h2))
         best = None
-        for th in sorted({1, min(8, cores), cores}):   # same thread candidates as --impl reference
-            dt, fl = cpu_oracle_time(h2_host, th)
-            if best is None or dt < best[0]:
+        for th in thread_candidates():   # same candidates as --impl reference
+            dt, fl = smp.run(0, th)
+            if best is None or fl / dt > best[1] / best[0]:
                 best = (dt, fl, th)
         dt, fl, th = best
         cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": th, "kind": "port",
-               "sample": f"one full {args.config.upper()} factorization (oracle/h2ulv_oracle.py), fastest of "
-                         f"{sorted({1, min(8, cores), cores})} BLAS threads: {th} threads, {dt:.2f} s"}
+               "sample": smp.describe(args.config) + f" (box 0 here); oracle/h2ulv_oracle.py, fastest of "
+                         f"{thread_candidates()} BLAS threads: {th} threads, {dt:.2f} s for {fl:.3e} flops"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform cube, seed 0)",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (uniform cube, seed 0)" if c["shape"] == "cube" else "synthetic (sphere, seed 0)",
                 "config": {"workload": workload_name(args.config, c),
                            "parallelism": (f"sharded{world}: boxes of levels >= log2 P split by contiguous leaf "
                                            f"ranges, top levels + root replicated, {backend} exchanges")
                            if world > 1 else "single GPU",
                            "flops_per_step": flops, "padded_flops": plan.flops["total_padded"],
-                           "factor_seconds": ms * 1e-3, "solve_ms": solve_ms, "residual": res,
+                           "factor_seconds": ms * 1e-3, "solve_ms_host": solve_ms, "residual": res,
                            "construct_seconds": construct_s, "eager_ms_per_step": eager_ms,
-                           "l2": "inputs > L2 (leaf near blocks + bases ~0.4 GB per step)",
+                           "l2": f"inputs > L2 (leaf near blocks + bases {h2d_bytes(h2_host) / 1e9:.2f} GB per step "
+                                 f"vs 126 MB L2)",
                            "depth": tree.depth, "root_dim": plan.root_dim},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "roofline": roofline, "solve": solve, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": sum(pg.kernel_launches for pg in progs) * args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -377,6 +377,7 @@ def construct(kernel, tree, lists, cfg, cloud, device=None, workers=None):
     dh2 = DeviceH2(device, depth, cloud.count, levels, q, s, leaf_a, aoff)
     h2._device = dh2
     h2._build_keep = (lqs, keep)
+    h2._choice = choice
     _attach_host_views(h2, dh2, choice, lqs)
     return h2
 
@@ -424,6 +425,104 @@ def _attach_host_views(h2, dh2, choice, lqs):
         return _flat(dh2.s[l], lay.soff[(i, j)], int(lay.k[i]), int(lay.k[j]))
 
     h2.couplings = _LazyMap(cpl_keys, cpl)
+
+
+def to_pinned_host(h2):
+    """Host copy of a GPU-built H², in the reference's numpy data model, whose
+    blocks all live in ONE pinned host buffer laid out like the upload
+    staging of DeviceH2.from_host (per level, leaves first: bases as q_red
+    then q_skel per box, couplings, then the leaf near blocks).
+
+    `bases[(l, i)].q_red / q_skel`, `near_blocks[(depth, i, j)]` and
+    `couplings[(l, i, j)]` are numpy views into that buffer, so `factorize`
+    of this matrix DMAs each level straight from it (no host gather): the
+    "inputs in pinned host memory" starting point of an end-to-end run.
+    Only the leaf-level near blocks are included (the factorization never
+    reads the upper-level ones, ulv_factor.py:175-176)."""
+    dh2 = h2._device
+    depth = dh2.depth
+    if depth == 0:
+        raise ValueError("to_pinned_host: depth-0 trees have a single dense block")
+    lqs = h2._build_keep[0]
+    regions, total = dh2.staging_regions()
+    arena_t = torch.empty(max(total, 1), dtype=F64, pin_memory=True)
+    arena = arena_t.numpy()
+    dev = dh2.device
+    # q_full -> [q_red | q_skel] split per box on the device (the inverse of the upload interleave)
+    split = {}
+    prog = Program(dev)
+    for l, lay in dh2.levels.items():
+        sp = torch.empty(max(lay.qsize, 1), dtype=F64, device=dev)
+        split[l] = sp
+        descs = []
+        for i in range(lay.nb):
+            n, k = int(lay.n[i]), int(lay.k[i])
+            r, o = n - k, int(lay.qoff[i])
+            descs.append((dh2.q[l].data_ptr() + 8 * o, sp.data_ptr() + 8 * o, n, r, n, r, 0))
+            descs.append((dh2.q[l].data_ptr() + 8 * (o + r), sp.data_ptr() + 8 * (o + n * r), n, k, n, k, 0))
+        prog.copy(descs)
+    prog.finalize().run()
+    for kind, l, base, size in regions:
+        src = split[l] if kind == "q" else dh2.s[l] if kind == "s" else dh2.leaf_a
+        arena_t[base:base + size].copy_(src[:size])
+    torch.cuda.synchronize(dev)
+    out = H2Matrix(tree=h2.tree, lists=h2.lists, kernel=h2.kernel, cloud=h2.cloud, config=h2.config)
+    out.skeletons, out.eff_points, out.build_flops = h2.skeletons, h2.eff_points, dict(h2.build_flops)
+    base_of = {(kind, l): base for kind, l, base, _ in regions}
+    expected = []
+    bases, near, cpl = {}, {}, {}
+    for l, lay in dh2.levels.items():
+        b0 = base_of[("q", l)]
+        lq = lqs[l]
+        fr_all = lq.frame.cpu().numpy()
+        for i in range(lay.nb):
+            n, k = int(lay.n[i]), int(lay.k[i])
+            r, o = n - k, b0 + int(lay.qoff[i])
+            qr = arena[o:o + n * r].reshape(n, r)
+            qs = arena[o + n * r:o + n * n].reshape(n, k)
+            c = h2._choice[(l, i)]
+            fr = fr_all[lq.foff[i]:lq.foff[i] + k * k].reshape(k, k)
+            bd = BasisDecomposition(q_skel=qs, q_red=qr, rank=k, frame=fr,
+                                    skeleton=c.skeleton if c is not None else np.zeros(0, dtype=np.int64))
+            bases[(l, i)] = bd
+            expected.append(("bases", (l, i), (bd, qr, qs)))
+        s0 = base_of[("s", l)]
+        for (i, j), o in lay.soff.items():
+            blk = arena[s0 + o:s0 + o + int(lay.k[i] * lay.k[j])].reshape(int(lay.k[i]), int(lay.k[j]))
+            cpl[(l, i, j)] = blk
+            expected.append(("couplings", (l, i, j), blk))
+    a0, leaf = base_of[("a", depth)], dh2.levels[depth]
+    for (i, j), o in dh2.aoff.items():
+        blk = arena[a0 + o:a0 + o + int(leaf.n[i] * leaf.n[j])].reshape(int(leaf.n[i]), int(leaf.n[j]))
+        near[(depth, i, j)] = blk
+        expected.append(("near_blocks", (depth, i, j), blk))
+    out.bases, out.near_blocks, out.couplings = bases, near, cpl
+    out._arena = PinnedArena(arena_t, dh2.signature(), expected)
+    return out
+
+
+class PinnedArena:
+    """The pinned buffer behind a `to_pinned_host` matrix plus the objects it
+    handed out; `intact(h2)` is true while every block of `h2` is still one of
+    them (a replaced block sends factorize back to the gather path)."""
+
+    def __init__(self, tensor, signature, expected):
+        self.tensor = tensor
+        self.signature = signature
+        self.expected = expected
+
+    def intact(self, h2):
+        try:
+            for name, key, obj in self.expected:
+                cur = getattr(h2, name)[key]
+                if name == "bases":
+                    if cur is not obj[0] or cur.q_red is not obj[1] or cur.q_skel is not obj[2]:
+                        return False
+                elif cur is not obj:
+                    return False
+        except KeyError:
+            return False
+        return True
 
 
 # --------------------------------------------------------------------------- matvec

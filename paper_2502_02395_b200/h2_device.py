@@ -156,7 +156,10 @@ class DeviceH2:
 
     def signature(self):
         """Structure key: equal signatures -> identical layouts and programs."""
-        return _signature(self.depth, self.count, self.levels)
+        sig = self.__dict__.get("_sig")
+        if sig is None:
+            sig = self._sig = _signature(self.depth, self.count, self.levels)
+        return sig
 
     @classmethod
     def allocate_for_host(cls, h2, device=None):
@@ -199,23 +202,32 @@ class DeviceH2:
         if into is None:
             into = cls.allocate_for_host(h2, device)
         levels, leaf, aoff = into.levels, into.levels[depth], into.aoff
-        asize = int(into.leaf_a.numel())
         q, s, leaf_a, qsplit, qprog = into.q, into.s, into.leaf_a, into._qsplit, into._qprog
-        # staging layout by level, leaves first: [q_L][s_L][a][q_L-1][s_L-1] ... [q_1][s_1]
-        regions, off = [], 0
-        for l in range(depth, 0, -1):
-            lay = levels[l]
-            regions.append(("q", l, off, lay.qsize))
-            off += lay.qsize
-            regions.append(("s", l, off, max(lay.ssize, 1)))
-            off += max(lay.ssize, 1)
-            if l == depth:
-                regions.append(("a", depth, off, max(asize, 1)))
-                off += max(asize, 1)
+        regions, off = into.staging_regions()
+        st = stream if stream is not None else torch.cuda.current_stream(device)
+        arena = getattr(h2, "_arena", None)
+        if arena is not None and arena.signature == into.signature() and arena.intact(h2):
+            # the blocks already sit in one pinned buffer in staging layout (to_pinned_host):
+            # one DMA per region, no host gather
+            with torch.cuda.stream(st):
+                for kind, l, base, size in regions:
+                    dst = qsplit[l] if kind == "q" else s[l] if kind == "s" else leaf_a
+                    dst[:size].copy_(arena.tensor[base:base + size], non_blocking=True)
+                    if kind == "q":
+                        qprog[l].run(st)
+                    if (kind == "s" and l != depth) or kind == "a":   # level l complete
+                        if on_level is not None:
+                            ev = torch.cuda.Event()
+                            ev.record(st)
+                            on_level(l, ev)
+            if stream is None:
+                st.synchronize()
+            return into
         prev = _STAGING.get("done")
         if prev is not None:
             prev.synchronize()                 # the staging buffer is still being read by the last upload
         host_t, host = _staging(off)
+        asize = int(into.leaf_a.numel())
         # chunks of ~0.5M doubles inside one region: gathered by the thread pool, each
         # DMA'd to HBM as soon as it is complete (gather and H2D overlap)
         chunks = []
@@ -244,7 +256,6 @@ class DeviceH2:
         last_of = {}
         for idx, ch in enumerate(chunks):
             last_of[ch[0]] = idx
-        st = stream if stream is not None else torch.cuda.current_stream(device)
         futs = [_pool().submit(_run_tasks, ch[5]) for ch in chunks]
         with torch.cuda.stream(st):
             for idx, ((l, dst, base, c0, c1, _), fu) in enumerate(zip(chunks, futs)):
@@ -262,6 +273,22 @@ class DeviceH2:
         if stream is None:
             done.synchronize()
         return into
+
+    def staging_regions(self):
+        """[(kind, level, offset, size)] of the host staging layout, leaves first:
+        [q_L][s_L][a][q_L-1][s_L-1] ... [q_1][s_1] (q: q_red then q_skel per box)."""
+        regions, off = [], 0
+        asize = int(self.leaf_a.numel())
+        for l in range(self.depth, 0, -1):
+            lay = self.levels[l]
+            regions.append(("q", l, off, lay.qsize))
+            off += lay.qsize
+            regions.append(("s", l, off, max(lay.ssize, 1)))
+            off += max(lay.ssize, 1)
+            if l == self.depth:
+                regions.append(("a", self.depth, off, max(asize, 1)))
+                off += max(asize, 1)
+        return regions, off
 
     def ptr_q(self, l, i, col=0):
         lay = self.levels[l]

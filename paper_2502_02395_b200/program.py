@@ -144,7 +144,7 @@ class Program:
         lower = (arr["flags"] & nat.GEMM_LOWER) != 0
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
         t = nat.GEMM_TILE[cfg]
-        ex = int((tiles * 2 * t * 64 * (-(-k64 // 16) * 16)).sum())
+        ex = int((tiles * 2 * t * t * (-(-k64 // 16) * 16)).sum())   # whole t x t tiles, K padded to 16
         self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex)
         return total
 

@@ -652,10 +652,13 @@ def _factorize_streamed(h2):
     segment is queued as soon as its operands are in flight, so the GPU factors
     level l while the host gathers and copies the levels above.  The symbolic
     part (layout, descriptors, per-level CUDA graphs) is cached per structure."""
-    levels = DeviceH2.layouts_from_host(h2)
     from .h2_device import _signature
 
-    key = ("stream", _signature(h2.tree.depth, h2.count, levels))
+    arena = getattr(h2, "_arena", None)
+    if arena is not None:      # a to_pinned_host matrix carries its structure signature
+        key = ("stream", arena.signature)
+    else:
+        key = ("stream", _signature(h2.tree.depth, h2.count, DeviceH2.layouts_from_host(h2)))
     ent = _PLAN_CACHE.get(key)
     if ent is not None and (ent[2] is None or ent[2]() is None):
         dh2, plan = ent[0], ent[1]
@@ -684,6 +687,7 @@ def factorize(h2, batched=True, retain=False):
     f = factors_from_plan(h2, plan)
     if retain:
         f.retained = _retained_views(plan)
+        f.retained._owner = f
     for key, ent in list(_PLAN_CACHE.items()):
         if ent[1] is plan:
             _PLAN_CACHE[key] = (ent[0], ent[1], weakref.ref(f))
@@ -734,7 +738,12 @@ def _retained_views(plan):
 def factors_from_plan(h2, plan):
     f = ULVFactors(h2, plan)
     for l in range(plan.depth, 0, -1):
-        f.levels[l] = plan.level_views(l)
+        lvl = plan.level_views(l)
+        # the lazy views read the plan's HBM buffers: they keep the factors alive, so the
+        # plan cache (weakref to the factors) never hands those buffers to a new factorization
+        for m in (lvl.lr_diag, lvl.lr_off, lvl.ls, lvl.v):
+            m._owner = f
+        f.levels[l] = lvl
     for l, parents in plan.merge_pairs.items():
         f.merge_map[l] = {(pi, pj): [(2 * pi + a, 2 * pj + b) for a in (0, 1) for b in (0, 1)]
                           for (pi, pj) in parents}

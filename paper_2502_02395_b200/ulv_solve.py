@@ -36,6 +36,7 @@ class BlockVector:
     width: int = 1
     vector: bool = True
     _plan: object = None
+    _owner: object = None     # the ULVFactors it came from (keeps their HBM buffers reserved)
 
 
 def _near_sets(lay):
@@ -356,10 +357,10 @@ class SolvePlan:
         for l in range(self.fp.depth, 0, -1):
             V = self.v[l]
             lay = self.fp.bufs[l].lay
-            y = V["Y"].view(-1, self.w)
+            y = V["Y"].view(-1, self.w)[:int(lay.r.sum())].cpu().numpy()   # one D2H per level
             for i in range(lay.nb):
                 o = int(V["offR"][i])
-                bv.yr[(l, i)] = y[o:o + int(lay.r[i])].cpu().numpy()
+                bv.yr[(l, i)] = y[o:o + int(lay.r[i])].copy()
         bv.root = self.yroot.view(-1, self.w)[:self.fp.root_dim].cpu().numpy()
         return bv
 
@@ -401,7 +402,9 @@ def _forward(factors, b, mode):
     sp = _plan_for(factors, bm.shape[1], mode)
     sp.xin.view(-1, sp.w)[:factors.h2.count].copy_(torch.from_numpy(np.ascontiguousarray(bm)))
     sp.run_forward()
-    return sp.block_vector(vector)
+    bv = sp.block_vector(vector)
+    bv._owner = factors
+    return bv
 
 
 def backward_parallel(factors, y):
@@ -413,20 +416,26 @@ def backward_naive(factors, y):
 
 
 def _backward(factors, y, mode):
+    """The backward sweep is a pure function of `y` (ulv_solve.py:127-188): the
+    host BlockVector is packed into the device layout and uploaded every call,
+    so in-place edits of y.yr / y.root and an interleaved forward of another
+    right-hand side cannot leak into the result."""
     nat.lib()
     sp = _plan_for(factors, y.width, mode)
-    if y._plan is not sp:  # upload a host BlockVector
-        for l in range(factors.device.depth, 0, -1):
+    fp = factors.device
+    with torch.cuda.device(sp.device):
+        for l in range(fp.depth, 0, -1):
             V = sp.v[l]
-            lay = factors.device.bufs[l].lay
-            dst = V["Y"].view(-1, sp.w)
+            lay = fp.bufs[l].lay
+            host = np.empty((int(lay.r.sum()), sp.w), dtype=np.float64)
             for i in range(lay.nb):
                 o = int(V["offR"][i])
-                dst[o:o + int(lay.r[i])].copy_(torch.from_numpy(np.asarray(y.yr[(l, i)]).reshape(-1, sp.w)))
-        sp.yroot.view(-1, sp.w)[:factors.device.root_dim].copy_(
-            torch.from_numpy(np.asarray(y.root).reshape(-1, sp.w)))
-    sp.run_backward()
-    x = sp.output.view(-1, sp.w)[:factors.h2.count].cpu().numpy()
+                host[o:o + int(lay.r[i])] = np.asarray(y.yr[(l, i)], dtype=np.float64).reshape(-1, sp.w)
+            V["Y"].view(-1, sp.w)[:host.shape[0]].copy_(torch.from_numpy(host))
+        sp.yroot.view(-1, sp.w)[:fp.root_dim].copy_(
+            torch.from_numpy(np.asarray(y.root, dtype=np.float64).reshape(-1, sp.w)))
+        sp.run_backward()
+        x = sp.output.view(-1, sp.w)[:factors.h2.count].cpu().numpy()
     return x[:, 0] if y.vector else x
 
 
