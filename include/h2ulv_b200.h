@@ -295,6 +295,36 @@ int h2g_kernel_blocks(const h2g_kblock_desc* d_descs, const int32_t* d_tile_map,
                       const double* d_points, int family, double shift, double decay,
                       int64_t* d_coincident, void* stream);
 
+/* ---- single-block API support (dense_core.cholesky / tri_solve) -------------
+ * h2g_sym_check: one CTA per matrix; d_out[2q] = max_{i>j} |A_ij - A_ji|,
+ * d_out[2q+1] = max |A_ij| as IEEE bit patterns (non-negative doubles; NaN
+ * propagates into the first).  The caller raises the reference's
+ * ValueError when the first exceeds 1e-10 x the second
+ * (dense_core.py:56-59).
+ * h2g_tri_inv: inverses of the 64 x 64 diagonal blocks of lower-triangular
+ * L (n x n, ld ldl) in the Linv layout of the Cholesky panels (block q at
+ * Linv + 4096 q, ld 64, identity beyond n), so h2g_trsm_rows can solve
+ * against any triangular factor; the first zero diagonal entry j records
+ * atomicMin(&d_status[status_slot], j) (SingularTriangularError,
+ * dense_core.py:75-76).  One CTA per diagonal block: d_tile_map[t] =
+ * descriptor of block CTA t, tile_start = its first block CTA.
+ */
+typedef struct h2g_symcheck_desc {
+  const double* A;
+  int32_t n, lda;
+} h2g_symcheck_desc;
+
+typedef struct h2g_triinv_desc {
+  const double* L;
+  double* Linv;
+  int32_t n, ldl;
+  int32_t tile_start, status_slot;
+} h2g_triinv_desc;
+
+int h2g_sym_check(const h2g_symcheck_desc* d_descs, int count, unsigned long long* d_out, void* stream);
+int h2g_tri_inv(const h2g_triinv_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int32_t* d_status,
+                void* stream);
+
 /* ---- native executor ---------------------------------------------------------
  * A factorization is a static list of steps (one batched phase each); the
  * executor issues them back to back on `stream` without returning to
@@ -315,6 +345,8 @@ enum {
   H2G_STEP_NOP = 12,     /* no kernel: carries a lane's event wait / record  */
   H2G_STEP_CHOL_PANEL = 13, /* descs/map = chol panel descs/tile map; npd = status */
   H2G_STEP_TRSM_ROWS = 14,  /* descs/map = rows descs/tile map */
+  H2G_STEP_SYMCHECK = 15,   /* descs = symcheck descs; aux = device output (2 x count u64) */
+  H2G_STEP_TRIINV = 16,     /* descs/map = triinv descs/tile map; npd = status */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

@@ -11,10 +11,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libh2ulv_b200.so")
-SOURCES = ["capi.cu", "gemm.cu", "panel.cu", "gather.cu", "solve.cu", "qr.cu", "kblock.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "panel.cu", "gather.cu", "solve.cu", "qr.cu", "kblock.cu", "blockops.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+OBJ_DIR = os.path.join(HERE, "build")
 
 
 def _stale():
@@ -29,10 +30,24 @@ def _stale():
 def build(force=False, verbose=False, extra=()):
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = [os.path.join(OBJ_DIR, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+    cmds = [[NVCC, *FLAGS, *extra, "-c", "-o", o, os.path.join(CSRC, s)] for s, o in zip(SOURCES, objs)]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        for c in cmds:
+            print(" ".join(c), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        procs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    for c, p in zip(cmds, procs):
+        if p.stdout or p.stderr:
+            print(p.stdout + p.stderr, file=sys.stderr)
+        if p.returncode:
+            raise subprocess.CalledProcessError(p.returncode, c)
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -69,6 +69,10 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
                                  (int32_t*)s.aux, st);
     case H2G_STEP_TRSM_ROWS:
       return h2g_trsm_rows((const h2g_rows_desc*)s.descs, s.map, s.grid, st);
+    case H2G_STEP_SYMCHECK:
+      return h2g_sym_check((const h2g_symcheck_desc*)s.descs, s.count, (unsigned long long*)s.aux, st);
+    case H2G_STEP_TRIINV:
+      return h2g_tri_inv((const h2g_triinv_desc*)s.descs, s.map, s.grid, s.npd, st);
     case H2G_STEP_NOP:
       return H2G_OK;
     default:

@@ -227,3 +227,49 @@ class PhaseFlops:
         ent["count"] += len(ops)
         self.flops["total_true"] += true
         self.flops["total_padded"] += padded
+
+
+# --------------------------------------------------------------------------- single-block API (GPU)
+# The reference's dense primitives and batch planner (dense_core.py:51-93,
+# 184-284) with the same signatures, errors and results; each call / each
+# BatchGroup is one batched launch of the library's kernels (block_engine).
+
+from .block_engine import (BatchGroup, BatchPlan, BlockOp, plan_batches, run_op,  # noqa: E402
+                           run_plan, run_sequential)
+
+
+def cholesky(a, context=None):
+    """Lower Cholesky factor on the GPU (dense_core.py:51-66): asymmetry
+    beyond 1e-10 relative -> ValueError; a non-positive pivot ->
+    NotPositiveDefiniteError(info - 1, *context)."""
+    from .block_engine import cholesky_batch
+
+    return cholesky_batch([a], [context])[0]
+
+
+def tri_solve(l, b, side="left", transposed=False):
+    """op(L) X = B (side="left") or X op(L) = B (side="right") on the GPU
+    (dense_core.py:69-81); a zero diagonal -> SingularTriangularError."""
+    from .block_engine import tri_solve_batch
+
+    return tri_solve_batch([(l, b, side, transposed)])[0]
+
+
+def multiply(a, b, transpose_a=False, transpose_b=False, accumulate_into=None, scale=1.0):
+    """C (+)= scale * op(A) op(B): one grouped DMMA GEMM launch (dense_core.py:84-93)."""
+    from .block_engine import multiply_batch
+
+    return multiply_batch([(a, b, transpose_a, transpose_b, accumulate_into, scale)])[0]
+
+
+def pad_for_cholesky(a, padded_n):
+    """Embed a square block top-left in a padded_n square with unit diagonal
+    fill (dense_core.py:153-163): the padded factor extends the true one."""
+    n = a.shape[0]
+    if padded_n < n:
+        raise ValueError("padded size smaller than block")
+    out = np.zeros((padded_n, padded_n))
+    out[:n, :n] = a
+    idx = np.arange(n, padded_n)
+    out[idx, idx] = 1.0
+    return out

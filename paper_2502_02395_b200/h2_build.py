@@ -29,7 +29,7 @@ import scipy.linalg
 import torch
 
 from . import _native as nat
-from . import kernels
+from . import dense_core, kernels
 from .basis_qr import LevelQR
 from .dense_core import BasisDecomposition, skeleton_selection, solve_triangular
 from .errors import CoincidentPointsError, SingularTriangularError, StructureError
@@ -582,3 +582,16 @@ def h2_matvec_host(h2, x):
         bi, bj = tree.box(depth, i), tree.box(depth, j)
         y[bi.begin:bi.end] += h2.near_block(depth, i, j) @ xm[bj.begin:bj.end]
     return y[:, 0] if vec else y
+
+
+def build_basis_for_box(kernel, cloud, box_pts, far_pts, close_block, rank=None, tol=None, row_weight=None):
+    """Composite basis from [G(B_i, far) | close_block] via the ID
+    (h2_build.py:155-167): host skeleton choice (bit-exact dgeqp3), the
+    complementary basis by the GPU Householder QR (dense_core.id_basis)."""
+    far_block = kernels.gen_block(kernel, box_pts, far_pts, cloud)
+    samples = np.hstack([far_block, np.asarray(close_block, dtype=np.float64).reshape(len(box_pts), -1)])
+    if samples.shape[1] == 0:
+        n = len(box_pts)
+        return dense_core.BasisDecomposition(q_skel=np.zeros((n, 0)), q_red=np.eye(n),
+                                             skeleton=np.zeros(0, dtype=np.int64), rank=0, frame=np.zeros((0, 0)))
+    return dense_core.id_basis(samples, rank=rank, tol=tol, row_weight=row_weight)

@@ -284,6 +284,32 @@ class Program:
         self._add(nat.STEP["TRSV"], len(descs), w, self._blob(arr), arg=trans, nbytes=nbytes)
         return len(descs)
 
+    def symcheck(self, descs, out_ptr):
+        """descs: list of (A, n, lda); out: 2 x len(descs) u64 (max |A - A^T|, max |A|)."""
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.SYMCHECK_DT)
+        for name, col in zip(("A", "n", "lda"), zip(*descs)):
+            arr[name] = col
+        nbytes = 8 * int((arr["n"].astype(np.int64) ** 2).sum()) * 2
+        self._add(nat.STEP["SYMCHECK"], len(descs), len(descs), self._blob(arr), aux=out_ptr, nbytes=nbytes)
+        return len(descs)
+
+    def triinv(self, descs, status_ptr):
+        """descs: list of (L, Linv, n, ldl, status_slot): inverses of the 64 x 64 diagonal blocks."""
+        descs = [d for d in descs if d[2] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.TRIINV_DT)
+        for name, col in zip(("L", "Linv", "n", "ldl", "status_slot"), zip(*descs)):
+            arr[name] = col
+        tiles = -(-arr["n"].astype(np.int64) // nat.PANEL_WIDTH)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        self._add(nat.STEP["TRIINV"], len(descs), int(tiles.sum()), self._blob(arr), self._blob(tmap),
+                  npd=status_ptr)
+        return int(tiles.sum())
+
     def kblock(self, descs, points_ptr, family, shift, decay, flag_ptr):
         """descs: list of (rows_ptr, cols_ptr, out_ptr, m, n, ldo)."""
         descs = [d for d in descs if d[3] > 0 and d[4] > 0]

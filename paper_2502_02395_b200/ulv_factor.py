@@ -300,104 +300,7 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
-        """Right-looking partial Cholesky of every box's H (and the V ride-along
-        rows in R), panels of W = 64 columns, one fused kernel per panel on the
-        critical lane:
-
-          lane 0:  [wait REST(q-2)] -> PANEL(q) -> [wait REST(q-1)] -> PANEL(q+1) ...
-          lane 1:          [wait PANEL(q)] -> REST(q)
-          lane 4:          [wait last PANEL] -> ROWS_V (all block columns, one launch)
-
-        PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
-        panel q-1 to block column q, factors the diagonal block and TRSMs the
-        rows below; REST(q) applies panel q to the columns < r right of block
-        column q+1 (lower tiles of RR, all SR rows); the SS corner receives its
-        single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.
-        ROWS_V (h2g_trsm_rows, left-looking, one CTA per 64 rows walking all
-        block columns) forms R = Q_red L^-T = V from Q (Qp) off the critical
-        lane; with Qp == 0 (the root) the identity rides along panel by panel
-        and R becomes L^-T (the root's explicit inverse for the solve).  Returns
-        (linv, loff, event after the last R column or None)."""
-        nb = len(n)
-        mine = np.ones(nb, dtype=bool) if mine is None else mine
-        rmax = int(np.asarray(r)[mine].max()) if mine.any() else 0
-        W = nat.PANEL_WIDTH
-        nblk = -(-np.asarray(r, dtype=np.int64) // W)
-        loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
-        linv = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=self.device)
-        if rmax == 0:
-            return linv, loff, None
-        lp = linv.data_ptr()
-        rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
-        for q, p in enumerate(range(0, rmax, W)):
-            descs, rest, rows = [], [], []
-            for i in range(nb):
-                ri, ni = int(r[i]), int(n[i])
-                if ri <= p or not mine[i]:
-                    continue
-                b = min(W, ri - p)
-                h = Hp + 8 * int(qo[i])
-                li = lp + 8 * (int(loff[i]) + q) * W * W
-                descs.append((h, li, ni, W, ni, p, b, slot0 + i))
-                q0 = p + b                               # first column right of the panel
-                c0 = q0 + (min(W, ri - q0) if ri > q0 else 0)   # right of the next panel
-                if ri > c0:
-                    # columns c0 .. r only: the SS corner gets its single Schur update at the end
-                    x = h + 8 * (c0 * ni + p)            # panel rows c0.. : H[c0:, p:p+b]
-                    rest.append((x, x, h + 8 * (c0 * ni + c0), ri - c0, ri - c0, b, ni, ni, ni,
-                                 nat.GEMM_LOWER, -1.0, 1.0))
-                    if ni > ri:                          # SR rows
-                        rest.append((h + 8 * (ri * ni + p), x, h + 8 * (ri * ni + c0), ni - ri, ri - c0, b,
-                                     ni, ni, ni, 0, -1.0, 1.0))
-                if Rp and not Qp:                        # root: L^-T panel by panel (rows < p + b)
-                    rows.append((h, 0, Rp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, ni, ri, q, q + 1,
-                                 ni, ni))
-            done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
-            if done:
-                prog.wait(done[-1])              # block column q has all updates of panels <= q-2
-            prog.chol_panel(descs, self.npd.data_ptr())
-            ev_fp = prog.event()
-            prog.record(ev_fp)
-            ev_rest = None
-            if rest:
-                prog.lane = 1
-                prog.wait(ev_fp)
-                prog.gemm(0, 1, rest)
-                ev_rest = prog.event()
-                prog.record(ev_rest)
-            rest_ev.append(ev_rest)
-            if rows:
-                prog.lane = 4
-                prog.wait(ev_fp)
-                prog.trsm_rows(rows)
-            prog.lane = 0
-        if Rp and Qp:
-            # V = Q_red L^-T for every box in ONE launch once all panels are factored:
-            # each CTA walks the block columns of its 64 rows (left-looking)
-            prog.lane = 4
-            prog.wait(ev_fp)
-            prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
-                             lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]), int(n[i]))
-                            for i in range(nb) if mine[i] and r[i] > 0])
-            prog.lane = 0
-        ev_v = None
-        if Rp:
-            ev_v = prog.event()
-            prog.lane = 4
-            prog.record(ev_v)
-            prog.lane = 0
-        last = [e for e in rest_ev if e is not None]
-        if last:
-            prog.wait(last[-1])                  # lane 1 is in order: the last REST covers all
-        # the single Schur update SS_ii -= L(s) L(s)^T with K = r (ulv_factor.py:236-241)
-        schur = []
-        for i in range(nb):
-            ri, ni = int(r[i]), int(n[i])
-            if mine[i] and ri > 0 and ni > ri:
-                ls = Hp + 8 * int(qo[i] + ri * ni)  # H[r:, 0:r]
-                schur.append((ls, ls, ls + 8 * ri, ni - ri, ni - ri, ri, ni, ni, ni, nat.GEMM_LOWER, -1.0, 1.0))
-        prog.gemm(0, 1, schur)
-        return linv, loff, ev_v
+        return partial_cholesky_steps(prog, self.device, self.npd.data_ptr(), Hp, Rp, qo, n, r, slot0, mine, Qp)
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
         """Root: full Cholesky of the merged d x d block; the identity rides along so
@@ -561,6 +464,107 @@ class FactorPlan:
         keys = [(i, i) for i in range(nb)] + list(lay.off_pairs) + [(j, i) for (i, j) in lay.off_pairs]
         lvl.ls = _LazyBlocks(keys, ls_fetch)
         return lvl
+
+
+def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
+    """Right-looking partial Cholesky of every box's H (and the V ride-along
+    rows in R), panels of W = 64 columns, one fused kernel per panel on the
+    critical lane:
+
+      lane 0:  [wait REST(q-2)] -> PANEL(q) -> [wait REST(q-1)] -> PANEL(q+1) ...
+      lane 1:          [wait PANEL(q)] -> REST(q)
+      lane 4:          [wait last PANEL] -> ROWS_V (all block columns, one launch)
+
+    PANEL(q) (h2g_chol_panel: a diag kernel and a row-chunk kernel) applies
+    panel q-1 to block column q, factors the diagonal block and TRSMs the
+    rows below; REST(q) applies panel q to the columns < r right of block
+    column q+1 (lower tiles of RR, all SR rows); the SS corner receives its
+    single Schur update SS -= L(s) L(s)^T (K = r) after the last panel.
+    ROWS_V (h2g_trsm_rows, left-looking, one CTA per 64 rows walking all
+    block columns) forms R = Q_red L^-T = V from Q (Qp) off the critical
+    lane; with Qp == 0 (the root) the identity rides along panel by panel
+    and R becomes L^-T (the root's explicit inverse for the solve).  Returns
+    (linv, loff, event after the last R column or None)."""
+    nb = len(n)
+    mine = np.ones(nb, dtype=bool) if mine is None else mine
+    rmax = int(np.asarray(r)[mine].max()) if mine.any() else 0
+    W = nat.PANEL_WIDTH
+    nblk = -(-np.asarray(r, dtype=np.int64) // W)
+    loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
+    linv = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=device)
+    if rmax == 0:
+        return linv, loff, None
+    lp = linv.data_ptr()
+    rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
+    for q, p in enumerate(range(0, rmax, W)):
+        descs, rest, rows = [], [], []
+        for i in range(nb):
+            ri, ni = int(r[i]), int(n[i])
+            if ri <= p or not mine[i]:
+                continue
+            b = min(W, ri - p)
+            h = Hp + 8 * int(qo[i])
+            li = lp + 8 * (int(loff[i]) + q) * W * W
+            descs.append((h, li, ni, W, ni, p, b, slot0 + i))
+            q0 = p + b                               # first column right of the panel
+            c0 = q0 + (min(W, ri - q0) if ri > q0 else 0)   # right of the next panel
+            if ri > c0:
+                # columns c0 .. r only: the SS corner gets its single Schur update at the end
+                x = h + 8 * (c0 * ni + p)            # panel rows c0.. : H[c0:, p:p+b]
+                rest.append((x, x, h + 8 * (c0 * ni + c0), ri - c0, ri - c0, b, ni, ni, ni,
+                             nat.GEMM_LOWER, -1.0, 1.0))
+                if ni > ri:                          # SR rows
+                    rest.append((h + 8 * (ri * ni + p), x, h + 8 * (ri * ni + c0), ni - ri, ri - c0, b,
+                                 ni, ni, ni, 0, -1.0, 1.0))
+            if Rp and not Qp:                        # root: L^-T panel by panel (rows < p + b)
+                rows.append((h, 0, Rp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, ni, ri, q, q + 1,
+                             ni, ni))
+        done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
+        if done:
+            prog.wait(done[-1])              # block column q has all updates of panels <= q-2
+        prog.chol_panel(descs, npd_ptr)
+        ev_fp = prog.event()
+        prog.record(ev_fp)
+        ev_rest = None
+        if rest:
+            prog.lane = 1
+            prog.wait(ev_fp)
+            prog.gemm(0, 1, rest)
+            ev_rest = prog.event()
+            prog.record(ev_rest)
+        rest_ev.append(ev_rest)
+        if rows:
+            prog.lane = 4
+            prog.wait(ev_fp)
+            prog.trsm_rows(rows)
+        prog.lane = 0
+    if Rp and Qp:
+        # V = Q_red L^-T for every box in ONE launch once all panels are factored:
+        # each CTA walks the block columns of its 64 rows (left-looking)
+        prog.lane = 4
+        prog.wait(ev_fp)
+        prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
+                         lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]), int(n[i]))
+                        for i in range(nb) if mine[i] and r[i] > 0])
+        prog.lane = 0
+    ev_v = None
+    if Rp:
+        ev_v = prog.event()
+        prog.lane = 4
+        prog.record(ev_v)
+        prog.lane = 0
+    last = [e for e in rest_ev if e is not None]
+    if last:
+        prog.wait(last[-1])                  # lane 1 is in order: the last REST covers all
+    # the single Schur update SS_ii -= L(s) L(s)^T with K = r (ulv_factor.py:236-241)
+    schur = []
+    for i in range(nb):
+        ri, ni = int(r[i]), int(n[i])
+        if mine[i] and ri > 0 and ni > ri:
+            ls = Hp + 8 * int(qo[i] + ri * ni)  # H[r:, 0:r]
+            schur.append((ls, ls, ls + 8 * ri, ni - ri, ni - ri, ri, ni, ni, ni, nat.GEMM_LOWER, -1.0, 1.0))
+    prog.gemm(0, 1, schur)
+    return linv, loff, ev_v
 
 
 def flop_report(levels, root_dim):
@@ -756,3 +760,16 @@ def h2_device_of(h2):
     if dh2 is None:
         dh2 = DeviceH2.from_host(h2)
     return dh2
+
+
+# --------------------------------------------------------------------------- single-box API (ulv_factor.py:70-132)
+from .block_engine import factor_diag, merge_level, sparsify_diag, sparsify_off  # noqa: E402,F401
+
+
+def inject_couplings(h2, level, ss_sink):
+    """Assign the far-pair couplings S_ij (i > j) into their SS slots
+    (ulv_factor.py:108-112).  The factorization itself places them on the
+    device with the merge's block copy (FactorPlan._merge_steps)."""
+    for (i, j) in h2.lists.far[level]:
+        if i > j:
+            ss_sink((i, j), h2.coupling(level, i, j))
