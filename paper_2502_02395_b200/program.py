@@ -89,6 +89,9 @@ class Program:
         self.work = []        # per step: (label, flops, bytes) of useful work, for the roofline
         self.exec_flops = []  # per step: DMMA flops the tiles execute (GEMM: padded to whole tiles)
         self.lane = 0         # lane of the steps added next (0: caller's stream, 1..4: side streams)
+        self.role = None      # role tag of the steps added next (write audit: "transform", "factor", ...)
+        self.record_writes = False
+        self.writes = []      # (step, role, ptr, rows, cols, ld, lower): matrix extents the steps write
         self.n_events = 0
         self.ctx = None
 
@@ -98,6 +101,12 @@ class Program:
             return -1
         self._blobs.append(np.ascontiguousarray(arr).view(np.uint8).reshape(-1))
         return len(self._blobs) - 1
+
+    def _writes(self, extents):
+        """Record the extents (ptr, rows, cols, ld, lower) the step added next writes."""
+        if self.record_writes:
+            q = len(self._steps)
+            self.writes.extend((q, self.role, int(p), int(r), int(c), int(ld), bool(lo)) for p, r, c, ld, lo in extents)
 
     def _add(self, kind, count, grid, descs=-1, map_=-1, npd=0, arg=0, aux=0, d0=0.0, d1=0.0, flops=0, nbytes=0,
              wait=-1, rec=-1, exec_flops=None):
@@ -140,6 +149,7 @@ class Program:
         tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
         # K == 0 problems still need their beta*C epilogue; keep them (tiles > 0)
         kind = nat.STEP["GEMM_NN"] + 2 * int(bool(trans_a)) + int(bool(trans_b))
+        self._writes((p[2], p[3], p[4], p[8], p[9] & nat.GEMM_LOWER) for p in rows)
         m64, n64, k64 = arr["M"].astype(np.int64), arr["N"].astype(np.int64), arr["K"].astype(np.int64)
         lower = (arr["flags"] & nat.GEMM_LOWER) != 0
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
@@ -176,6 +186,8 @@ class Program:
         # useful flops: previous-panel update of block column p (K = 64) + chol + TRSM of the rows below
         upd = np.where(arr["p"] > 0, (b64 * (b64 + 1) + 2 * below * b64) * nat.PANEL_WIDTH, 0)
         fl = int((upd + b64 ** 3 // 3 + below * b64 * b64).sum())
+        # the panel's diagonal block (lower) and the rows below it, columns p .. p+b
+        self._writes((d[0] + 8 * (d[5] * d[2] + d[5]), d[4] - d[5], d[6], d[2], False) for d in descs)
         # ticket / flag words of the one-launch variant (h2g_chol_panel_sync), zero between launches
         sync = torch.zeros(2 * len(descs) + 2, dtype=torch.int32, device=self.device)
         self._keep.append(sync)
@@ -196,6 +208,8 @@ class Program:
         tiles = -(-arr["rows"].astype(np.int64) // nat.PANEL_WIDTH)
         arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        self._writes((d[2] + 8 * nat.PANEL_WIDTH * d[6], d[4], min(d[5], nat.PANEL_WIDTH * d[7]) - nat.PANEL_WIDTH * d[6],
+                      d[9], False) for d in descs)
         fl = 0
         W = nat.PANEL_WIDTH
         for d in descs:   # useful flops: rows x b x (2 p + b) per panel (update + triangular solve)
@@ -215,6 +229,7 @@ class Program:
         cols = list(zip(*rows))
         for name, col in zip(("src", "dst", "rows", "cols", "lds", "ldd", "mode"), cols):
             arr[name] = col
+        self._writes((d[1], d[2], d[3], d[5], False) for d in rows)
         tiles = np.array([copy_tiles(r, c) for r, c in zip(arr["rows"], arr["cols"])], dtype=np.int64)
         arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
@@ -225,6 +240,7 @@ class Program:
     def memcpy(self, dst_ptr, src_ptr, nbytes):
         """Device-to-device copy (split into <= 1 GiB steps: the step count is int32)."""
         nbytes = int(nbytes)
+        self._writes([(dst_ptr, 1, nbytes // 8, nbytes // 8, False)])
         off = 0
         while off < nbytes:
             sz = min(nbytes - off, 1 << 30)

@@ -142,7 +142,8 @@ class FactorPlan:
         self.device = dev
         depth = self.depth
         self.segments = []
-        prog = Program(dev)
+        self._programs = []
+        prog = self._new_program()
         # pivot status: one slot per box of every level plus the root
         self.slot_base = {}
         acc = 0
@@ -211,10 +212,12 @@ class FactorPlan:
                 prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], qp + 8 * (qo[j] + r[j]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   int(n[i]), int(k[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
                                  for (i, j) in own_off])
+                prog.role = "transform"
                 prog.gemm(1, 0, [(qp + 8 * (qo[i] + r[i]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   Tp + 8 * (B.toff[(i, j)] + r[i] * n[j] + r[j]),
                                   int(k[i]), int(k[j]), int(n[i]), int(n[i]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
                                  for (i, j) in own_off])
+                prog.role = None
                 ev_ss = prog.event()
                 prog.record(ev_ss)
                 # ---- diagonal phase (lane 0 = the critical chain)
@@ -231,7 +234,9 @@ class FactorPlan:
                 # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
                 prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
                          int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
+                prog.role = "transform"
                 prog.gemm(1, 0, prob)
+                prog.role = None
                 B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
                                                                     Qp=qp)
                 if self.distributed_level(l):
@@ -256,7 +261,9 @@ class FactorPlan:
                     prob.append((qp + 8 * qo[i], mo, Tp + 8 * B.toff[(i, j)], ni, rj, ni, ni, nj, nj, 0, 1.0, 0.0))
                     prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
                                  0, 1.0, 0.0))
+                prog.role = "transform"
                 prog.gemm(1, 0, prob)
+                prog.role = None
                 prog.lane = 0
                 if self.distributed_level(l) and not self.distributed_level(l - 1):
                     # boundary: the parent level is replicated -> every rank needs all SS blocks
@@ -275,11 +282,11 @@ class FactorPlan:
 
         self.flops = flop_report({l: (B.lay.n, B.lay.k, B.lay.off_pairs) for l, B in self.bufs.items()},
                                  self.root_dim)
-        self.audit = self._audit()
         if self.part is not None and self.part.p > 1 and depth >= 1:
             # cross-owner off-diagonal factor blocks also go to the column box's owner (solve)
             prog = self._cut(prog, ("solve_halo", -1))
         self.segments.append(prog.finalize())
+        self.audit = self._audit()
         self.program = self.segments[0] if len(self.segments) == 1 else None
 
     # ------------------------------------------------------------------ distribution hooks
@@ -293,10 +300,16 @@ class FactorPlan:
     def distributed_level(self, l):
         return self.part is not None and self.part.p > 1 and l >= self.part.L0
 
+    def _new_program(self):
+        prog = Program(self.device)
+        prog.record_writes = True       # the write audit is derived from the programs' extents
+        self._programs.append(prog)
+        return prog
+
     def _cut(self, prog, tag):
         self.segments.append(prog.finalize())
         self.segments.append(tag)
-        return Program(self.device)
+        return self._new_program()
 
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
@@ -358,18 +371,27 @@ class FactorPlan:
         return abuf, aoff
 
     def _audit(self):
-        """Write audit of the reference's slab store (ulv_factor.py:319-337),
-        derived from the program: off-diagonal SS blocks (T) and the RR/RS/SR
-        slabs are written once by their producing GEMM and never updated; the
-        diagonal SS receives its single Schur update (split into one trailing
-        GEMM per Cholesky panel on the GPU)."""
-        boxes = sum(2 ** l for l in range(1, self.depth + 1))
-        panels = []
+        """Write audit of the reference's slab store (ulv_factor.py:50-67, 319-337),
+        derived from the write extents of every step of the program(s): see
+        audit_writes.  The slabs are the sparsified diagonal blocks H_i and the
+        off-diagonal blocks T_ij of every level."""
+        regions = []
         for l, B in self.bufs.items():
-            panels.extend(int(-(-ri // nat.PANEL_WIDTH)) for ri in B.lay.r)
-        return {"offdiag_ss_post_init_writes": 0, "rr_rs_sr_post_init_writes": 0,
-                "diag_ss_update_counts": [1] if boxes else [], "diag_ss_blocks": boxes,
-                "diag_ss_panel_updates": sorted(set(panels))}
+            lay = B.lay
+            n, r = lay.n, lay.r
+            mine = self.mine(l)
+            for i in range(lay.nb):
+                if mine[i]:
+                    regions.append((B.H.data_ptr() + 8 * int(lay.qoff[i]), int(n[i]), int(n[i]), int(r[i]), int(r[i]),
+                                    ("diag", l, i, i)))
+            for (i, j), off in B.toff.items():
+                if mine[i]:
+                    regions.append((B.T.data_ptr() + 8 * int(off), int(n[i]), int(n[j]), int(r[i]), int(r[j]),
+                                    ("off", l, i, j)))
+        writes = [w for prog in self._programs for w in prog.writes]
+        for prog in self._programs:
+            prog.writes = []
+        return audit_writes(regions, writes)
 
     # ------------------------------------------------------------------ run / check
     def run(self, stream=None):
@@ -522,6 +544,7 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
         done = [e for e in rest_ev[:max(q - 1, 0)] if e is not None]
         if done:
             prog.wait(done[-1])              # block column q has all updates of panels <= q-2
+        prog.role = "factor"
         prog.chol_panel(descs, npd_ptr)
         ev_fp = prog.event()
         prog.record(ev_fp)
@@ -529,7 +552,7 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
         if rest:
             prog.lane = 1
             prog.wait(ev_fp)
-            prog.gemm(0, 1, rest)
+            prog.gemm(0, 1, rest)     # role "factor": the in-place trailing update of RR / SR
             ev_rest = prog.event()
             prog.record(ev_rest)
         rest_ev.append(ev_rest)
@@ -563,8 +586,109 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
         if mine[i] and ri > 0 and ni > ri:
             ls = Hp + 8 * int(qo[i] + ri * ni)  # H[r:, 0:r]
             schur.append((ls, ls, ls + 8 * ri, ni - ri, ni - ri, ri, ni, ni, ni, nat.GEMM_LOWER, -1.0, 1.0))
+    prog.role = "schur"
     prog.gemm(0, 1, schur)
+    prog.role = None
     return linv, loff, ev_v
+
+
+def audit_writes(regions, writes):
+    """The reference's write audit (ulv_factor.py:50-67, 319-337) from program extents.
+
+    regions: (ptr, rows, cols, r_split, c_split, key) of every slab block —
+      key ("diag", l, i, i) for H_i, ("off", l, i, j) for T_ij; its sub-blocks
+      are rr = [:r_split, :c_split], rs, sr, ss as in the reference.
+    writes: (step, role, ptr, rows, cols, ld, lower) of every step descriptor
+      (Program.writes); roles: "transform" — the U^T A V GEMM that stores the
+      sparsified block (the reference's _Slabs.init), "factor" — the in-place
+      partial Cholesky of the box's own RR / SR (panels + their trailing
+      updates: the reference keeps L(r) / L(s) outside its slab store, so these
+      overwrite factor OUTPUT, not a slab), "schur" — the SS_ii -= L(s) L(s)^T
+      update; anything else (or any write of a wrong role) is a post-init update.
+
+    Returns the reference's dict: offdiag_ss_post_init_writes,
+    rr_rs_sr_post_init_writes, diag_ss_update_counts (sorted distinct per-box
+    counts; a box with r = 0 or k = 0 receives the reference's vacuous update,
+    counted once), diag_ss_blocks, plus in_place_factor_writes,
+    uninitialized_slabs and initialized_twice (structure checks)."""
+    import bisect
+
+    regions = sorted(regions)
+    starts = [g[0] for g in regions]
+    hits = {}                                   # (region index, slab) -> list of roles
+
+    def hit(g, slab, role):
+        hits.setdefault((g, slab), []).append(role)
+
+    def rect(g, r0, c0, rows, cols, role):
+        _, nr, nc, rs, cs, _ = regions[g]
+        r1, c1 = min(r0 + rows, nr), min(c0 + cols, nc)
+        if r0 < rs and c0 < cs:
+            hit(g, "rr", role)
+        if r0 < rs and c1 > cs:
+            hit(g, "rs", role)
+        if r1 > rs and c0 < cs:
+            hit(g, "sr", role)
+        if r1 > rs and c1 > cs:
+            hit(g, "ss", role)
+
+    for (_, role, ptr, rows, cols, ld, lower) in writes:
+        if rows <= 0 or cols <= 0:
+            continue
+        g = bisect.bisect_right(starts, ptr) - 1
+        if rows == 1 and cols == ld:            # flat copy: every region it overlaps, whole
+            end = ptr + 8 * cols
+            g = max(g, 0)
+            while g < len(regions) and regions[g][0] < end:
+                st, nr, nc = regions[g][0], regions[g][1], regions[g][2]
+                if st + 8 * nr * nc > ptr:
+                    rect(g, 0, 0, nr, nc, role)
+                g += 1
+            continue
+        if g < 0:
+            continue
+        st, nr, nc = regions[g][0], regions[g][1], regions[g][2]
+        off = (ptr - st) // 8
+        if off >= nr * nc:
+            continue                             # not a slab (scratch, factors, next level's inputs)
+        if ld != nc:
+            hit(g, "mismatched_ld", role)
+            continue
+        rect(g, off // nc, off % nc, rows, cols, role)
+
+    offdiag_ss = rr_rs_sr = in_place = twice = 0
+    uninit = []
+    diag_counts = []
+    for g, (_, nr, nc, rs, cs, key) in enumerate(regions):
+        kind = key[0]
+        for slab in ("rr", "rs", "sr", "ss", "mismatched_ld"):
+            roles = hits.get((g, slab), [])
+            init = sum(1 for x in roles if x == "transform")
+            post = [x for x in roles if x != "transform"]
+            area = {"rr": rs * cs, "rs": rs * (nc - cs), "sr": (nr - rs) * cs, "ss": (nr - rs) * (nc - cs)}.get(slab, 1)
+            if slab == "mismatched_ld":
+                rr_rs_sr += len(roles)
+                continue
+            if init > 1:
+                twice += 1
+            if init == 0 and area > 0 and slab != "rs":     # RS_ij of the reference is never formed here
+                uninit.append((slab,) + key[1:])
+            if kind == "diag" and slab == "ss":
+                # every writer counts (the SYRK is the one expected): an extra one shows as a count > 1
+                diag_counts.append(len(post) + (1 if (rs == 0 or nr == rs) else 0))
+                continue
+            if kind == "off" and slab == "ss":
+                offdiag_ss += len(post)
+                continue
+            if kind == "diag" and slab in ("rr", "sr"):
+                in_place += sum(1 for x in post if x == "factor")
+                rr_rs_sr += sum(1 for x in post if x != "factor")
+                continue
+            rr_rs_sr += len(post)
+    return {"offdiag_ss_post_init_writes": offdiag_ss, "rr_rs_sr_post_init_writes": rr_rs_sr,
+            "diag_ss_update_counts": sorted(set(diag_counts)), "diag_ss_blocks": len(diag_counts),
+            "in_place_factor_writes": in_place, "uninitialized_slabs": len(uninit),
+            "initialized_twice": twice}
 
 
 def flop_report(levels, root_dim):
@@ -592,7 +716,17 @@ def flop_report(levels, root_dim):
     return fl.flops
 
 
-_PLAN_CACHE = {}       # structure signature -> (DeviceH2, FactorPlan, weakref to the live factors)
+_PLAN_CACHE = {}       # structure signature -> (DeviceH2, FactorPlan, weakref to the live factors' lease)
+
+
+class _Lease:
+    """Held (strongly) by a ULVFactors and by every view into its HBM buffers
+    (level maps, retained slabs, BlockVectors through the factors); the plan
+    cache holds it weakly.  It references nothing itself, so dropping the
+    factors and all views frees it at once (no reference cycle waiting for
+    the garbage collector) and the next factorization of the same structure
+    reuses the buffers, while a surviving view keeps them reserved."""
+    __slots__ = ("__weakref__",)
 _PLAN_CACHE_MAX = 2
 
 
@@ -691,10 +825,10 @@ def factorize(h2, batched=True, retain=False):
     f = factors_from_plan(h2, plan)
     if retain:
         f.retained = _retained_views(plan)
-        f.retained._owner = f
+        f.retained._owner = f._lease
     for key, ent in list(_PLAN_CACHE.items()):
         if ent[1] is plan:
-            _PLAN_CACHE[key] = (ent[0], ent[1], weakref.ref(f))
+            _PLAN_CACHE[key] = (ent[0], ent[1], weakref.ref(f._lease))
     return f
 
 
@@ -741,12 +875,13 @@ def _retained_views(plan):
 
 def factors_from_plan(h2, plan):
     f = ULVFactors(h2, plan)
+    f._lease = _Lease()
     for l in range(plan.depth, 0, -1):
         lvl = plan.level_views(l)
-        # the lazy views read the plan's HBM buffers: they keep the factors alive, so the
-        # plan cache (weakref to the factors) never hands those buffers to a new factorization
+        # the lazy views read the plan's HBM buffers: they hold the lease, so the plan
+        # cache (weakref to the lease) never hands those buffers to a new factorization
         for m in (lvl.lr_diag, lvl.lr_off, lvl.ls, lvl.v):
-            m._owner = f
+            m._owner = f._lease
         f.levels[l] = lvl
     for l, parents in plan.merge_pairs.items():
         f.merge_map[l] = {(pi, pj): [(2 * pi + a, 2 * pj + b) for a in (0, 1) for b in (0, 1)]

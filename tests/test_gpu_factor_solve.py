@@ -30,7 +30,9 @@ def test_factor_blocks_match_reference(pkg, name):
     ref = reference_factors(name)
     f = pkg.factorize(h2)
     assert flops_equal(f.flops, meta(name)["flops"])
-    assert f.audit["offdiag_ss_post_init_writes"] == 0 and f.audit["diag_ss_update_counts"] == [1]
+    # the audit is derived from the program's write extents; its four reference keys equal the reference's
+    assert {k: f.audit[k] for k in meta(name)["audit"]} == meta(name)["audit"]
+    assert f.audit["uninitialized_slabs"] == 0 and f.audit["initialized_twice"] == 0
     for (l, i), v in ref["lr_diag"].items():
         assert _rel(f.levels[l].lr_diag[i], v) < RTOL_BLOCK, (l, i)
     for (l, i, j), v in ref["lr_off"].items():
@@ -114,3 +116,24 @@ def test_retain_slabs_consistent(pkg, name):
         for (i, j), lo in lvl.lr_off.items():
             if lo.size:
                 assert _rel(lo @ lvl.lr_diag[j].T, f.retained[("rr", l, i, j)]) < 1e-10, (l, i, j)
+
+
+def test_plan_cache_reused_after_factors_dropped(pkg):
+    """Dropping the factors frees their lease at once (no reference cycle), so the
+    next factorization of the same structure reuses the cached program and HBM
+    buffers; a surviving view keeps them reserved (lifetime of views)."""
+    import gc
+
+    h2 = load_h2(H2_FIXTURES[0])
+    f1 = pkg.factorize(h2)
+    p1 = f1.device
+    del f1
+    f2 = pkg.factorize(h2)
+    assert f2.device is p1
+    view = f2.levels[max(f2.levels)].lr_diag
+    del f2
+    gc.collect()
+    f3 = pkg.factorize(h2)
+    assert f3.device is not p1          # the view still reads p1's buffers
+    v0 = view[0]
+    assert v0.shape[0] == v0.shape[1]
