@@ -529,59 +529,18 @@ class PinnedArena:
 
 def h2_matvec(h2, x):
     """y = A x through the hierarchical representation, tree order
-    (h2_build.py:232-282).  On the GPU (one grouped GEMV per level and pass,
-    matvec_device.MatvecPlan) when the operands are in HBM (our construct);
-    otherwise the reference's host algorithm."""
-    if getattr(h2, "_device", None) is not None:
-        from .matvec_device import device_matvec
+    (h2_build.py:232-282), on the GPU: one grouped GEMV launch per level and
+    pass (matvec_device.MatvecPlan).  A GPU-built H² uses the operands already
+    in HBM; a host (numpy) H² — the reference's data model, e.g. one read back
+    by storage.load_h2 — is uploaded with DeviceH2.from_host on every call, so
+    the product stays a pure function of the blocks and the two agree bit for
+    bit (test_storage.py:49-55).  There is no host path."""
+    from .matvec_device import device_matvec
 
-        xm = np.asarray(x, dtype=np.float64)
-        if xm.reshape(xm.shape[0], -1).shape[0] != h2.count:
-            raise ValueError("length mismatch")
-        return device_matvec(h2, xm)
-    return h2_matvec_host(h2, x)
-
-
-def h2_matvec_host(h2, x):
-    """The reference's host H² matvec (h2_build.py:232-282), numpy."""
-    x = np.asarray(x, dtype=np.float64)
-    vec = x.ndim == 1
-    xm = x.reshape(h2.count, -1)
-    if xm.shape[0] != h2.count:
+    xm = np.asarray(x, dtype=np.float64)
+    if xm.reshape(xm.shape[0], -1).shape[0] != h2.count:
         raise ValueError("length mismatch")
-    tree, lists = h2.tree, h2.lists
-    depth = tree.depth
-    if depth == 0:
-        y = h2.near_blocks[(0, 0, 0)] @ xm
-        return y[:, 0] if vec else y
-    y = np.zeros_like(xm)
-    up = {}
-    for l in range(depth, 0, -1):
-        for i in range(2 ** l):
-            if l == depth:
-                b = tree.box(l, i)
-                seg = xm[b.begin:b.end]
-            else:
-                seg = np.vstack([up[(l + 1, 2 * i)], up[(l + 1, 2 * i + 1)]])
-            up[(l, i)] = h2.bases[(l, i)].q_skel.T @ seg
-    down = {key: np.zeros_like(v) for key, v in up.items()}
-    for l in range(depth, 0, -1):
-        for (i, j) in lists.far[l]:
-            down[(l, i)] += h2.coupling(l, i, j) @ up[(l, j)]
-    for l in range(1, depth + 1):
-        for i in range(2 ** l):
-            full = h2.bases[(l, i)].q_skel @ down[(l, i)]
-            if l == depth:
-                b = tree.box(l, i)
-                y[b.begin:b.end] += full
-            else:
-                ka = h2.bases[(l + 1, 2 * i)].rank
-                down[(l + 1, 2 * i)] += full[:ka]
-                down[(l + 1, 2 * i + 1)] += full[ka:]
-    for (i, j) in lists.near[depth]:
-        bi, bj = tree.box(depth, i), tree.box(depth, j)
-        y[bi.begin:bi.end] += h2.near_block(depth, i, j) @ xm[bj.begin:bj.end]
-    return y[:, 0] if vec else y
+    return device_matvec(h2, xm)
 
 
 def build_basis_for_box(kernel, cloud, box_pts, far_pts, close_block, rank=None, tol=None, row_weight=None):

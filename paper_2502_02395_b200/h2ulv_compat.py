@@ -10,7 +10,7 @@ GPU path:
     from h2ulv.ulv_factor import factorize          # the GPU factorization
 
 Modules of the reference that are outside this build's hot path (the dense
-oracle, the storage container, the communication simulator, the CLI) are
+oracle, the communication simulator, the CLI) are
 not provided by the package.  `install(extra_dir=...)` loads them from a
 directory holding the reference's own files, as submodules of the alias, so
 their relative imports (`from . import kernels`) bind to this package's
@@ -22,10 +22,10 @@ import importlib.util
 import os
 import sys
 
-PROVIDED = ("dense_core", "errors", "geometry", "h2_build", "kernels", "ulv_factor", "ulv_solve")
+PROVIDED = ("dense_core", "errors", "geometry", "h2_build", "kernels", "storage", "ulv_factor", "ulv_solve")
 
 
-def install(extra_dir=None, extra=("oracle", "storage", "comm_sim", "cli")):
+def install(extra_dir=None, extra=("oracle", "comm_sim", "cli")):
     import paper_2502_02395_b200 as pkg
 
     sys.modules["h2ulv"] = pkg

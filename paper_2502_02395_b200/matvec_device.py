@@ -132,16 +132,24 @@ def dh2_child_off(dh2, l, i, koff):
 
 
 def device_matvec(h2, x):
-    """y = A x (tree order) with the operands of h2._device; plans cached per width."""
+    """y = A x (tree order).  GPU-built H²: the operands of h2._device, plans
+    cached per width.  Host H²: uploaded (DeviceH2.from_host) and planned per
+    call — a pure function of the numpy blocks."""
     nat.lib()
-    dh2 = h2._device
+    dh2 = getattr(h2, "_device", None)
     xm = np.asarray(x, dtype=np.float64)
     vec = xm.ndim == 1
     xm = xm.reshape(h2.count, -1)
     w = xm.shape[1]
-    cache = h2.__dict__.setdefault("_matvec_plans", {})
-    if w not in cache:
-        cache[w] = MatvecPlan(dh2, h2.tree, h2.lists, w)
-    plan = cache[w]
+    if dh2 is None:
+        from .h2_device import DeviceH2
+
+        dh2 = DeviceH2.from_host(h2)
+        plan = MatvecPlan(dh2, h2.tree, h2.lists, w)
+    else:
+        cache = h2.__dict__.setdefault("_matvec_plans", {})
+        if w not in cache:
+            cache[w] = MatvecPlan(dh2, h2.tree, h2.lists, w)
+        plan = cache[w]
     y = plan.run(torch.from_numpy(np.ascontiguousarray(xm)).to(dh2.device)).cpu().numpy()
     return y[:, 0] if vec else y

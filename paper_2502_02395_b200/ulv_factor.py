@@ -85,31 +85,98 @@ class ULVLevel:
 
 
 class ULVFactors:
-    """Factor container with the reference's attributes (ulv_factor.py:34-47)."""
+    """Factor container with the reference's attributes (ulv_factor.py:34-47).
 
-    def __init__(self, h2, plan):
+    Device factors (`plan` given, from factorize): the blocks stay in HBM and
+    `levels[l].lr_diag[i]` etc. download lazily.  Host factors (`plan` None,
+    the reference's own constructor signature `ULVFactors(h2=...)`, e.g. from
+    storage.load_factors): numpy blocks filled in by the caller; the first
+    solve uploads them into the device layout (plan_from_host_factors)."""
+
+    def __init__(self, h2, plan=None, levels=None, root=None, merge_map=None, flops=None, audit=None,
+                 retained=None):
         self.h2 = h2
         self._plan = plan
-        self.levels = {}
-        self.merge_map = {}
-        self.flops = plan.flops
-        self.audit = plan.audit
-        self.retained = None
-        self._root = None
+        self.levels = {} if levels is None else levels
+        self.merge_map = {} if merge_map is None else merge_map
+        self.flops = plan.flops if plan is not None else ({} if flops is None else flops)
+        self.audit = plan.audit if plan is not None else ({} if audit is None else audit)
+        self.retained = retained
+        self._root = root
+        self._host = plan is None
 
     @property
     def depth(self):
-        return self._plan.depth
+        return self._plan.depth if self._plan is not None else self.h2.tree.depth
 
     @property
     def root(self):
-        if self._root is None:
+        if self._root is None and self._plan is not None:
             self._root = self._plan.download_root()
         return self._root
 
+    @root.setter
+    def root(self, value):
+        self._root = value
+
     @property
     def device(self):
+        """The FactorPlan whose HBM buffers hold these factors (uploaded on first use for host factors)."""
+        if self._plan is None:
+            self._plan = plan_from_host_factors(self)
         return self._plan
+
+
+def factor_plan_of(factors):
+    """FactorPlan of any factor container: ours, or a duck-typed host one
+    (e.g. the reference's own ULVFactors dataclass), uploaded once."""
+    if isinstance(factors, ULVFactors):
+        return factors.device
+    plan = factors.__dict__.get("_b200_plan")
+    if plan is None:
+        plan = plan_from_host_factors(factors)
+        factors.__dict__["_b200_plan"] = plan
+    return plan
+
+
+def plan_from_host_factors(factors):
+    """Device layout of host (numpy) factors: the bases / leaf blocks of
+    factors.h2 (DeviceH2) and every factor block the substitution reads —
+    L(r)_ii and L(s)_ii into H_i, lr_off / L(s)_ij into T_ij, L(s)_ji into
+    the mirror slab, L_00 into the root buffer — placed exactly where the
+    factorization leaves them, so the same solve program runs on them."""
+    h2 = factors.h2
+    dh2 = getattr(h2, "_device", None)
+    if dh2 is None:
+        dh2 = DeviceH2.from_host(h2)
+    plan = FactorPlan(dh2, h2.lists)
+    for l, B in plan.bufs.items():
+        lay = B.lay
+        lvl = factors.levels[l]
+        n, r = lay.n, lay.r
+        H = np.zeros(B.H.numel())
+        for i in range(lay.nb):
+            ni, ri = int(n[i]), int(r[i])
+            blk = H[int(lay.qoff[i]):int(lay.qoff[i]) + ni * ni].reshape(ni, ni)
+            blk[:ri, :ri] = lvl.lr_diag[i]
+            blk[ri:, :ri] = lvl.ls[(i, i)]
+        T = np.zeros(B.T.numel())
+        LS = np.zeros(B.LSm.numel())
+        for (i, j), off in B.toff.items():
+            ni, nj, ri, rj = int(n[i]), int(n[j]), int(r[i]), int(r[j])
+            blk = T[off:off + ni * nj].reshape(ni, nj)
+            blk[:ri, :rj] = lvl.lr_off[(i, j)]
+            blk[ri:, :rj] = lvl.ls[(i, j)]
+            kj = nj - rj
+            o = B.lsoff[(i, j)]
+            LS[o:o + kj * ri] = np.asarray(lvl.ls[(j, i)], dtype=np.float64).reshape(-1)
+        for dst, src in ((B.H, H), (B.T, T), (B.LSm, LS)):
+            dst.copy_(torch.from_numpy(src))
+    d = plan.root_dim
+    plan.root_buf[:d * d].copy_(torch.from_numpy(np.ascontiguousarray(factors.root, dtype=np.float64).reshape(-1)))
+    plan.generation = 1
+    torch.cuda.synchronize(plan.device)
+    return plan
 
 
 def _mat(t, off, rows, cols, ld, r0=0, c0=0):
@@ -136,6 +203,7 @@ class FactorPlan:
     def __init__(self, dh2: DeviceH2, lists, part=None, comm=None, level_cuts=False):
         self.dh2 = dh2
         self.depth = dh2.depth
+        self.generation = 0      # bumped whenever the buffers receive new factors (solve inverses follow)
         self.part = part
         self.comm = comm
         dev = dh2.device
@@ -316,12 +384,11 @@ class FactorPlan:
         return partial_cholesky_steps(prog, self.device, self.npd.data_ptr(), Hp, Rp, qo, n, r, slot0, mine, Qp)
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
-        """Root: full Cholesky of the merged d x d block; the identity rides along so
-        that root_winv = L^-T (upper) turns the solve's root TRSVs into GEMVs."""
+        """Root: full Cholesky of the merged d x d block (the solve forms its
+        explicit inverse from L_00 itself, ulv_solve.SolvePlan._build_prepare)."""
         assert d == ld
-        self.root_winv = torch.zeros(max(d * d, 1), dtype=F64, device=self.device)
-        self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, self.root_winv.data_ptr(), np.array([0]),
-                                                            np.array([d]), np.array([d]), slot)
+        self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]),
+                                                            np.array([d]), slot)
 
     def _merge_steps(self, prog, l, B, lists, dh2):
         lay = B.lay
@@ -395,6 +462,7 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ run / check
     def run(self, stream=None):
+        self.generation += 1
         if self.program is not None:
             self.program.launch(stream)
             return
@@ -435,6 +503,7 @@ class FactorPlan:
                 seg.launch(stream)
                 state["i"] += 1
 
+        self.generation += 1
         return on_level, finish
 
     def capture(self):

@@ -74,6 +74,7 @@ class SolvePlan:
                              offS=np.concatenate([[0], np.cumsum(lay.k)[:-1]]).astype(np.int64),
                              offX=np.concatenate([[0], np.cumsum(lay.n)[:-1]]).astype(np.int64))
         self.dist = fplan.part is not None and fplan.part.p > 1
+        self._build_prepare()
         self._segs = []
         self._masks = {}
         self.fwd_segments = self._finish(self._build_forward())
@@ -81,6 +82,50 @@ class SolvePlan:
         self.fwd = self.fwd_segments[0] if len(self.fwd_segments) == 1 else None
         self.bwd = self.bwd_segments[0] if len(self.bwd_segments) == 1 else None
         self.output = self.v[depth]["FULL"] if depth >= 1 else self.xroot
+
+    # -------------------------------------------------------------- triangular inverses
+    def _build_prepare(self):
+        """The inverses the substitution reads are formed from the stored factor
+        blocks themselves, once per factorization (h2g_tri_inv: the 64 x 64
+        diagonal blocks of every L(r)_ii; the root's explicit W = L_00^-T by
+        the row solve of the identity), not taken from the Cholesky's own
+        by-products.  The solve is then a pure function of the factor blocks
+        (lr_diag, lr_off, ls, root) — like the reference's — so factors read
+        back from storage solve to the same bits (test_storage.py:90-98)."""
+        fp = self.fp
+        dev = self.device
+        W = nat.PANEL_WIDTH
+        prog = Program(dev)
+        self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        self.linv, self.loff = {}, {}
+        for l in range(fp.depth, 0, -1):
+            B = fp.bufs[l]
+            lay = B.lay
+            nblk = -(-np.asarray(lay.r, dtype=np.int64) // W)
+            loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
+            lt = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
+            self.linv[l], self.loff[l] = lt, loff
+            mine = self._mine(l)
+            prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
+                          int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
+                        self._tri_status.data_ptr())
+        d = fp.root_dim
+        nb0 = -(-d // W)
+        self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
+        self.root_w = torch.zeros(max(d * d, 1), dtype=F64, device=dev)
+        rp = fp.root_buf.data_ptr()
+        prog.triinv([(rp, self.root_linv.data_ptr(), d, d, 0)], self._tri_status.data_ptr())
+        prog.trsm_rows([(rp, 0, self.root_w.data_ptr(), self.root_linv.data_ptr(), d, d, 0, nb0, d, d)])
+        self.prepare = prog.finalize()
+        self.prepare.capture()
+        self._prepared = None
+
+    def ensure_prepared(self, stream=None):
+        """Run the inverse program if the factors changed since the last solve."""
+        gen = self.fp.generation
+        if self._prepared != gen:
+            self.prepare.launch(stream)
+            self._prepared = gen
 
     # -------------------------------------------------------------- distribution
     def _mine(self, l):
@@ -149,17 +194,17 @@ class SolvePlan:
         """TRSV descriptor (L, Linv, x, n, ld) of box i at level l (l = 0: root)."""
         if l == 0:
             d = self.fp.root_dim
-            return (self.fp.root_buf.data_ptr(), self.fp.root_linv.data_ptr(), x, d, d)
+            return (self.fp.root_buf.data_ptr(), self.root_linv.data_ptr(), x, d, d)
         B = self.fp.bufs[l]
         lay = B.lay
-        return (B.H.data_ptr() + 8 * int(lay.qoff[i]), B.linv.data_ptr() + 8 * int(B.loff[i]) * 4096, x,
+        return (B.H.data_ptr() + 8 * int(lay.qoff[i]), self.linv[l].data_ptr() + 8 * int(self.loff[l][i]) * 4096, x,
                 int(lay.r[i]), int(lay.n[i]))
 
     def _root_solve(self, prog, y, x, trans):
         """y = L_00^-1 x (trans 0) or L_00^-T x (trans 1) with the root's explicit
         W = L_00^-T from the factorization: one grouped GEMV instead of a TRSV."""
         d = self.fp.root_dim
-        wp = self.fp.root_winv.data_ptr()
+        wp = self.root_w.data_ptr()
         prog.gemv([(y.data_ptr(), 0, 0, d, 0, nat.GEMV_PLUS, [(wp, x.data_ptr(), d, 1 - trans, d)])], self.w)
 
     # -------------------------------------------------------------- forward
@@ -341,12 +386,14 @@ class SolvePlan:
 
     # -------------------------------------------------------------- run
     def run_forward(self, stream=None):
+        self.ensure_prepared(stream)
         if self.fwd is not None:
             self.fwd.launch(stream)
         else:
             self._run_segments(self.fwd_segments, stream)
 
     def run_backward(self, stream=None):
+        self.ensure_prepared(stream)
         if self.bwd is not None:
             self.bwd.launch(stream)
         else:
@@ -368,7 +415,9 @@ class SolvePlan:
 def _plan_for(factors, w, mode):
     """Solve programs live with the factorization program they read, so a
     re-factorization with a cached FactorPlan reuses them too."""
-    fp = factors.device
+    from .ulv_factor import factor_plan_of
+
+    fp = factor_plan_of(factors)
     cache = fp.__dict__.setdefault("_solve_plans", {})
     key = (w, mode)
     if key not in cache:
@@ -422,7 +471,7 @@ def _backward(factors, y, mode):
     right-hand side cannot leak into the result."""
     nat.lib()
     sp = _plan_for(factors, y.width, mode)
-    fp = factors.device
+    fp = sp.fp
     with torch.cuda.device(sp.device):
         for l in range(fp.depth, 0, -1):
             V = sp.v[l]

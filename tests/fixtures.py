@@ -66,9 +66,9 @@ def load_h2(name):
             qs = z[f"q_skel/{l}/{i}"]
             bases[(l, i)] = BasisDecomposition(q_skel=qs, q_red=z[key], skeleton=z[f"skeleton/{l}/{i}"],
                                                rank=qs.shape[1], frame=None)
-        elif parts[0] == "near":
+        elif parts[0] == "near" and len(parts) == 4:
             near[tuple(int(p) for p in parts[1:])] = z[key]
-        elif parts[0] == "coupling":
+        elif parts[0] == "coupling" and len(parts) == 4:
             cpl[tuple(int(p) for p in parts[1:])] = z[key]
     h2.bases, h2.near_blocks, h2.couplings = bases, near, cpl
     return h2
