@@ -132,6 +132,25 @@ int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count, const int
                         int32_t* d_npd, int32_t* d_sync, void* stream);
 int h2g_chol_panel_fused_max(void);
 
+/* ---- fused per-box partial Cholesky ----------------------------------------
+ * ONE CTA per descriptor (box) performs the box's whole elimination
+ * (ulv_factor.py:217-241, factor_diag): left-looking over the 64-wide panels
+ * of RR, each diagonal block updated by the earlier panels, factored
+ * (L_qq -> H, L_qq^-1 -> Linv + 4096 q, pivot status -> d_npd exactly like
+ * h2g_chol_panel), every row below it (rest of RR and the SR rows) updated
+ * and solved against L_qq^-T in place; then the single Schur update
+ * SS -= L(s) L(s)^T on the lower 64 x 64 tiles of the k x k corner.  For
+ * levels with many boxes: no per-panel launches and no inter-CTA waits.
+ */
+typedef struct h2g_cholbox_desc {
+  double* H;          /* n x n, ld ldh; RR = H[:r, :r], SR = H[r:, :r], SS = H[r:, r:] (lower parts used) */
+  double* Linv;       /* ceil(r / 64) blocks of 64 x 64 */
+  int32_t n, r;
+  int32_t ldh, npd_slot;
+} h2g_cholbox_desc;
+
+int h2g_chol_box(const h2g_cholbox_desc* d_descs, int count, int32_t* d_npd, void* stream);
+
 /* ---- left-looking row solve --------------------------------------------------
  * X = B L^-T block column by block column, one CTA per 64-row chunk of every
  * descriptor.  For panel q in [q_begin, q_end) (p = 64q, b = min(64, cols-p)):
@@ -347,6 +366,7 @@ enum {
   H2G_STEP_TRSM_ROWS = 14,  /* descs/map = rows descs/tile map */
   H2G_STEP_SYMCHECK = 15,   /* descs = symcheck descs; aux = device output (2 x count u64) */
   H2G_STEP_TRIINV = 16,     /* descs/map = triinv descs/tile map; npd = status */
+  H2G_STEP_CHOL_BOX = 17,   /* descs = cholbox descs; npd = status */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

@@ -949,6 +949,228 @@ __global__ void __launch_bounds__(RW_THREADS, 3) trsm_rows_kernel(const h2g_rows
   }
 }
 
+
+// ------------------------------------------------------------------ fused per-box partial Cholesky
+// chol_box_kernel (h2g_chol_box): ONE CTA factors one box's H completely —
+// the whole ULV elimination of the box (ulv_factor.py:217-241) in one
+// kernel: for every 64-column panel q of RR, left-looking,
+//   diag:   D = H[p:p+b, p:p+b] - L[p:p+b, 0:p] L[p:p+b, 0:p]^T  (DMMA)
+//           -> L_qq (blocked 64x64 factorization, diag_blocked) and L_qq^-1,
+//              pivot status (NotPositiveDefiniteError contract)
+//   rows:   for every 64-row chunk below (the rest of RR and all SR rows)
+//           L[c, p:p+b] = (H[c, p:p+b] - L[c, 0:p] L[p:p+b, 0:p]^T) L_qq^-T
+// then the single Schur update SS -= L(s) L(s)^T (lower 64x64 tiles, K = r).
+// No trailing matrix is ever written back (left-looking), so a box costs one
+// read of its block columns per panel and no inter-CTA synchronisation; the
+// latency of the 64-pivot chains is hidden by the other boxes' CTAs on the
+// SM (3 per SM).  Used for levels with many boxes (the leaf of N = 1M has
+// 4096), where a launch per panel step leaves the SMs waiting on the chain.
+// Shared memory: the two stage regions of trsm_rows (74 KB); the diagonal
+// factorization puts D in region 0 (+ its pivots / 16x16 scratch in the
+// region's spare tail) and L_qq^-1 in region 1.
+constexpr int CB_PV = PB * SD;                  // pivots after D in region 0
+constexpr int CB_CS = CB_PV + PB;               // Chol16Shared after the pivots
+static_assert(CB_CS + (int)(sizeof(Chol16Shared) / sizeof(double)) <= TS_REGION, "diag scratch must fit region 0");
+
+// acc (64 x 64, warp tile 32 x 16 at (wm, wn)) += A[0:arows, 0:K] B[0:brows, 0:K]^T, operands row-major in
+// global memory (lda / ldb), streamed through the two stage regions in 64 x 32 slices.  Leaves both
+// regions free (ends with a barrier).
+__device__ __forceinline__ void cb_gemm_nt(double (&acc)[4][2][2], const double* __restrict__ A, int lda, int arows,
+                                           const double* __restrict__ B, int ldb, int brows, int K, double* tsm,
+                                           bool wact) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int KT = (K + TS_BK - 1) / TS_BK;
+  auto load_stage = [&](int st, int k0) {
+    double* as = tsm + st * TS_REGION;
+    double* bs = as + PB * TS_S;
+#pragma unroll
+    for (int u = 0; u < (PB * TS_BK) / RW_THREADS; ++u) {
+      const int idx = tid + u * RW_THREADS;
+      const int m = idx / TS_BK, k = idx % TS_BK;
+      const bool va = m < arows && k0 + k < K;
+      cp_async8(as + m * TS_S + k, va ? A + (size_t)m * lda + k0 + k : A, va);
+      const bool vb = m < brows && k0 + k < K;
+      cp_async8(bs + m * TS_S + k, vb ? B + (size_t)m * ldb + k0 + k : B, vb);
+    }
+  };
+  if (KT > 0) load_stage(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt + 1 < KT) load_stage((kt + 1) & 1, (kt + 1) * TS_BK);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* as = tsm + (kt & 1) * TS_REGION;
+    const double* bs = as + PB * TS_S;
+#pragma unroll
+    for (int kk = 0; kk < (wact ? TS_BK : 0); kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(wm * 32 + i * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * TS_S + kk + tq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// acc = -X[0:rows, 0:cols] (ld ldx): the K loop then accumulates +A B^T, the result is -acc
+__device__ __forceinline__ void cb_load_neg(double (&acc)[4][2][2], const double* X, int ldx, int rows, int cols) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3, wm = warp >> 2, wn = warp & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq + e;
+        acc[i][j][e] = (m < rows && c < cols) ? neg_int(X[(size_t)m * ldx + c]) : 0.0;
+      }
+}
+
+__device__ __forceinline__ void cb_store_neg(const double (&acc)[4][2][2], double* S, int lds) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3, wm = warp >> 2, wn = warp & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m = wm * 32 + i * 8 + g, c = wn * 16 + j * 8 + 2 * tq;
+      S[m * lds + c] = neg_int(acc[i][j][0]);
+      S[m * lds + c + 1] = neg_int(acc[i][j][1]);
+    }
+}
+
+__global__ void __launch_bounds__(RW_THREADS, 3) chol_box_kernel(const h2g_cholbox_desc* __restrict__ descs,
+                                                                 int32_t* __restrict__ npd) {
+  extern __shared__ __align__(16) double tsm[];
+  const h2g_cholbox_desc P = descs[blockIdx.x];
+  const int n = P.n, r = P.r, ld = P.ldh;
+  double* __restrict__ H = P.H;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3, wm = warp >> 2, wn = warp & 3;
+  double* R0 = tsm;
+  double* R1 = tsm + TS_REGION;
+  bool bad = false;
+  const int nq = (r + PB - 1) / PB;
+#pragma unroll 1
+  for (int q = 0; q < nq; ++q) {
+    const int p = PB * q, b = min(PB, r - p);
+    double* Hp = H + (size_t)p * ld;          // rows p.., column 0
+    double acc[4][2][2];
+    // ---- diagonal block: D = H[p:p+b, p:p+b] - L[p:p+b, 0:p] L[p:p+b, 0:p]^T
+    cb_load_neg(acc, Hp + p, ld, b, b);
+    cb_gemm_nt(acc, Hp, ld, b, Hp, ld, b, p, tsm, true);
+    cb_store_neg(acc, R0, SD);
+    __syncthreads();
+    if (tid < PB && tid >= b) {
+      for (int x = 0; x < PB; ++x) R0[tid * SD + x] = (x == tid) ? 1.0 : 0.0;   // identity padding
+    }
+    __syncthreads();
+    double* pv = R0 + CB_PV;
+    diag_blocked<8>(R0, R1, pv, *reinterpret_cast<Chol16Shared*>(R0 + CB_CS));
+    if (warp == 0) {
+      const unsigned lo = __ballot_sync(0xffffffffu, lane < b && !(pv[lane] > 0.0));
+      const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < b && !(pv[lane + 32] > 0.0));
+      if (lane == 0 && (lo | hi) && !bad) atomicMin(&npd[P.npd_slot], p + (lo ? __ffs(lo) - 1 : 32 + __ffs(hi) - 1));
+      bad = bad || (lo | hi);
+    }
+    double* Lq = P.Linv + (size_t)q * PB * PB;
+    for (int t = tid; t < PB * PB; t += RW_THREADS) {
+      const int i = t / PB, x = t % PB;
+      if (x <= i && i < b) Hp[(size_t)i * ld + p + x] = R0[i * SD + x];
+      Lq[(size_t)i * PB + x] = R1[i * SD + x];
+    }
+    __syncthreads();
+    // ---- row chunks below the diagonal block (rest of RR, then all SR rows)
+    const bool wact = wn * 16 < b;
+    const int kend = wact ? min(16 * (wn + 1), (b + 3) & ~3) : 0;   // Linv[n][k] = 0 for k > n, k >= b
+#pragma unroll 1
+    for (int c0 = p + b; c0 < n; c0 += PB) {
+      const int rows = min(PB, n - c0);
+      double* Hc = H + (size_t)c0 * ld;
+      cb_load_neg(acc, Hc + p, ld, rows, b);
+      cb_gemm_nt(acc, Hc, ld, rows, Hp, ld, b, p, tsm, wact);
+      // L_qq^-1 (written above by this CTA; .cg reads it from L2) -> R1, C = -acc -> R0
+#pragma unroll 4
+      for (int t = tid; t < PB * PB / 2; t += RW_THREADS) {
+        const int i = t / (PB / 2), x = 2 * (t % (PB / 2));
+        cp_async16_cg(R1 + i * SD + x, Lq + (size_t)i * PB + x);
+      }
+      cp_async_commit();
+      cb_store_neg(acc, R0, SD);
+      cp_async_wait<0>();
+      __syncthreads();
+      double out[4][2][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < kend; kk += 4) {
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = R0[(wm * 32 + i * 8 + g) * SD + kk + tq];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = R1[(wn * 16 + j * 8 + g) * SD + kk + tq];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma884(out[i][j], af[i], bf[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + g;
+        if (m >= rows) continue;
+        double* dst = Hc + (size_t)m * ld + p;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = wn * 16 + j * 8 + 2 * tq;
+          if (c < b) dst[c] = out[i][j][0];
+          if (c + 1 < b) dst[c + 1] = out[i][j][1];
+        }
+      }
+      __syncthreads();   // R0 / R1 are reused by the next chunk
+    }
+  }
+  // ---- the single Schur update SS -= L(s) L(s)^T (lower 64 x 64 tiles of the k x k corner, K = r)
+  const int k = n - r;
+  if (r > 0 && k > 0) {
+    const int T = (k + PB - 1) / PB;
+#pragma unroll 1
+    for (int t = 0; t < T * (T + 1) / 2; ++t) {
+      const int ti = tri_row(t), tj = t - ti * (ti + 1) / 2;
+      const int rows = min(PB, k - PB * ti), cols = min(PB, k - PB * tj);
+      double* A = H + (size_t)(r + PB * ti) * ld;
+      double* B = H + (size_t)(r + PB * tj) * ld;
+      double* C = A + r + PB * tj;
+      double acc[4][2][2];
+      cb_load_neg(acc, C, ld, rows, cols);
+      cb_gemm_nt(acc, A, ld, rows, B, ld, cols, r, tsm, true);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + g;
+        if (m >= rows) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = wn * 16 + j * 8 + 2 * tq;
+          if (c < cols) C[(size_t)m * ld + c] = neg_int(acc[i][j][0]);
+          if (c + 1 < cols) C[(size_t)m * ld + c + 1] = neg_int(acc[i][j][1]);
+        }
+      }
+    }
+  }
+}
+
 constexpr size_t TS_SMEM = (2 * TS_REGION) * sizeof(double);
 
 constexpr size_t DIAG_SMEM = (2 * PB * SD) * sizeof(double) + sizeof(LdltShared);
@@ -1018,6 +1240,20 @@ extern "C" int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count
   if (rc || total_tiles <= 0) return rc;
   h2g::chol_rows_kernel<<<total_tiles, h2g::RW_THREADS, h2g::RW_SMEM, st>>>(d_descs, d_tile_map);
   return h2g_check_launch("chol_rows");
+}
+
+extern "C" int h2g_chol_box(const h2g_cholbox_desc* d_descs, int count, int32_t* d_npd, void* stream) {
+  if (count <= 0) return H2G_OK;
+  if (!d_descs || !d_npd) return h2g_set_error(H2G_EINVAL, "h2g_chol_box: null argument");
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(h2g::chol_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::TS_SMEM);
+    attr_dev = dev;
+  }
+  h2g::chol_box_kernel<<<count, h2g::RW_THREADS, h2g::TS_SMEM, (cudaStream_t)stream>>>(d_descs, d_npd);
+  return h2g_check_launch("chol_box");
 }
 
 extern "C" int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int total_tiles, void* stream) {

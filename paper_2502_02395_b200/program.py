@@ -195,6 +195,27 @@ class Program:
                   self._blob(tmap) if tmap.size else -1, npd=npd_ptr, aux=sync.data_ptr(), flops=fl)
         return int(tiles.sum())
 
+    def chol_box(self, descs, npd_ptr):
+        """descs: list of (H, Linv, n, r, ldh, npd_slot): the fused per-box partial Cholesky
+        (h2g_chol_box, one CTA per box)."""
+        descs = [d for d in descs if d[3] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.CHOLBOX_DT)
+        for name, col in zip(("H", "Linv", "n", "r", "ldh", "npd_slot"), zip(*descs)):
+            arr[name] = col
+        role = self.role
+        self.role = "factor"      # RR -> L(r), SR -> L(s) in place
+        self._writes((d[0], d[2], d[3], d[4], False) for d in descs)
+        self.role = "schur"       # the single SS -= L(s) L(s)^T
+        self._writes((d[0] + 8 * (d[3] * d[4] + d[3]), d[2] - d[3], d[2] - d[3], d[4], True) for d in descs if d[2] > d[3])
+        self.role = role
+        n64, r64 = arr["n"].astype(np.int64), arr["r"].astype(np.int64)
+        k64 = n64 - r64
+        fl = int((r64 ** 3 // 3 + r64 * r64 * k64 + 2 * k64 * k64 * r64).sum())   # chol + trsm of SR + Schur
+        self._add(nat.STEP["CHOL_BOX"], len(descs), len(descs), self._blob(arr), npd=npd_ptr, flops=fl)
+        return len(descs)
+
     def trsm_rows(self, descs):
         """descs: list of (Lb, Xin, Xout, Linv, rows, cols, q_begin, q_end, ldlb, ldx): X = B L^-T for
         the block columns [q_begin, q_end) (h2g_trsm_rows), one CTA per 64-row chunk."""

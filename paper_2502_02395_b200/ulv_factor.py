@@ -34,6 +34,7 @@ GPU path, and it is deterministic (no atomics in any reduction), so repeated
 runs are bitwise identical — the property test_ulv_factor.py:227-241 checks.
 """
 
+import os
 import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass, field
@@ -49,6 +50,10 @@ from .program import Program
 
 INT_MAX = 2 ** 31 - 1
 F64 = torch.float64
+# fused per-box partial Cholesky (h2g_chol_box) for levels with at least this many boxes of
+# size <= CHOL_BOX_MAX_N; the panel-step chain otherwise (few large boxes: the upper levels)
+CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "1024"))
+CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -586,6 +591,24 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
     if rmax == 0:
         return linv, loff, None
     lp = linv.data_ptr()
+    nmine = int(mine.sum())
+    if Qp and nmine >= CHOL_BOX_MIN and int(np.asarray(n)[mine].max()) <= CHOL_BOX_MAX_N:
+        # many boxes: the whole elimination of a box in ONE CTA (h2g_chol_box), all boxes in
+        # one launch — no panel-by-panel launch chain, REST or separate SYRK
+        prog.chol_box([(Hp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), int(n[i]),
+                        slot0 + i) for i in range(nb) if mine[i] and r[i] > 0], npd_ptr)
+        prog.role = None
+        ev_fp = prog.event()
+        prog.record(ev_fp)
+        prog.lane = 4
+        prog.wait(ev_fp)
+        prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
+                         lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]), int(n[i]))
+                        for i in range(nb) if mine[i] and r[i] > 0])
+        ev_v = prog.event()
+        prog.record(ev_v)
+        prog.lane = 0
+        return linv, loff, ev_v
     rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
     for q, p in enumerate(range(0, rmax, W)):
         descs, rest, rows = [], [], []

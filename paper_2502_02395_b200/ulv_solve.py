@@ -257,17 +257,19 @@ class SolvePlan:
         prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb) if mine[i]], 0, w)
         if dist:
             prog = self._cut(prog, ("Z", l, "offR"))
-        # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j
+        # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j ;  P3  y_i = L_ii^-1 t_i.
+        # A box without lower near neighbours has t_i = b_R,i, so y_i = z_i (the same
+        # TRSV on the same input): Y starts as a copy of Z and P2 / P3 run only for the
+        # boxes with neighbours (none at a cube-shaped leaf level).
+        prog.memcpy(V["Y"].data_ptr(), V["Z"].data_ptr(), 8 * int(r.sum()) * w)
+        nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in below[i])]
         outs = []
-        for i in range(nb):
-            if not mine[i]:
-                continue
+        for i in nbr:
             terms = [(B.T.data_ptr() + 8 * int(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
                      for j in below[i] if r[j] > 0]
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
         prog.gemv(outs, w)
-        # P3  y_i = L_ii^-1 t_i
-        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in range(nb) if mine[i]], 0, w)
+        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in nbr], 0, w)
         if dist:
             prog = self._cut(prog, ("Y", l, "offR"))
         # P4  b_S,a -= sum_b L(s)_ab y_b
@@ -284,8 +286,11 @@ class SolvePlan:
             if owned is not None and not owned[a]:
                 continue
             ptr, ld = self._ls(l, a, b)
-            terms.setdefault(a, []).append((ptr, self._p(V["Y"], offR[b]), ld, 0, int(lay.r[b])))
-        outs = [(self._p(V["BS"], offS[a]), 0, self._p(V["BS"], offS[a]), int(lay.k[a]), 0, 0, sorted(t))
+            terms.setdefault(a, []).append((b, (ptr, self._p(V["Y"], offR[b]), ld, 0, int(lay.r[b]))))
+        # terms in box order (a structural order: the summation order — hence the bits — must not
+        # depend on where the buffers happen to live, so reloaded factors solve identically)
+        outs = [(self._p(V["BS"], offS[a]), 0, self._p(V["BS"], offS[a]), int(lay.k[a]), 0, 0,
+                 [tm for _, tm in sorted(t, key=lambda x: x[0])])
                 for a, t in sorted(terms.items())]
         prog.gemv(outs, w)
 
@@ -330,8 +335,9 @@ class SolvePlan:
             src = {}
             for (a, b) in self._ls_keys(lay):
                 ptr, ld = self._ls(l, a, b)
-                src.setdefault(b, []).append((ptr, self._p(xs, offS[a]), ld, 1, int(k[a])))
-            outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0, sorted(src.get(i, [])))
+                src.setdefault(b, []).append((a, (ptr, self._p(xs, offS[a]), ld, 1, int(k[a]))))
+            outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0,
+                     [tm for _, tm in sorted(src.get(i, []), key=lambda x: x[0])])
                     for i in range(nb) if mine[i]]
             prog.gemv(outs, w)
             if self.mode == "parallel":
@@ -340,15 +346,16 @@ class SolvePlan:
                 prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
                 if dist:
                     prog = self._cut(prog, ("Z2", l, "offR"))
+                # boxes without upper near neighbours: x_R,i = z2_i (same TRSV, same input)
+                prog.memcpy(V["XR"].data_ptr(), V["Z2"].data_ptr(), 8 * int(r.sum()) * w)
+                nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in above[i])]
                 outs = []
-                for i in range(nb):
-                    if not mine[i]:
-                        continue
+                for i in nbr:
                     terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
                 prog.gemv(outs, w)
-                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in range(nb) if mine[i]], 1, w)
+                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in nbr], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
             # B3  full_i = q_red x_R + q_skel x_S

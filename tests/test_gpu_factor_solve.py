@@ -137,3 +137,27 @@ def test_plan_cache_reused_after_factors_dropped(pkg):
     assert f3.device is not p1          # the view still reads p1's buffers
     v0 = view[0]
     assert v0.shape[0] == v0.shape[1]
+
+
+@pytest.mark.parametrize("name", H2_FIXTURES)
+def test_fused_box_cholesky_matches_reference(pkg, name, monkeypatch):
+    """The fused per-box partial Cholesky (h2g_chol_box, used for levels with many
+    boxes) forced on every level: factor blocks vs the reference's, audit, solve."""
+    from paper_2502_02395_b200 import ulv_factor
+    monkeypatch.setattr(ulv_factor, "CHOL_BOX_MIN", 1)
+    ulv_factor.clear_cache()
+    h2 = load_h2(name)
+    ref = reference_factors(name)
+    f = pkg.factorize(h2)
+    assert any(k == ulv_factor.nat.STEP["CHOL_BOX"] for k in f.device.program.step_kinds)
+    assert {k: f.audit[k] for k in meta(name)["audit"]} == meta(name)["audit"]
+    for (l, i), v in ref["lr_diag"].items():
+        assert _rel(f.levels[l].lr_diag[i], v) < RTOL_BLOCK, (l, i)
+    for (l, a, b), v in ref["ls"].items():
+        assert _rel(f.levels[l].ls[(a, b)], v) < RTOL_BLOCK, (l, a, b)
+    for (l, i, j), v in ref["lr_off"].items():
+        assert _rel(f.levels[l].lr_off[(i, j)], v) < RTOL_BLOCK, (l, i, j)
+    assert _rel(f.root, ref["root"]) < RTOL_BLOCK
+    x = pkg.solve(f, ref["b"])
+    assert _rel(x, ref["x"]) < RTOL_X
+    ulv_factor.clear_cache()
