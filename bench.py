@@ -66,6 +66,15 @@ CONFIGS = {
     "c2": dict(shape="cube", n=65536, leaf=256, family="laplace", shift=1e5, tol=1e-8, s_far=512, s_near=512),
     "c3": dict(shape="sphere", n=262144, leaf=256, family="yukawa", shift=1e5, tol=1e-8, s_far=512, s_near=512),
     "m1": dict(shape="cube", n=1048576, leaf=256, family="laplace", shift=2e6, tol=1e-8, s_far=512, s_near=512),
+    # BASELINE configs[3]: Gaussian covariance exp(-(r/l)^2), l = 0.1 (no reference family: opt-in
+    # GaussianKernelSpec; shift ~ 2x the kernel row sum N pi^1.5 l^3, SURVEY §8(d) C4 probes)
+    "c4": dict(shape="cube", n=1048576, leaf=256, family="gaussian", length_scale=0.1, shift=2e4, tol=1e-8,
+               s_far=512, s_near=512),
+    # BASELINE configs[4] points on one GPU: the metric config at the tolerance sweep ends
+    "m1_tol6": dict(shape="cube", n=1048576, leaf=256, family="laplace", shift=2e6, tol=1e-6, s_far=512, s_near=512),
+    "m1_tol10": dict(shape="cube", n=1048576, leaf=256, family="laplace", shift=2e6, tol=1e-10, s_far=512,
+                     s_near=512),
+    "m2": dict(shape="cube", n=2097152, leaf=256, family="laplace", shift=4e6, tol=1e-8, s_far=512, s_near=512),
 }
 
 
@@ -80,7 +89,10 @@ def build_problem(pkg, c, on_gpu=True):
     tree = pkg.build_tree(cloud, c["leaf"])
     lists = pkg.build_interaction_lists(tree, 1.0)
     cfg = pkg.BuildConfig(eta=1.0, leaf_max=c["leaf"], tol=c["tol"], s_far=c["s_far"], s_near=c["s_near"], seed=0)
-    kernel = pkg.KernelSpec(family=c["family"], diagonal_shift=c["shift"])
+    if c["family"] == "gaussian":
+        kernel = pkg.GaussianKernelSpec(length_scale=c["length_scale"], diagonal_shift=c["shift"])
+    else:
+        kernel = pkg.KernelSpec(family=c["family"], diagonal_shift=c["shift"])
     return kernel, cloud, tree, lists, cfg
 
 

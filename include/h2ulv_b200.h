@@ -297,7 +297,8 @@ int h2g_basis_finish(const h2g_basis_desc* d_descs, int count, void* stream);
 
 /* ---- kernel matrix blocks ------------------------------------------------------
  * out[a, b] = K(|x_rows[a] - x_cols[b]|) with K = 1/r (laplace) or
- * exp(-decay r)/r (yukawa); out = shift where the two global point ids are
+ * exp(-decay r)/r (yukawa) or exp(-decay r^2) (family 2, the opt-in Gaussian
+ * covariance of BASELINE configs[3], decay = 1/l^2); out = shift where the two global point ids are
  * equal (kernels.gen_block, kernels.py:46-64).  Coincident distinct points
  * set d_coincident[0] = 1 (the host then locates the pair and raises
  * CoincidentPointsError like kernels.py:55-57).

@@ -4,7 +4,8 @@
 // Distances are evaluated without FMA contraction in the same order as
 // scipy's cdist ((dx^2 + dy^2) + dz^2, then a correctly rounded sqrt), and
 // 1/r is an IEEE division, so Laplace entries are bit-identical to the
-// reference's.
+// reference's.  Family 2 is the opt-in Gaussian covariance exp(-r^2 / l^2)
+// (BASELINE configs[3]; not a reference family).
 #include "common.cuh"
 
 namespace h2g {
@@ -41,6 +42,8 @@ __global__ void __launch_bounds__(256) kernel_block_kernel(const h2g_kblock_desc
         v = __longlong_as_double(0x7ff8000000000000LL);
       } else if (family == 0) {
         v = __ddiv_rn(1.0, d);
+      } else if (family == 2) {       // gaussian covariance exp(-(r/l)^2), decay = 1/l^2
+        v = exp(-__dmul_rn(__dmul_rn(d, d), decay));   // host: exp(-(r * r) / l^2)
       } else {
         v = __ddiv_rn(exp(-decay * d), d);
       }
@@ -57,7 +60,7 @@ extern "C" int h2g_kernel_blocks(const h2g_kblock_desc* d_descs, const int32_t* 
   if (total_tiles <= 0) return H2G_OK;
   if (!d_descs || !d_tile_map || !d_points || !d_coincident)
     return h2g_set_error(H2G_EINVAL, "h2g_kernel_blocks: null argument");
-  if (family != 0 && family != 1) return h2g_set_error(H2G_EINVAL, "h2g_kernel_blocks: unknown family %d", family);
+  if (family < 0 || family > 2) return h2g_set_error(H2G_EINVAL, "h2g_kernel_blocks: unknown family %d", family);
   h2g::kernel_block_kernel<<<total_tiles, 256, 0, (cudaStream_t)stream>>>(
       d_descs, d_tile_map, d_points, family, shift, decay, (long long*)d_coincident);
   return h2g_check_launch("kernel_blocks");

@@ -266,7 +266,7 @@ def construct(kernel, tree, lists, cfg, cloud, device=None, workers=None):
     pts_dev = torch.from_numpy(np.ascontiguousarray(cloud.points, dtype=np.float64)).to(device)
     flag = torch.zeros(2, dtype=torch.int64, device=device)
     fam = kernels.FAMILY_CODE[kernel.family]
-    shift, decay = float(kernel.diagonal_shift), float(kernel.yukawa_decay)
+    shift, decay = float(kernel.diagonal_shift), float(kernel.device_param)
     prog = Program(device)
     keep = []  # index arrays referenced by the program
 
