@@ -77,6 +77,22 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   const int wm = warp / wn_count, wn = warp % wn_count;
   // a warp tile strictly above the diagonal of a LOWER diagonal tile is never read: skip its math
   const bool upper_warp = (P.flags & H2G_GEMM_LOWER) && tm == tn && wm * C::WM + C::WM <= wn * C::WN;
+  // 8x8 sub-tiles the warp actually needs: inside M x N (ragged edge tiles of variable-size
+  // problems) and, on a LOWER diagonal tile, not strictly above the diagonal.  The others issue
+  // no DMMA, so padding to the 64x64 tile costs loads but not tensor-pipe time.
+  unsigned act = 0;
+  {
+    const bool diag_tile = (P.flags & H2G_GEMM_LOWER) && tm == tn;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int r0 = wm * C::WM + i * 8, c0 = wn * C::WN + j * 8;
+        const bool in = m0 + r0 < P.M && n0 + c0 < P.N;
+        const bool above = diag_tile && r0 + 7 < c0;
+        if (in && !above) act |= 1u << (i * C::NI + j);
+      }
+  }
 
   double acc[C::MI][C::NI][2];
   double* Cp = P.C;  // may alias A (in-place TRSM with N <= 64)
@@ -182,7 +198,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < C::NI; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < C::NI; ++j)
+          if (act & (1u << (i * C::NI + j))) dmma884(acc[i][j], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();

@@ -52,7 +52,7 @@ INT_MAX = 2 ** 31 - 1
 F64 = torch.float64
 # fused per-box partial Cholesky (h2g_chol_box) for levels with at least this many boxes of
 # size <= CHOL_BOX_MAX_N; the panel-step chain otherwise (few large boxes: the upper levels)
-CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "1024"))
+CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 PANEL_ROWS_PER_CTA = 128
 
