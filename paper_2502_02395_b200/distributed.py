@@ -136,52 +136,65 @@ class Comm:
 
 # --------------------------------------------------------------------------- factorization exchanges
 
+def _view(t, off, rows, cols, ld):
+    return t.as_strided((rows, cols), (ld, 1), t.storage_offset() + off)
+
+
 def _exchange_blocks(plan, blocks, phase, level):
     """all_gather of per-rank block exports.
 
-    blocks: list of (owner_rank, flat device tensor, offset, size) — every rank
-    lists the same blocks in the same order; after the call each rank's copy of
-    every block equals its owner's."""
+    blocks: list of (owner_rank, flat device tensor, offset, rows, cols, ld) —
+    strided sub-blocks (only the slabs the receiver reads, e.g. the k x k SS
+    corner of H_i, not all of H_i); every rank lists the same blocks in the
+    same order; after the call each rank's copy of every block equals its
+    owner's."""
     comm = plan.comm
     dev = plan.device
     sizes = np.zeros(comm.world, dtype=np.int64)
-    for own, _, _, sz in blocks:
-        sizes[own] += sz
+    for own, _, _, rows, cols, _ in blocks:
+        sizes[own] += rows * cols
     cap = int(sizes.max())
     if cap == 0:
         return
     send = torch.zeros(cap, dtype=F64, device=dev)
     pos = 0
-    for own, t, off, sz in blocks:
-        if own == comm.rank:
-            send[pos:pos + sz].copy_(t[off:off + sz])
-            pos += sz
+    for own, t, off, rows, cols, ld in blocks:
+        if own == comm.rank and rows * cols:
+            send[pos:pos + rows * cols].view(rows, cols).copy_(_view(t, off, rows, cols, ld))
+            pos += rows * cols
     recv = comm.all_gather(send, phase=phase, level=level)
     cursor = np.zeros(comm.world, dtype=np.int64)
-    for own, t, off, sz in blocks:
+    for own, t, off, rows, cols, ld in blocks:
         c = int(cursor[own])
-        if own != comm.rank:
-            t[off:off + sz].copy_(recv[own][c:c + sz])
-        cursor[own] = c + sz
+        if own != comm.rank and rows * cols:
+            _view(t, off, rows, cols, ld).copy_(recv[own][c:c + rows * cols].view(rows, cols))
+        cursor[own] = c + rows * cols
 
 
 def _halo_v_blocks(plan, l):
+    """V_j (n_j x r_j, the first r_j columns of R_j) of the column boxes of cross-owner near pairs."""
     part, B = plan.part, plan.bufs[l]
     lay = B.lay
     need = sorted({j for (i, j) in lay.off_pairs if part.owner(l, i) != part.owner(l, j)})
-    return [(part.owner(l, j), B.R, int(lay.qoff[j]), int(lay.n[j] * lay.n[j])) for j in need]
+    return [(part.owner(l, j), B.R, int(lay.qoff[j]), int(lay.n[j]), int(lay.r[j]), int(lay.n[j])) for j in need]
 
 
 def _boundary_blocks(plan, l):
+    """The level-L0 Schur blocks the replicated parent level is merged from: the k_i x k_i SS
+    corner of every H_i and the k_i x k_j SS slab of every near T_ij (ulv_factor.py:289-303)."""
     part, B = plan.part, plan.bufs[l]
     lay = B.lay
-    out = [(part.owner(l, i), B.H, int(lay.qoff[i]), int(lay.n[i] * lay.n[i])) for i in range(lay.nb)]
-    out += [(part.owner(l, i), B.T, int(B.toff[(i, j)]), int(lay.n[i] * lay.n[j])) for (i, j) in lay.off_pairs]
+    n, k, r = lay.n, lay.k, lay.r
+    out = [(part.owner(l, i), B.H, int(lay.qoff[i] + r[i] * n[i] + r[i]), int(k[i]), int(k[i]), int(n[i]))
+           for i in range(lay.nb)]
+    out += [(part.owner(l, i), B.T, int(B.toff[(i, j)] + r[i] * n[j] + r[j]), int(k[i]), int(k[j]), int(n[j]))
+            for (i, j) in lay.off_pairs]
     return out
 
 
 def _solve_halo_blocks(plan):
-    """Cross-owner off-diagonal factor blocks, for the column box's owner."""
+    """Cross-owner off-diagonal factor blocks for the column box's owner: lr_off_ij and L(s)_ij
+    (T_ij[:, :r_j]) and the mirror L(s)_ji."""
     part = plan.part
     out = []
     for l, B in sorted(plan.bufs.items(), reverse=True):
@@ -192,8 +205,8 @@ def _solve_halo_blocks(plan):
             oi = part.owner(l, i)
             if oi == part.owner(l, j):
                 continue
-            out.append((oi, B.T, int(B.toff[(i, j)]), int(lay.n[i] * lay.n[j])))
-            out.append((oi, B.LSm, int(B.lsoff[(i, j)]), int(lay.k[j] * lay.r[i])))
+            out.append((oi, B.T, int(B.toff[(i, j)]), int(lay.n[i]), int(lay.r[j]), int(lay.n[j])))
+            out.append((oi, B.LSm, int(B.lsoff[(i, j)]), int(lay.k[j]), int(lay.r[i]), int(lay.r[i])))
     return out
 
 

@@ -28,6 +28,7 @@ import numpy as np
 import scipy.linalg
 import torch
 
+from .trace import ranged
 from . import _native as nat
 from . import dense_core, kernels
 from .basis_qr import LevelQR
@@ -255,6 +256,7 @@ def _skel_global(eff, choice, l, i):
     return eff[(l, i)][c.skeleton]
 
 
+@ranged("h2ulv.construct")
 def construct(kernel, tree, lists, cfg, cloud, device=None, workers=None):
     """Build the H² representation (h2_build.py:170-220); operands end in HBM."""
     nat.lib()

@@ -153,11 +153,8 @@ class Program:
         m64, n64, k64 = arr["M"].astype(np.int64), arr["N"].astype(np.int64), arr["K"].astype(np.int64)
         lower = (arr["flags"] & nat.GEMM_LOWER) != 0
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
-        # DMMA work the tiles issue: 8x8 sub-tiles inside the problem (and on/below the diagonal for
-        # LOWER), K padded to the 16-wide stage
-        m8, n8 = -(-m64 // 8), -(-n64 // 8)
-        sub = np.where(lower, m8 * (m8 + 1) // 2, m8 * n8)
-        ex = int((sub * 2 * 64 * (-(-k64 // 16) * 16)).sum())
+        t = nat.GEMM_TILE[cfg]
+        ex = int((tiles * 2 * t * t * (-(-k64 // 16) * 16)).sum())   # whole t x t tiles, K padded to 16
         self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex)
         return total
 

@@ -42,6 +42,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from .trace import ranged
 from . import _native as nat
 from .dense_core import PhaseFlops
 from .errors import NotPositiveDefiniteError, StructureError
@@ -904,6 +905,7 @@ def _factorize_streamed(h2):
     return dh2, plan
 
 
+@ranged("h2ulv.factorize")
 def factorize(h2, batched=True, retain=False):
     """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
     nat.lib()

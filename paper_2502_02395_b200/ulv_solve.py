@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from .trace import ranged
 from . import _native as nat
 from .program import Program
 
@@ -490,6 +491,7 @@ def _backward(factors, y, mode):
     return x[:, 0] if y.vector else x
 
 
+@ranged("h2ulv.solve")
 def solve(factors, b, mode="parallel"):
     """Solve A x = b with b in the ORIGINAL input order (ulv_solve.py:191-207)."""
     if mode not in ("naive", "parallel"):

@@ -66,14 +66,19 @@ def _exchange_worker(rank, world, port, q):
         comm = Comm.from_env()
         plan = _FakePlan(comm)
         buf = torch.full((40,), -1.0, dtype=torch.float64)
-        # block b (owner b % world) lives at [10 b, 10 b + 7); owners write their id
-        blocks = [(b % world, buf, 10 * b, 7) for b in range(4)]
-        for own, t, off, sz in blocks:
+        # block b (owner b % world): a 2 x 3 slab with leading dimension 5 at offset 10 b
+        # (entries 10b + {0,1,2, 5,6,7}); owners write their id, the gaps stay -1 everywhere
+        blocks = [(b % world, buf, 10 * b, 2, 3, 5) for b in range(4)]
+        want = torch.full((40,), -1.0, dtype=torch.float64)
+        for b in range(4):
+            for e, off in enumerate((0, 1, 2, 5, 6, 7)):
+                want[10 * b + off] = 100.0 * (b % world) + e
+        for own, t, off, rows, cols, ld in blocks:
             if own == rank:
-                t[off:off + sz] = 100.0 * own + torch.arange(sz, dtype=torch.float64)
+                for e, o in enumerate((0, 1, 2, 5, 6, 7)):
+                    t[off + o] = 100.0 * own + e
         _exchange_blocks(plan, blocks, "factor", 0)
-        ok = all(torch.equal(buf[10 * b:10 * b + 7], 100.0 * (b % world) + torch.arange(7, dtype=torch.float64))
-                 for b in range(4))
+        ok = torch.equal(buf, want)
         v = torch.tensor([1.0 + rank], dtype=torch.float64)
         comm.all_reduce_(v)
         q.put((rank, ok, float(v.item()), len(comm.trace)))
