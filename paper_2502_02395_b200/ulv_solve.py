@@ -16,6 +16,7 @@ segments of level l-1 (n_p = k_2p + k_2p+1), so the merge
 `segs[p] = vstack(b_S,2p, b_S,2p+1)` (ulv_solve.py:113) costs nothing.
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -26,6 +27,7 @@ from . import _native as nat
 from .program import Program
 
 F64 = torch.float64
+_XFORM_T = os.environ.get("H2G_SOLVE_XFORM", "1") != "0"   # G1 by h2g_xform_t (1) or the grouped GEMV (0)
 
 
 @dataclass
@@ -227,9 +229,15 @@ class SolvePlan:
             q = fp.dh2.q[l]
             mine = self._mine(l)
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
-            prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), self._p(V["BR"], offR[i]),
-                           self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
-                          for i in range(nb) if mine[i]], w)
+            if not _XFORM_T:
+                prog.gemv([(self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
+                            nat.GEMV_PLUS | nat.GEMV_SPLIT,
+                            [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))])
+                           for i in range(nb) if mine[i]], w)
+            else:
+                prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]),
+                               self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
+                              for i in range(nb) if mine[i]], w)
             if self.mode == "parallel":
                 prog = self._forward_parallel_level(prog, l, V, lay, below)
             else:
