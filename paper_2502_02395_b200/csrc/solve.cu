@@ -212,48 +212,7 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trsv_batched_kernel(const h2g_t
   }
 }
 
-// Basis transform of the forward sweep, [b_R; b_S] = q_full^T seg (_transform_in,
-// ulv_solve.py:33-41): column-sum GEMV with q_full row-major, so thread c of a
-// CTA owns output column c and walks the rows — every load is a coalesced
-// row segment and each thread keeps 8 independent rows in flight; no
-// cross-thread reduction.  One CTA per 128 output columns of a box.
-constexpr int XT_COLS = 128;
-__global__ void __launch_bounds__(XT_COLS) xform_t_kernel(const h2g_xform_desc* __restrict__ descs,
-                                                          const int32_t* __restrict__ tile_map, int w) {
-  const h2g_xform_desc D = descs[tile_map[blockIdx.x]];
-  const int c = (blockIdx.x - D.tile_start) * XT_COLS + threadIdx.x;
-  if (c >= D.n) return;
-  const double* __restrict__ Q = D.Q + c;
-  const double* __restrict__ x = D.x;
-  const int n = D.n, ld = D.ldq;
-  for (int j = 0; j < w; ++j) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int r = 0;
-#pragma unroll 2
-    for (; r + 4 <= n; r += 4) {
-      const double q0 = Q[(size_t)r * ld], q1 = Q[(size_t)(r + 1) * ld];
-      const double q2 = Q[(size_t)(r + 2) * ld], q3 = Q[(size_t)(r + 3) * ld];
-      s0 = fma(q0, __ldg(x + (size_t)r * w + j), s0);
-      s1 = fma(q1, __ldg(x + (size_t)(r + 1) * w + j), s1);
-      s2 = fma(q2, __ldg(x + (size_t)(r + 2) * w + j), s2);
-      s3 = fma(q3, __ldg(x + (size_t)(r + 3) * w + j), s3);
-    }
-    for (; r < n; ++r) s0 = fma(Q[(size_t)r * ld], __ldg(x + (size_t)r * w + j), s0);
-    const double v = (s0 + s1) + (s2 + s3);
-    if (c < D.split) D.y1[(size_t)c * w + j] = v;
-    else D.y2[(size_t)(c - D.split) * w + j] = v;
-  }
-}
-
 }  // namespace h2g
-
-extern "C" int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w,
-                           void* stream) {
-  if (total_tiles <= 0) return H2G_OK;
-  if (!d_descs || !d_tile_map || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_xform_t: bad argument");
-  h2g::xform_t_kernel<<<total_tiles, h2g::XT_COLS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
-  return h2g_check_launch("xform_t");
-}
 
 extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms, int total_chunks,
                                 int w, void* stream) {

@@ -38,7 +38,12 @@ F64 = torch.float64
 
 
 class Partition:
-    """Box ownership over P = 2^L0 ranks (comm_sim.ProcAssignment semantics)."""
+    """Box ownership over P = 2^L0 ranks (comm_sim.ProcAssignment semantics,
+    comm_sim.py:17-37): at a level l >= L0 box i has the single owner
+    i >> (l - L0) (contiguous leaf ranges); at a level l < L0 it is computed by
+    its process group [i * P/2^l, (i+1) * P/2^l) — the replication the
+    reference's simulator assumes (replicated_work, comm_sim.py:151-167), so a
+    rank computes ONE box per replicated level and the root."""
 
     def __init__(self, p, depth):
         if p < 1 or p & (p - 1):
@@ -59,11 +64,45 @@ class Partition:
     def owner(self, l, i):
         return self.group(l, i)[0]
 
+    contributor = owner   # the group member whose copy of a box's blocks enters a sum
+
     def owned_mask(self, l, rank):
+        """Boxes of level l this rank computes (member of their group)."""
         i = np.arange(2 ** l)
         if l < self.L0:
-            return np.ones(2 ** l, dtype=bool)
+            return i == (rank >> (self.L0 - l))
         return (i >> (l - self.L0)) == rank
+
+    def contrib_mask(self, l, rank):
+        """Boxes of level l whose contributor is this rank."""
+        i = np.arange(2 ** l)
+        if l < self.L0:
+            return (i * (self.p >> l)) == rank
+        return (i >> (l - self.L0)) == rank
+
+    def union(self, l, i, j):
+        gi, gj = self.group(l, i), self.group(l, j)
+        return (min(gi[0], gj[0]), max(gi[1], gj[1]))
+
+
+def merge_events(part, lists, kdims, depth):
+    """The factorization's merge AllReduces, a pure function of the structure:
+    one per parent near block (pi >= pj) of every level pl < L0 whose union
+    group spans >= 2 ranks, over that group, 8 d_pi d_pj bytes (the zero-padded
+    contributions of Eq. 34).  Equal to comm_sim.simulate_factor
+    (comm_sim.py:92-106).  kdims: {l: array of ranks k}."""
+    out = []
+    for pl in range(min(depth - 1, part.L0 - 1), -1, -1):
+        k = kdims[pl + 1]
+        for (pi, pj) in sorted(lists.near[pl]):
+            if pi < pj:
+                continue
+            g = part.union(pl, pi, pj)
+            if g[1] - g[0] < 2:
+                continue
+            di, dj = int(k[2 * pi] + k[2 * pi + 1]), int(k[2 * pj] + k[2 * pj + 1])
+            out.append(("factor", pl, "allreduce", g, 8 * di * dj, (pi, pj)))
+    return out
 
 
 @dataclass
@@ -72,6 +111,7 @@ class CommEvent:
     level: int
     kind: str
     bytes: int
+    participants: tuple = None
 
 
 @dataclass
@@ -83,6 +123,7 @@ class Comm:
     group: object = None
     host_staged: bool = False      # gloo: collectives on host copies
     trace: list = field(default_factory=list)
+    groups: dict = field(default_factory=dict)   # (lo, hi) -> process group of ranks [lo, hi)
 
     @classmethod
     def from_env(cls, group=None):
@@ -94,8 +135,39 @@ class Comm:
         return cls(rank=dist.get_rank(group), world=dist.get_world_size(group), group=group,
                    host_staged=(backend != "nccl"))
 
-    def _log(self, phase, level, kind, nbytes):
-        self.trace.append(CommEvent(phase, level, kind, int(nbytes)))
+    def _log(self, phase, level, kind, nbytes, participants=None):
+        self.trace.append(CommEvent(phase, level, kind, int(nbytes),
+                                    participants if participants is not None else (0, self.world)))
+
+    def make_groups(self, ranges):
+        """Create the sub-communicators of the rank ranges [lo, hi) — collectively:
+        every rank calls this with the same list (plan construction is replicated)."""
+        import torch.distributed as dist
+
+        for lo, hi in sorted(set(ranges)):
+            if (lo, hi) in self.groups:
+                continue
+            if lo == 0 and hi == self.world:
+                self.groups[(lo, hi)] = self.group
+            else:
+                self.groups[(lo, hi)] = dist.new_group(ranks=list(range(lo, hi)))
+
+    def group_all_reduce_(self, t, rng, phase="factor", level=-1):
+        """Sum over the ranks [lo, hi); a rank outside the range does nothing."""
+        import torch.distributed as dist
+
+        lo, hi = rng
+        if not (lo <= self.rank < hi):
+            return t
+        self._log(phase, level, "allreduce", t.numel() * t.element_size(), (lo, hi))
+        g = self.groups[(lo, hi)]
+        if self.host_staged:
+            h = t.cpu()
+            dist.all_reduce(h, group=g)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, group=g)
+        return t
 
     def all_gather(self, t, phase="factor", level=-1):
         import torch.distributed as dist
@@ -171,40 +243,42 @@ def _exchange_blocks(plan, blocks, phase, level):
         cursor[own] = c + rows * cols
 
 
+def cross_pairs(part, l, pairs):
+    """Near pairs (i, j) whose boxes are computed by different process groups."""
+    return [(i, j) for (i, j) in pairs if part.group(l, i) != part.group(l, j)]
+
+
 def _halo_v_blocks(plan, l):
-    """V_j (n_j x r_j, the first r_j columns of R_j) of the column boxes of cross-owner near pairs."""
+    """V_j (n_j x r_j, the first r_j columns of R_j) of the column boxes of cross-group near pairs
+    (the row box's group forms T_ij = Q_i^T A_ij [V_j | q_skel_j]), from j's contributor."""
     part, B = plan.part, plan.bufs[l]
     lay = B.lay
-    need = sorted({j for (i, j) in lay.off_pairs if part.owner(l, i) != part.owner(l, j)})
-    return [(part.owner(l, j), B.R, int(lay.qoff[j]), int(lay.n[j]), int(lay.r[j]), int(lay.n[j])) for j in need]
+    need = sorted({j for (i, j) in cross_pairs(part, l, lay.off_pairs)})
+    return [(part.contributor(l, j), B.R, int(lay.qoff[j]), int(lay.n[j]), int(lay.r[j]), int(lay.n[j]))
+            for j in need]
 
 
-def _boundary_blocks(plan, l):
-    """The level-L0 Schur blocks the replicated parent level is merged from: the k_i x k_i SS
-    corner of every H_i and the k_i x k_j SS slab of every near T_ij (ulv_factor.py:289-303)."""
-    part, B = plan.part, plan.bufs[l]
-    lay = B.lay
-    n, k, r = lay.n, lay.k, lay.r
-    out = [(part.owner(l, i), B.H, int(lay.qoff[i] + r[i] * n[i] + r[i]), int(k[i]), int(k[i]), int(n[i]))
-           for i in range(lay.nb)]
-    out += [(part.owner(l, i), B.T, int(B.toff[(i, j)] + r[i] * n[j] + r[j]), int(k[i]), int(k[j]), int(n[j]))
-            for (i, j) in lay.off_pairs]
-    return out
+def _merge_allreduce(plan, l):
+    """Merge of level l into the group-computed parent level l - 1: every rank wrote
+    the child blocks it contributes into the zeroed parent buffer; one AllReduce
+    per parent near block over its union group completes it (Eq. 34,
+    comm_sim.simulate_factor)."""
+    comm = plan.comm
+    abuf, aoff, pn = plan.parent_buf[l]
+    for (_, pl, _, g, _, (pi, pj)) in plan.merge_schedule[l]:
+        seg = abuf[aoff[(pi, pj)]: aoff[(pi, pj)] + pn[pi] * pn[pj]]
+        comm.group_all_reduce_(seg, g, phase="factor", level=pl)
 
 
 def _solve_halo_blocks(plan):
-    """Cross-owner off-diagonal factor blocks for the column box's owner: lr_off_ij and L(s)_ij
-    (T_ij[:, :r_j]) and the mirror L(s)_ji."""
+    """Cross-group off-diagonal factor blocks for the column box's group: lr_off_ij and L(s)_ij
+    (T_ij[:, :r_j]) and the mirror L(s)_ji, from the row box's contributor."""
     part = plan.part
     out = []
     for l, B in sorted(plan.bufs.items(), reverse=True):
-        if not plan.distributed_level(l):
-            continue
         lay = B.lay
-        for (i, j) in lay.off_pairs:
-            oi = part.owner(l, i)
-            if oi == part.owner(l, j):
-                continue
+        for (i, j) in cross_pairs(part, l, lay.off_pairs):
+            oi = part.contributor(l, i)
             out.append((oi, B.T, int(B.toff[(i, j)]), int(lay.n[i]), int(lay.r[j]), int(lay.n[j])))
             out.append((oi, B.LSm, int(B.lsoff[(i, j)]), int(lay.k[j]), int(lay.r[i]), int(lay.r[i])))
     return out
@@ -216,8 +290,8 @@ def run_exchange(plan, seg):
         torch.cuda.current_stream(plan.device).synchronize()
     if kind == "halo_v":
         _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l)
-    elif kind == "boundary":
-        _exchange_blocks(plan, _boundary_blocks(plan, l), "factor", l)
+    elif kind == "merge":
+        _merge_allreduce(plan, l)
     elif kind == "solve_halo":
         _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1)
     else:

@@ -212,6 +212,16 @@ class FactorPlan:
         self.generation = 0      # bumped whenever the buffers receive new factors (solve inverses follow)
         self.part = part
         self.comm = comm
+        self.dist = part is not None and part.p > 1
+        self.merge_schedule, self.parent_buf = {}, {}
+        if self.dist and dh2.depth >= 1:
+            from .distributed import merge_events
+
+            kdims = {l: lay.k for l, lay in dh2.levels.items()}
+            for ev in merge_events(part, lists, kdims, dh2.depth):
+                self.merge_schedule.setdefault(ev[1] + 1, []).append(ev)
+            # the merge sub-communicators, created collectively in the same order on every rank
+            comm.make_groups([ev[3] for evs in self.merge_schedule.values() for ev in evs])
         dev = dh2.device
         self.device = dev
         depth = self.depth
@@ -313,8 +323,8 @@ class FactorPlan:
                 prog.role = None
                 B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
                                                                     Qp=qp)
-                if self.distributed_level(l):
-                    # V_j of boxes owned elsewhere but coupled to mine by a near pair
+                if self.dist and self._cross(l, lay):
+                    # V_j of boxes computed by another group but coupled to mine by a near pair
                     prog = self._cut(prog, ("halo_v", l))
                     ev_v = ev_ss = None          # the cut joined every lane
                 # ---- deferred off-diagonal factor blocks (lane 3): read only by the solve
@@ -339,16 +349,20 @@ class FactorPlan:
                 prog.gemm(1, 0, prob)
                 prog.role = None
                 prog.lane = 0
-                if self.distributed_level(l) and not self.distributed_level(l - 1):
-                    # boundary: the parent level is replicated -> every rank needs all SS blocks
-                    prog = self._cut(prog, ("boundary", l))
-                    ev_ss = None
                 # ---- merge into the parent level (or the root)
                 if ev_ss is not None:
                     prog.wait(ev_ss)
-                a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2)
-                merge_ev = prog.event()
-                prog.record(merge_ev)
+                if self.dist and l - 1 < self.part.L0:
+                    # group-computed parent level: each rank writes the child blocks it contributes
+                    # into the zeroed parent blocks; one AllReduce per parent near block over its
+                    # union group completes them (Eq. 34; comm_sim.simulate_factor)
+                    a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2, group=True)
+                    prog = self._cut(prog, ("merge", l))
+                    merge_ev = None
+                else:
+                    a_buf, a_off = self._merge_steps(prog, l, B, lists, dh2)
+                    merge_ev = prog.event()
+                    prog.record(merge_ev)
             d = self._root_d
             self.root_dim = d
             self.root_buf = a_buf
@@ -356,8 +370,8 @@ class FactorPlan:
 
         self.flops = flop_report({l: (B.lay.n, B.lay.k, B.lay.off_pairs) for l, B in self.bufs.items()},
                                  self.root_dim)
-        if self.part is not None and self.part.p > 1 and depth >= 1:
-            # cross-owner off-diagonal factor blocks also go to the column box's owner (solve)
+        if self.dist and depth >= 1 and any(self._cross(l, B.lay) for l, B in self.bufs.items()):
+            # cross-group off-diagonal factor blocks also go to the column box's group (solve)
             prog = self._cut(prog, ("solve_halo", -1))
         self.segments.append(prog.finalize())
         self.audit = self._audit()
@@ -365,11 +379,16 @@ class FactorPlan:
 
     # ------------------------------------------------------------------ distribution hooks
     def mine(self, l):
-        """Boolean mask of the level-l boxes this rank computes."""
+        """Boolean mask of the level-l boxes this rank computes (distributed.Partition)."""
         nb = 2 ** l
-        if self.part is None or not self.distributed_level(l):
+        if not self.dist:
             return np.ones(nb, dtype=bool)
         return self.part.owned_mask(l, self.comm.rank)
+
+    def _cross(self, l, lay):
+        from .distributed import cross_pairs
+
+        return bool(cross_pairs(self.part, l, lay.off_pairs))
 
     def distributed_level(self, l):
         return self.part is not None and self.part.p > 1 and l >= self.part.L0
@@ -396,19 +415,33 @@ class FactorPlan:
         self.root_linv, _, _ = self._partial_cholesky_steps(prog, ptr, 0, np.array([0]), np.array([d]),
                                                             np.array([d]), slot)
 
-    def _merge_steps(self, prog, l, B, lists, dh2):
+    def _merge_steps(self, prog, l, B, lists, dh2, group=False):
+        """Parent near blocks of level l-1 from the child SS blocks / couplings.
+        group=True (distributed, group-computed parent level): only the child blocks
+        this rank contributes are written, into zeroed parent blocks (the merge
+        AllReduce sums them)."""
         lay = B.lay
         n, k, r = lay.n, lay.k, lay.r
         parents = sorted((pi, pj) for (pi, pj) in lists.near[l - 1] if pi >= pj)
         self.merge_pairs[l] = parents
-        pmine = self.mine(l - 1) if l - 1 >= 1 else np.ones(1, dtype=bool)
-        built = [(pi, pj) for (pi, pj) in parents if pmine[pi]]
+        if group:
+            rank, part = self.comm.rank, self.part
+            built = [(pi, pj) for (pi, pj) in parents
+                     if part.union(l - 1, pi, pj)[0] <= rank < part.union(l - 1, pi, pj)[1]]
+        else:
+            pmine = self.mine(l - 1) if l - 1 >= 1 else np.ones(1, dtype=bool)
+            built = [(pi, pj) for (pi, pj) in parents if pmine[pi]]
         pn = {p: int(k[2 * p] + k[2 * p + 1]) for p in range(2 ** (l - 1))}
         aoff, acc = {}, 0
         for (pi, pj) in parents:
             aoff[(pi, pj)] = acc
             acc += pn[pi] * pn[pj]
         abuf = torch.empty(max(acc, 1), dtype=F64, device=self.device)
+        if group:
+            zero = torch.zeros_like(abuf)
+            self._keep.append(zero)
+            prog.memcpy(abuf.data_ptr(), zero.data_ptr(), 8 * abuf.numel())
+            self.parent_buf[l] = (abuf, aoff, pn)
         if l == 1:
             self._root_d = pn[0]
         Hp, Tp, Sp = B.H.data_ptr(), B.T.data_ptr(), dh2.s[l].data_ptr()
@@ -425,6 +458,13 @@ class FactorPlan:
                     co = 0 if b == 0 else int(k[2 * pj])
                     dst = dst0 + 8 * (ro * ldd + co)
                     kci, kcj = int(k[ci]), int(k[cj])
+                    if group:   # exactly one member of the union group contributes each child block
+                        hi_ = max(ci, cj)
+                        near_child = ci == cj or (hi_, min(ci, cj)) in B.toff
+                        who = (self.part.contributor(l, hi_) if near_child
+                               else self.part.union(l - 1, pi, pj)[0])
+                        if who != rank:
+                            continue
                     if ci == cj:
                         src = Hp + 8 * int(qo[ci] + r[ci] * n[ci] + r[ci])
                         descs.append((src, dst, kci, kcj, int(n[ci]), ldd, 2))

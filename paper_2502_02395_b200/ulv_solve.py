@@ -16,7 +16,6 @@ segments of level l-1 (n_p = k_2p + k_2p+1), so the merge
 `segs[p] = vstack(b_S,2p, b_S,2p+1)` (ulv_solve.py:113) costs nothing.
 """
 
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,7 +26,6 @@ from . import _native as nat
 from .program import Program
 
 F64 = torch.float64
-_XFORM_T = os.environ.get("H2G_SOLVE_XFORM", "1") != "0"   # G1 by h2g_xform_t (1) or the grouped GEMV (0)
 
 
 @dataclass
@@ -149,12 +147,14 @@ class SolvePlan:
         return segs
 
     def _mask(self, l, offkey):
-        """0/1 row mask (x w columns) of the owned segments of a level-l vector."""
+        """0/1 row mask (x w columns) of the segments this rank contributes to the sum of a
+        level-l vector (one member per box's process group: the masked all-reduce leaves every
+        rank with the complete vector)."""
         key = (l, offkey)
         if key not in self._masks:
             lay = self.fp.bufs[l].lay
             sizes = {"offR": lay.r, "offS": lay.k, "offX": lay.n}[offkey]
-            mine = self._mine(l)
+            mine = self.fp.part.contrib_mask(l, self.fp.comm.rank)
             m = np.repeat(mine.astype(np.float64), np.asarray(sizes, dtype=np.int64))
             self._masks[key] = torch.from_numpy(np.repeat(m, self.w)).to(self.device)
         return self._masks[key]
@@ -229,21 +229,16 @@ class SolvePlan:
             q = fp.dh2.q[l]
             mine = self._mine(l)
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
-            if not _XFORM_T:
-                prog.gemv([(self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
-                            nat.GEMV_PLUS | nat.GEMV_SPLIT,
-                            [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))])
-                           for i in range(nb) if mine[i]], w)
-            else:
-                prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]),
-                               self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
-                              for i in range(nb) if mine[i]], w)
+            prog.gemv([(self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
+                        nat.GEMV_PLUS | nat.GEMV_SPLIT,
+                        [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))])
+                       for i in range(nb) if mine[i]], w)
             if self.mode == "parallel":
                 prog = self._forward_parallel_level(prog, l, V, lay, below)
             else:
                 self._forward_naive_level(prog, l, V, lay)
-            if self.dist and fp.distributed_level(l) and not fp.distributed_level(l - 1):
-                prog = self._cut(prog, ("BS", l, "offS"))   # the parent level is replicated
+            if self.dist and l - 1 < fp.part.L0:
+                prog = self._cut(prog, ("BS", l, "offS"))   # the parent level is group-computed
             xin = V["BS"]
         d = fp.root_dim
         self._root_solve(prog, self.yroot, xin, 0)
@@ -255,7 +250,7 @@ class SolvePlan:
         offR, offS = V["offR"], V["offS"]
         B = self.fp.bufs[l]
         mine = self._mine(l)
-        dist = self.dist and self.fp.distributed_level(l)
+        dist = self.dist
         # P1  z_i = L_ii^-1 b_R,i
         prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
         prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb) if mine[i]], 0, w)
@@ -332,9 +327,9 @@ class SolvePlan:
             offR, offS, offX = V["offR"], V["offS"], V["offX"]
             B = fp.bufs[l]
             mine = self._mine(l)
-            dist = self.dist and fp.distributed_level(l)
-            if dist and fp.distributed_level(l - 1):
-                prog = self._cut(prog, ("FULL", l - 1, "offX"))   # x_S of neighbours owned elsewhere
+            dist = self.dist
+            if dist and l >= 2:
+                prog = self._cut(prog, ("FULL", l - 1, "offX"))   # x_S of neighbours computed elsewhere
             # B1  y_R,i -= sum_a L(s)_ai^T x_S,a
             src = {}
             for (a, b) in self._ls_keys(lay):
@@ -377,7 +372,7 @@ class SolvePlan:
                 outs.append((self._p(V["FULL"], offX[i]), 0, 0, int(n[i]), 0, nat.GEMV_PLUS, terms))
             prog.gemv(outs, w)
             xs = V["FULL"]
-        if self.dist and depth >= 1 and fp.distributed_level(depth):
+        if self.dist and depth >= 1:
             prog = self._cut(prog, ("FULL", depth, "offX"))     # assemble x on every rank
         return prog
 

@@ -116,8 +116,10 @@ def _gpu_worker(rank, world, port, q, name):
         g = pkg.factorize(h2)
         xg = pkg.solve(g, ref["b"])
         root_err = float(np.abs(f.root - g.root).max())
+        merges = [["factor", e.level, e.kind, list(e.participants), e.bytes] for e in f.comm.trace
+                  if e.phase == "factor" and e.kind == "allreduce"]
         q.put((rank, root_err, float(np.linalg.norm(x - xg) / np.linalg.norm(xg)),
-               float(np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])), len(f.comm.trace)))
+               float(np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])), merges))
     except Exception as e:  # pragma: no cover - surfaced by the assertion below
         q.put((rank, repr(e), None, None, None))
     finally:
@@ -137,9 +139,87 @@ def test_distributed_factor_solve_matches_single_gpu(name, world):
     res = [q.get(timeout=600) for _ in procs]
     for pr in procs:
         pr.join(timeout=60)
-    for rank, root_err, xdiff, xref, ntrace in res:
+    import json
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name][str(world)]["factor"]
+    for rank, root_err, xdiff, xref, merges in res:
         assert not isinstance(root_err, str), root_err
         assert root_err == 0.0          # identical tiles, identical arithmetic
         assert xdiff < 1e-12
         assert xref < 1e-8
-        assert ntrace > 0
+        # the merge AllReduces this rank took part in = the simulator's events containing it (f)4
+        assert merges == [e for e in golden if e[3][0] <= rank < e[3][1]]
+
+
+def _structure(name):
+    import json
+
+    import paper_2502_02395_b200 as pkg
+    meta = json.load(open(os.path.join(ROOT, "tests", "golden", f"{name}.json")))
+    cfg = meta["config"]
+    gen = pkg.gen_uniform_cube if cfg["shape"] == "cube" else pkg.gen_sphere_surface
+    tree = pkg.build_tree(gen(cfg["n"], seed=cfg.get("seed", 0)), cfg["leaf"])
+    lists = pkg.build_interaction_lists(tree, cfg.get("eta", 1.0))
+    kdims = {int(l): np.array([rk[1] for rk in boxes]) for l, boxes in meta["dims"].items()}
+    return tree, lists, kdims
+
+
+@pytest.mark.parametrize("name", ["h2_cube512_rank16", "h2_sphere1024_yukawa_tol", "h2_cube1024_sampled", "c2"])
+def test_merge_allreduces_equal_comm_sim(name):
+    """(f)4: the factorization's collective schedule (distributed.merge_events, the exact
+    list the runtime executes) equals the reference simulator's trace
+    (comm_sim.simulate_factor, golden from tests/golden/make_comm_golden.py): same events,
+    levels, process ranges and bytes, in order."""
+    import json
+
+    from paper_2502_02395_b200.distributed import merge_events
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name]
+    tree, lists, kdims = _structure(name)
+    for p, tr in golden.items():
+        part = Partition(int(p), tree.depth)
+        ours = [[ph, lvl, kind, list(g), nb] for (ph, lvl, kind, g, nb, _) in
+                merge_events(part, lists, kdims, tree.depth)]
+        assert ours == tr["factor"], p
+
+
+def test_group_ownership_matches_reference_replication():
+    """A rank computes one box per replicated level (its group), the owned range below
+    (comm_sim.ProcAssignment.group / replicated_work)."""
+    part = Partition(8, 6)
+    for rank in range(8):
+        for l in range(0, 3):
+            m = part.owned_mask(l, rank)
+            assert m.sum() == 1 and part.group(l, int(np.flatnonzero(m)[0]))[0] <= rank < part.group(
+                l, int(np.flatnonzero(m)[0]))[1]
+            assert part.contrib_mask(l, rank).sum() == (1 if rank % (8 >> l) == 0 else 0)
+        for l in range(3, 7):
+            assert part.owned_mask(l, rank).sum() == 2 ** (l - 3)
+            assert (part.owned_mask(l, rank) == part.contrib_mask(l, rank)).all()
+
+
+def _subgroup_worker(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        comm = Comm.from_env()
+        comm.make_groups([(0, 2), (2, 4), (0, 4), (1, 3)])
+        t = torch.full((3,), float(rank + 1), dtype=torch.float64)
+        comm.group_all_reduce_(t, (0, 2) if rank < 2 else (2, 4))
+        u = torch.full((2,), float(rank), dtype=torch.float64)
+        comm.group_all_reduce_(u, (1, 3))
+        q.put((rank, t.tolist(), u.tolist(), [(e.kind, e.participants, e.bytes) for e in comm.trace]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_subgroup_allreduce_gloo_world4():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_subgroup_worker, args=(r, 4, port, q)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert [r[1][0] for r in res] == [3.0, 3.0, 7.0, 7.0]
+    assert [r[2][0] for r in res] == [0.0, 3.0, 3.0, 3.0]          # rank 0, 3 outside (1, 3)
+    assert res[1][3] == [("allreduce", (0, 2), 24), ("allreduce", (1, 3), 16)]
