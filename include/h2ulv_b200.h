@@ -20,7 +20,7 @@
  *   - every function returns 0 on success or a nonzero H2G_E* code; the
  *     message is available from h2g_last_error().  No exception crosses the
  *     ABI.  Numerical breakdown (non-positive pivot) is reported through
- *     the device array `d_npd`, see h2g_panel_potrf.
+ *     the device array `d_npd`, see h2g_chol_panel.
  */
 #ifndef H2ULV_B200_H
 #define H2ULV_B200_H
@@ -43,8 +43,8 @@ enum {
 /* ---- grouped GEMM ---------------------------------------------------------
  * C = alpha * op(A) * op(B) + beta * C  for every problem of the group.
  * op(A) is M x K, op(B) is K x N.  trans_a / trans_b and the tile shape are
- * uniform for the launch: tile_cfg 0 = 64x64 tiles (128 threads), 1 =
- * 128x128 tiles (256 threads).  flags bit 0 (H2G_GEMM_LOWER, requires
+ * uniform for the launch: tile_cfg 2 = 64x64 tiles at 4 CTAs/SM, 7 = 64x64
+ * tiles at 3 CTAs/SM (K <= 64 updates), 9 = 32x32 tiles (ragged problems).  flags bit 0 (H2G_GEMM_LOWER, requires
  * M == N) computes only the output tiles on or below the diagonal
  * (SYRK-style Schur updates).  C may alias A when N fits one tile (the
  * in-place TRSM X <- X Linv^T).
@@ -69,37 +69,14 @@ int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg); /* tiles one problem 
 int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
                      const int32_t* d_tile_map, int total_tiles, void* stream);
 
-/* ---- diagonal block of a panel of the partial (ULV) Cholesky ---------------
- * One CTA per descriptor (box): factor the b x b diagonal block
- * H[p:p+b, p:p+b] (b <= 64) in place (lower Cholesky) and write its inverse
- * L_pp^-1 into the 64 x 64 scratch block `Linv` (ld ldl; zero padded).  The
- * host program follows it with two h2g_gemm_grouped launches (NT):
- *   TRSM  X <- X * Linv^T in place for X = H[p+b:n, p:p+b] and R[0:n, p:p+b]
- *   TRAIL H[p+b:, p+b:] -= X X^T (H2G_GEMM_LOWER), R[:, p+b:r] -= V_P L^T
- * which together are the right-looking partial Cholesky of the sparsified
- * diagonal block yielding L(r)_ii, L(s)_ii, V_i and the single Schur update
- * of SS_ii in ONE pass over H (ulv_factor.py:217-241 = factor_diag,
- * ulv_factor.py:78-84).  A pivot that is not > 0 (or NaN) at column p+j
- * records atomicMin(&d_npd[npd_slot], p+j) — the pivot index dpotrf's
- * info-1 reports (dense_core.py:60-63).
- */
-typedef struct h2g_panel_desc {
-  double* H;
-  double* Linv;       /* 64 x 64 scratch output */
-  int32_t ldh, ldl;
-  int32_t p, b;       /* panel start column and width (1..64) */
-  int32_t npd_slot;   /* index into d_npd */
-  int32_t pad_;
-} h2g_panel_desc;
-
-int h2g_panel_potrf(const h2g_panel_desc* d_descs, int count, int32_t* d_npd, void* stream);
-
 /* ---- panel step of the partial (ULV) Cholesky --------------------------------
  * For panel q (columns p = 64q .. p+b-1) of every box:
  *   kernel 1, one CTA per descriptor: apply the previous panel's update
  *      (columns p-64 .. p-1, final L; nothing when p == 0) to the diagonal
  *      block, factor it: L_pp -> H, L_pp^-1 -> the 64 x 64 block `Linv`,
- *      pivot status -> d_npd exactly like h2g_panel_potrf;
+ *      pivot status: a pivot that is not > 0 (or NaN) at column p+j records
+ *      atomicMin(&d_npd[npd_slot], p+j) — the pivot dpotrf reports as info-1
+ *      (dense_core.py:60-63);
  *   kernel 2, one CTA per 64-row chunk of the rows below the panel: apply
  *      the previous panel's update to the chunk rows, then X <- X L_pp^-T.
  * The update of the columns >= p+b+64 by the previous panel (REST) is left
@@ -242,7 +219,7 @@ int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term
 /* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
  * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
  * leading dimension ldl, Linv the inverses of its 64 x 64 diagonal blocks
- * (written by h2g_panel_potrf, 64*64 doubles per block, block q at
+ * (h2g_tri_inv / h2g_chol_panel layout, 64*64 doubles per block, block q at
  * Linv + q*4096) (dense_core.tri_solve, dense_core.py:69-81).
  */
 typedef struct h2g_trsv_desc {
@@ -355,7 +332,7 @@ enum {
   H2G_STEP_GEMM_NT = 1,
   H2G_STEP_GEMM_TN = 2,
   H2G_STEP_GEMM_TT = 3,
-  H2G_STEP_PANEL = 4,
+  /* 4: retired (the stand-alone diagonal-block step of round 1) */
   H2G_STEP_COPY = 5,
   H2G_STEP_MEMCPY = 6,   /* descs = dst, map = src (bytes in count) */
   H2G_STEP_QR_PANEL = 7,

@@ -43,8 +43,6 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
       int k = s.kind - H2G_STEP_GEMM_NN;
       return h2g_gemm_grouped(k >> 1, k & 1, s.arg, (const h2g_gemm_problem*)s.descs, s.map, s.grid, st);
     }
-    case H2G_STEP_PANEL:
-      return h2g_panel_potrf((const h2g_panel_desc*)s.descs, s.count, s.npd, st);
     case H2G_STEP_COPY:
       return h2g_block_copy((const h2g_copy_desc*)s.descs, s.map, s.grid, st);
     case H2G_STEP_MEMCPY: {

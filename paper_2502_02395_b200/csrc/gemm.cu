@@ -3,10 +3,9 @@
 // One CTA computes one BMxBN tile of one problem; the tile -> problem map is
 // precomputed on the host so a level's whole phase (every box or every near
 // pair, all different sizes) is ONE launch with no padding beyond the tile
-// edge.  Two tile shapes:
-//   cfg 0: 64x64,  4 warps (32x32 warp tiles) — small / thin problems;
-//   cfg 1: 128x128, 8 warps (64x32 warp tiles) — the n >= 128 transforms.
-// Operands are staged global -> shared with 3-stage cp.async; the smem layout
+// edge.  Tile shapes: 64x64 with 4 warps (32x32 warp tiles; cfg 2 at 4 CTAs/SM,
+// cfg 7 at 3 CTAs/SM) and 32x32 (cfg 9) for ragged small problems.
+// Operands are staged global -> shared with 2-stage cp.async; the smem layout
 // per operand follows its transpose so both the global reads (coalesced
 // along the contiguous axis) and the fragment reads (stride = 4 mod 16
 // doubles: bank-conflict free) are clean.  With beta != 0 the C tile is read
@@ -35,13 +34,11 @@ struct GemmCfg {
   static constexpr int SMEM = STAGES * (A_DBL + B_DBL) * 8;
 };
 
-using Cfg64 = GemmCfg<64, 64, 2, 2, 1, 3>;      // 3 CTAs/SM (smem-bound), 3 stages
-using Cfg128 = GemmCfg<128, 128, 2, 4, 1, 3>;
-using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // 4 CTAs/SM, <= 128 registers, 2 stages
-using Cfg64k3 = GemmCfg<64, 64, 2, 2, 3, 3>;    // 3 CTAs/SM, 3 stages (m16n8k16 path)
-using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // experiment: 3 CTAs/SM (170 registers), 2 stages
-using Cfg64m2 = GemmCfg<64, 64, 2, 2, 2, 3>;    // experiment: 2 CTAs/SM (255 registers), 3 stages
-using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // small / ragged problems: 32x32 tiles, 6 CTAs/SM
+// The three configurations the planner chooses from (program.choose_tile_cfg; tile shapes,
+// stage counts and the m16n8k16 variant measured in profiles/r01_gemm_tile_configs*.jsonl):
+using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // cfg 2: 4 CTAs/SM, <= 128 registers, 2 stages (transforms)
+using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // cfg 7: 3 CTAs/SM (170 registers), 2 stages (K <= 64 updates)
+using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // cfg 9: small / ragged problems, 32x32 tiles, 6 CTAs/SM
 
 template <class C, bool TA, bool TB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
@@ -244,186 +241,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
 }
 
 template <class C, bool TA, bool TB>
-__global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_k16_kernel(const h2g_gemm_problem* __restrict__ probs,
-                                                                      const int32_t* __restrict__ tile_map) {
-  static_assert(C::WM == 32 && C::WN == 32, "k16 path: 32x32 warp tiles");
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + C::STAGES * C::A_DBL;
-  constexpr int tBM = C::TBM, tBN = C::TBN, wn_count = C::NWARP_N;
-
-  const int tile = blockIdx.x;
-  const int pi = tile_map[tile];
-  const h2g_gemm_problem P = probs[pi];
-  int t = tile - P.tile_start;
-  int tm, tn;
-  if (P.flags & H2G_GEMM_LOWER) {
-    const int i = tri_row(t);
-    tm = i;
-    tn = t - i * (i + 1) / 2;
-  } else {
-    int ntn = (P.N + tBN - 1) / tBN;
-    tm = t / ntn;
-    tn = t - tm * ntn;
-  }
-  const int m0 = tm * tBM, n0 = tn * tBN;
-  const int M = P.M, N = P.N, K = P.K;
-  const double* __restrict__ A = P.A;
-  const double* __restrict__ B = P.B;
-  const int lda = P.lda, ldb = P.ldb;
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  const int wm = warp / wn_count, wn = warp % wn_count;
-
-  double acc[2][4][4];
-  double* Cp = P.C;
-  const int ldc = P.ldc;
-  const double alpha = P.alpha, beta = P.beta;
-  const int cmode = (beta == 0.0 || alpha == 0.0) ? 0 : beta == alpha ? 1 : beta == -alpha ? 2 : 3;
-  const double cscale = cmode == 3 ? beta / alpha : 1.0;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int row = m0 + wm * 32 + i * 16 + g + 8 * (e >> 1);
-        const int col = n0 + wn * 32 + j * 8 + 2 * tq + (e & 1);
-        double v = 0.0;
-        if (cmode && row < M && col < N) {
-          v = Cp[(size_t)row * ldc + col];
-          v = cmode == 1 ? v : cmode == 2 ? neg_int(v) : cscale * v;
-        }
-        acc[i][j][e] = v;
-      }
-
-  auto load_stage = [&](int stage, int k0) {
-    double* as = As + stage * C::A_DBL;
-    double* bs = Bs + stage * C::B_DBL;
-#pragma unroll
-    for (int jj = 0; jj < (tBM * BK) / C::THREADS; ++jj) {
-      int idx = tid + jj * C::THREADS;
-      if (!TA) {
-        int m = idx / BK, k = idx % BK;
-        int gm = m0 + m, gk = k0 + k;
-        bool v = gm < M && gk < K;
-        cp_async8(as + m * C::S_MK + k, v ? A + (size_t)gm * lda + gk : A, v);
-      } else {
-        int k = idx / tBM, m = idx % tBM;
-        int gm = m0 + m, gk = k0 + k;
-        bool v = gm < M && gk < K;
-        cp_async8(as + k * C::SA_KM + m, v ? A + (size_t)gk * lda + gm : A, v);
-      }
-    }
-#pragma unroll
-    for (int jj = 0; jj < (tBN * BK) / C::THREADS; ++jj) {
-      int idx = tid + jj * C::THREADS;
-      if (!TB) {
-        int k = idx / tBN, n = idx % tBN;
-        int gn = n0 + n, gk = k0 + k;
-        bool v = gn < N && gk < K;
-        cp_async8(bs + k * C::SB_KN + n, v ? B + (size_t)gk * ldb + gn : B, v);
-      } else {
-        int n = idx / BK, k = idx % BK;
-        int gn = n0 + n, gk = k0 + k;
-        bool v = gn < N && gk < K;
-        cp_async8(bs + n * C::S_MK + k, v ? B + (size_t)gn * ldb + gk : B, v);
-      }
-    }
-  };
-
-  const int KT = (K + BK - 1) / BK;
-#pragma unroll
-  for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s * BK);
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<C::STAGES - 2>();
-    __syncthreads();
-    {
-      int nk = kt + C::STAGES - 1;
-      if (nk < KT) load_stage(nk % C::STAGES, nk * BK);
-      cp_async_commit();
-    }
-    const double* as = As + (kt % C::STAGES) * C::A_DBL;
-    const double* bs = Bs + (kt % C::STAGES) * C::B_DBL;
-    double af[2][8], bf[4][4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int m = wm * 32 + i * 16 + g + 8 * (e & 1), k = tq + 4 * (e >> 1);
-        af[i][e] = TA ? as[k * C::SA_KM + m] : as[m * C::S_MK + k];
-      }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int n = wn * 32 + j * 8 + g, k = tq + 4 * e;
-        bf[j][e] = TB ? bs[n * C::S_MK + k] : bs[k * C::SB_KN + n];
-      }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma16816(acc[i][j], af[i], bf[j]);
-  }
-  cp_async_wait<0>();
-
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = m0 + wm * 32 + i * 16 + g + 8 * h;
-      if (row >= M) continue;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * tq;
-        double* cp = Cp + (size_t)row * ldc + col;
-        if (alpha == 0.0) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (col + e < N) cp[e] = beta * cp[e];
-          continue;
-        }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double a = acc[i][j][2 * h + e];
-          if (col + e < N) cp[e] = alpha == 1.0 ? a : alpha == -1.0 ? neg_int(a) : alpha * a;
-        }
-      }
-    }
-}
-
-template <class C, bool TA, bool TB>
-static int launch_gemm_k16(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_grouped_k16_kernel<C, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
-  gemm_grouped_k16_kernel<C, TA, TB><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map);
-  return h2g_check_launch("gemm_grouped_k16");
-}
-
-template <class C>
-static int dispatch_k16(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles,
-                        cudaStream_t s) {
-  if (!trans_a && !trans_b) return launch_gemm_k16<C, false, false>(d_probs, d_map, tiles, s);
-  if (!trans_a && trans_b) return launch_gemm_k16<C, false, true>(d_probs, d_map, tiles, s);
-  if (trans_a && !trans_b) return launch_gemm_k16<C, true, false>(d_probs, d_map, tiles, s);
-  return launch_gemm_k16<C, true, true>(d_probs, d_map, tiles, s);
-}
-
-template <class C, bool TA, bool TB>
 static int launch_gemm(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static int attr_dev = -1;   // cudaFuncSetAttribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
     cudaFuncSetAttribute(gemm_grouped_kernel<C, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
+    attr_dev = dev;
   }
   gemm_grouped_kernel<C, TA, TB><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map);
   return h2g_check_launch("gemm_grouped");
@@ -442,7 +266,7 @@ static int dispatch(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, c
 
 extern "C" int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg) {
   if (M <= 0 || N <= 0) return 0;
-  const int T = tile_cfg == 1 ? 128 : tile_cfg == 9 ? 32 : 64;   // cfg 9: 32x32, the others 64x64
+  const int T = tile_cfg == 9 ? 32 : 64;   // cfg 9: 32x32 tiles, cfg 2 / 7: 64x64
   if (flags & H2G_GEMM_LOWER) {
     int t = (M + T - 1) / T;
     return t * (t + 1) / 2;
@@ -455,14 +279,8 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   if (total_tiles <= 0) return H2G_OK;
   if (!d_probs || !d_tile_map) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: null descriptor");
   cudaStream_t s = (cudaStream_t)stream;
-  if (tile_cfg == 1) return h2g::dispatch<h2g::Cfg128>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 2) return h2g::dispatch<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  if (tile_cfg == 3) return h2g::dispatch_k16<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  if (tile_cfg == 4) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  if (tile_cfg == 6) return h2g::dispatch_k16<h2g::Cfg64k3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 7) return h2g::dispatch<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  if (tile_cfg == 8) return h2g::dispatch<h2g::Cfg64m2>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 9) return h2g::dispatch<h2g::Cfg32>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  if (tile_cfg != 0) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d", tile_cfg);
-  return h2g::dispatch<h2g::Cfg64>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d (2, 7, 9)", tile_cfg);
 }

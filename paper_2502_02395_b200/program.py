@@ -17,7 +17,7 @@ import torch
 from . import _native as nat
 
 
-def gemm_tiles(m, n, flags=0, cfg=0):
+def gemm_tiles(m, n, flags=0, cfg=2):
     if m <= 0 or n <= 0:
         return 0
     t = nat.GEMM_TILE[cfg]
@@ -157,18 +157,6 @@ class Program:
         ex = int((tiles * 2 * t * t * (-(-k64 // 16) * 16)).sum())   # whole t x t tiles, K padded to 16
         self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex)
         return total
-
-    def panel(self, descs, npd_ptr):
-        """descs: list of (H, Linv, ldh, ldl, p, b, npd_slot)."""
-        if not descs:
-            return 0
-        arr = np.zeros(len(descs), dtype=nat.PANEL_DT)
-        for name, col in zip(("H", "Linv", "ldh", "ldl", "p", "b", "npd_slot"), zip(*descs)):
-            arr[name] = col
-        b64 = arr["b"].astype(np.int64)
-        self._add(nat.STEP["PANEL"], len(descs), len(descs), self._blob(arr), npd=npd_ptr,
-                  flops=int((b64 ** 3 // 3 + b64 ** 3 // 3).sum()))
-        return len(descs)
 
     def chol_panel(self, descs, npd_ptr):
         """descs: list of (H, Linv, ldh, ldl, n, p, b, npd_slot): one diag CTA per box plus one
