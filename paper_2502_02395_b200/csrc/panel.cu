@@ -967,14 +967,18 @@ extern "C" int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count
   if (count <= 0) return H2G_OK;
   if (!d_descs || !d_npd || (total_tiles > 0 && !d_tile_map))
     return h2g_set_error(H2G_EINVAL, "h2g_chol_panel: null argument");
-  static bool attr = false;
-  if (!attr) {
+  // function attributes are per device; so is the SM count (the current device, not device 0)
+  static int attr_dev = -1, sms = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
     cudaFuncSetAttribute(h2g::chol_diag_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
     cudaFuncSetAttribute(h2g::chol_diag_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::DIAG_SMEM);
     cudaFuncSetAttribute(h2g::chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::RW_SMEM);
     cudaFuncSetAttribute(h2g::chol_panel_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)h2g::FUSED_SMEM);
-    attr = true;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_dev = dev;
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (d_sync && total_tiles > 0 && count <= h2g_chol_panel_fused_max()) {
@@ -983,8 +987,6 @@ extern "C" int h2g_chol_panel_sync(const h2g_chol_panel_desc* d_descs, int count
     return h2g_check_launch("chol_panel_fused");
   }
   // many boxes: the 4-warp variant fits 3 CTAs per SM (throughput); few boxes: 8 warps (latency)
-  static int sms = 0;
-  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   if (count >= 2 * sms) h2g::chol_diag_kernel<4><<<count, 128, h2g::DIAG_SMEM, st>>>(d_descs, d_npd);
   else h2g::chol_diag_kernel<8><<<count, 256, h2g::DIAG_SMEM, st>>>(d_descs, d_npd);
   int rc = h2g_check_launch("chol_diag");
@@ -1010,10 +1012,12 @@ extern "C" int h2g_chol_box(const h2g_cholbox_desc* d_descs, int count, int32_t*
 extern "C" int h2g_trsm_rows(const h2g_rows_desc* d_descs, const int32_t* d_tile_map, int total_tiles, void* stream) {
   if (total_tiles <= 0) return H2G_OK;
   if (!d_descs || !d_tile_map) return h2g_set_error(H2G_EINVAL, "h2g_trsm_rows: null argument");
-  static bool attr = false;
-  if (!attr) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
     cudaFuncSetAttribute(h2g::trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h2g::TS_SMEM);
-    attr = true;
+    attr_dev = dev;
   }
   h2g::trsm_rows_kernel<<<total_tiles, h2g::RW_THREADS, h2g::TS_SMEM, (cudaStream_t)stream>>>(d_descs, d_tile_map);
   return h2g_check_launch("trsm_rows");

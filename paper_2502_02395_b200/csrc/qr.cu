@@ -184,10 +184,13 @@ extern "C" int h2g_qr_panel(const h2g_qr_panel_desc* d_descs, int count, int max
   // panels up to ~780 rows are factored in shared memory (one global read / write of the panel)
   const size_t smem = (size_t)max_rows * (h2g::QB + 1) * sizeof(double);
   if (max_rows > 0 && smem <= 200 * 1024) {
-    static size_t attr = 0;
-    if (smem > attr) {
+    static size_t attr[64] = {};   // per device (function attributes are per device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 63;
+    if (smem > attr[dev]) {
       cudaFuncSetAttribute(h2g::qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
+      attr[dev] = smem;
     }
     h2g::qr_panel_kernel<true><<<count, h2g::QR_THREADS, smem, (cudaStream_t)stream>>>(d_descs);
   } else {

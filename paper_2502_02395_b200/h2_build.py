@@ -258,9 +258,17 @@ def _skel_global(eff, choice, l, i):
 
 @ranged("h2ulv.construct")
 def construct(kernel, tree, lists, cfg, cloud, device=None, workers=None):
-    """Build the H² representation (h2_build.py:170-220); operands end in HBM."""
+    """Build the H² representation (h2_build.py:170-220); operands end in HBM on
+    `device` (default: the current CUDA device), every launch bound to it."""
     nat.lib()
     device = torch.device(device or "cuda")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(device):
+        return _construct(kernel, tree, lists, cfg, cloud, device, workers)
+
+
+def _construct(kernel, tree, lists, cfg, cloud, device, workers):
     workers = workers or min(32, os.cpu_count() or 1)
     h2 = H2Matrix(tree=tree, lists=lists, kernel=kernel, cloud=cloud, config=cfg)
     h2.build_flops.setdefault("prefactor", 0)

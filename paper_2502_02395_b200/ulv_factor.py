@@ -947,8 +947,15 @@ def _factorize_streamed(h2):
 
 @ranged("h2ulv.factorize")
 def factorize(h2, batched=True, retain=False):
-    """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154."""
+    """Factor the hierarchy on the GPU; same contract as ulv_factor.py:154.  Runs on
+    the device holding a GPU-built H² (else the current device)."""
     nat.lib()
+    own = getattr(h2, "_device", None)
+    with torch.cuda.device(own.device if own is not None else torch.cuda.current_device()):
+        return _factorize(h2, retain)
+
+
+def _factorize(h2, retain):
     if getattr(h2, "_device", None) is None and h2.tree.depth > 0:
         dh2, plan = _factorize_streamed(h2)
     else:

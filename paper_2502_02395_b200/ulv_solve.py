@@ -504,6 +504,11 @@ def solve(factors, b, mode="parallel"):
     vector = bm.ndim == 1
     bm = bm.reshape(factors.h2.count, -1)
     sp = _plan_for(factors, bm.shape[1], mode)
+    with torch.cuda.device(sp.device):
+        return _solve_on(factors, sp, bm, vector)
+
+
+def _solve_on(factors, sp, bm, vector):
     dev = sp.device
     perm = factors.__dict__.get("_perm_dev")
     if perm is None:
