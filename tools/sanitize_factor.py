@@ -1,0 +1,43 @@
+"""One small factorization + solve run EAGERLY (no CUDA graph) for compute-sanitizer:
+  compute-sanitizer --tool {memcheck,racecheck,synccheck} python tools/sanitize_factor.py [box]
+C1-sized problem (N = 4096, 16 leaves: the one-launch fused panel step with its
+ticket / flag synchronisation runs at every level); with `box` the fused per-box
+Cholesky (h2g_chol_box) is forced on every level."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2502_02395_b200 as pkg
+from paper_2502_02395_b200 import ulv_factor
+from paper_2502_02395_b200.program import Program
+from paper_2502_02395_b200.ulv_solve import SolvePlan
+
+if "box" in sys.argv[1:]:
+    ulv_factor.CHOL_BOX_MIN = 1
+cloud = pkg.gen_uniform_cube(4096, seed=0)
+tree = pkg.build_tree(cloud, 256)
+lists = pkg.build_interaction_lists(tree, 1.0)
+cfg = pkg.BuildConfig(eta=1.0, leaf_max=256, tol=1e-8, s_far=256, s_near=256)
+h2 = pkg.construct(pkg.KernelSpec(family="laplace", diagonal_shift=1e3), tree, lists, cfg, cloud)
+plan = ulv_factor.FactorPlan(h2._device, lists)
+for _ in range(2):                       # twice: the sync words must be left clean
+    for seg in plan.segments:
+        seg.run()
+torch.cuda.synchronize()
+plan.check_pivots()
+f = ulv_factor.factors_from_plan(h2, plan)
+sp = SolvePlan(plan, 1, "parallel")
+b = np.random.default_rng(1).standard_normal(cloud.count)
+sp.xin[:cloud.count].copy_(torch.from_numpy(b[cloud.perm]))
+sp.prepare.run()
+for seg in sp.fwd_segments + sp.bwd_segments:
+    if isinstance(seg, Program):
+        seg.run()
+torch.cuda.synchronize()
+x = np.empty_like(b)
+x[cloud.perm] = sp.output[:cloud.count].cpu().numpy()
+from oracle import h2ulv_oracle as orc  # noqa: E402  (checker only)
+print("residual", orc.residual(h2, x, b))
