@@ -216,6 +216,25 @@ typedef struct h2g_gemv_out {
 int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
                      int total_chunks, int w, void* stream);
 
+/* h2g_xform_t: [y1; y2] = Q^T x for every box (Q n x n row-major, ld ldq;
+ * x n x w, ld w; rows [0, split) of the result -> y1, rows [split, n) -> y2):
+ * the basis transform of the forward sweep (_transform_in,
+ * ulv_solve.py:33-41).  One CTA per 128 output columns of a box (d_tile_map[t]
+ * = descriptor of CTA t, tile_start = its first CTA); the rows are split over
+ * the CTA's warps.  vec16 != 0 promises every Q row start 16-byte aligned
+ * (even ldq, aligned Q) and selects 16-byte loads.
+ */
+typedef struct h2g_xform_desc {
+  const double* Q;
+  const double* x;
+  double* y1;
+  double* y2;
+  int32_t n, split, ldq, tile_start;
+} h2g_xform_desc;
+
+int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w, int vec16,
+                void* stream);
+
 /* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
  * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
  * leading dimension ldl, Linv the inverses of its 64 x 64 diagonal blocks
@@ -345,6 +364,7 @@ enum {
   H2G_STEP_SYMCHECK = 15,   /* descs = symcheck descs; aux = device output (2 x count u64) */
   H2G_STEP_TRIINV = 16,     /* descs/map = triinv descs/tile map; npd = status */
   H2G_STEP_CHOL_BOX = 17,   /* descs = cholbox descs; npd = status */
+  H2G_STEP_XFORM_T = 18,    /* descs/map = xform descs/tile map; arg = w; count < 0: 16-byte loads */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

@@ -11,6 +11,13 @@ namespace h2g {
 constexpr int GV_THREADS = 512;
 constexpr int GV_CHUNK = 64;    // output rows per CTA (small: many CTAs for memory-level parallelism)
 constexpr int GV_W = 4;         // RHS columns per pass
+#ifndef H2G_GV_MINB
+#define H2G_GV_MINB 4           // CTAs per SM the GEMV / TRSV are compiled for (4: 32 registers)
+#endif
+#ifndef H2G_GV_UNROLL
+#define H2G_GV_UNROLL 4         // rows of a transposed operand in flight per warp
+#endif
+constexpr int GV_UNROLL = H2G_GV_UNROLL;
 
 __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) {
   int lo = 0, hi = n - 1;
@@ -22,7 +29,7 @@ __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) 
 }
 
 // y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t
-__global__ void __launch_bounds__(GV_THREADS, 4) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
+__global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
                                                                   const h2g_gemv_term* __restrict__ terms, int w) {
   __shared__ double acc[GV_CHUNK * GV_W];
   __shared__ double red[GV_THREADS / 32][GV_CHUNK];
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(GV_THREADS, 4) gemv_grouped_kernel(const h2g_g
           double s[GV_CHUNK / 32];
 #pragma unroll
           for (int t = 0; t < GV_CHUNK / 32; ++t) s[t] = 0.0;
-#pragma unroll 4
+#pragma unroll GV_UNROLL
           for (int c = warp; c < K; c += NW) {
             const double xv = x[(size_t)c * w + j0 + j];
             const double* arow = A + (size_t)c * lda + r0;
@@ -117,7 +124,7 @@ constexpr int TB = 64;
 constexpr int TR_THREADS = 512;
 constexpr int TR_WARPS = TR_THREADS / 32;
 constexpr int TR_RPW = TB / TR_WARPS;   // rows per warp in the forward GEMV (4)
-__global__ void __launch_bounds__(TR_THREADS, 4) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
+__global__ void __launch_bounds__(TR_THREADS, H2G_GV_MINB) trsv_batched_kernel(const h2g_trsv_desc* __restrict__ descs, int trans,
                                                                   int w) {
   __shared__ double t[TB];
   __shared__ double red[TR_WARPS][TB];
@@ -212,7 +219,71 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trsv_batched_kernel(const h2g_t
   }
 }
 
+// Basis transform of the forward sweep, [b_R; b_S] = q_full^T seg (_transform_in,
+// ulv_solve.py:33-41), as a column-chunked GEMV: a CTA owns 128 output
+// columns of one box (lane l: columns 4l..4l+3 of the chunk, two 16-byte
+// loads per row), its 8 warps split the n rows (4 rows in flight each) and
+// reduce through shared memory once at the end.  Every load is part of a
+// 1 KB coalesced row segment, so a warp keeps 8 x 16 B per lane in flight
+// (the general grouped GEMV reads 64-column chunks, 256 B per row and warp).
+constexpr int XT_COLS = 128, XT_WARPS = 8, XT_THREADS = 32 * XT_WARPS;
+template <bool VEC>
+__global__ void __launch_bounds__(XT_THREADS) xform_t_kernel(const h2g_xform_desc* __restrict__ descs,
+                                                             const int32_t* __restrict__ tile_map, int w) {
+  __shared__ double red[XT_WARPS][XT_COLS];
+  const h2g_xform_desc D = descs[tile_map[blockIdx.x]];
+  const int c0 = (blockIdx.x - D.tile_start) * XT_COLS;
+  const int n = D.n, ld = D.ldq;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cl = c0 + 4 * lane;                  // this lane's first column
+  for (int j = 0; j < w; ++j) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+    for (int r = warp; r < n; r += XT_WARPS) {
+      const double xv = __ldg(D.x + (size_t)r * w + j);
+      const double* row = D.Q + (size_t)r * ld + cl;
+      if (VEC && cl + 3 < n) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(row));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(row) + 1);
+        s[0] = fma(a.x, xv, s[0]);
+        s[1] = fma(a.y, xv, s[1]);
+        s[2] = fma(b.x, xv, s[2]);
+        s[3] = fma(b.y, xv, s[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (cl + e < n) s[e] = fma(__ldg(row + e), xv, s[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = s[e];
+    __syncthreads();
+    if (threadIdx.x < XT_COLS) {
+      const int c = c0 + threadIdx.x;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < XT_WARPS; ++q) v += red[q][threadIdx.x];
+      if (c < n) {
+        if (c < D.split) D.y1[(size_t)c * w + j] = v;
+        else D.y2[(size_t)(c - D.split) * w + j] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace h2g
+
+extern "C" int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w,
+                           int vec16, void* stream) {
+  if (total_tiles <= 0) return H2G_OK;
+  if (!d_descs || !d_tile_map || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_xform_t: bad argument");
+  if (vec16)
+    h2g::xform_t_kernel<true><<<total_tiles, h2g::XT_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+  else
+    h2g::xform_t_kernel<false><<<total_tiles, h2g::XT_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+  return h2g_check_launch("xform_t");
+}
 
 extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms, int total_chunks,
                                 int w, void* stream) {

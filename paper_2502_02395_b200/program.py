@@ -297,6 +297,25 @@ class Program:
         self._add(nat.STEP["GEMV"], len(outs), chunks, self._blob(oarr), self._blob(tarr), arg=w, nbytes=nbytes)
         return len(outs)
 
+    def xform_t(self, descs, w):
+        """descs: list of (Q, x, y1, y2, n, split, ldq): [y1; y2] = Q^T x (h2g_xform_t)."""
+        descs = [d for d in descs if d[4] > 0]
+        if not descs:
+            return 0
+        arr = np.zeros(len(descs), dtype=nat.XFORM_DT)
+        for name, col in zip(("Q", "x", "y1", "y2", "n", "split", "ldq"), zip(*descs)):
+            arr[name] = col
+        tiles = -(-arr["n"].astype(np.int64) // 128)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        vec = bool(((arr["Q"] % 16) == 0).all() and ((arr["ldq"] % 2) == 0).all())
+        n64 = arr["n"].astype(np.int64)
+        nbytes = 8 * int((n64 * n64).sum()) + 16 * int(n64.sum()) * w
+        # count < 0 tells the executor every Q row is 16-byte aligned
+        self._add(nat.STEP["XFORM_T"], -len(descs) if vec else len(descs), int(tiles.sum()), self._blob(arr),
+                  self._blob(tmap), arg=w, nbytes=nbytes)
+        return int(tiles.sum())
+
     def trsv(self, descs, trans, w):
         """descs: list of (L, Linv, x, n, ldl)."""
         descs = [d for d in descs if d[3] > 0]

@@ -229,10 +229,8 @@ class SolvePlan:
             q = fp.dh2.q[l]
             mine = self._mine(l)
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
-            prog.gemv([(self._p(V["BR"], offR[i]), self._p(V["BS"], offS[i]), 0, int(n[i]), int(r[i]),
-                        nat.GEMV_PLUS | nat.GEMV_SPLIT,
-                        [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), int(n[i]), 1, int(n[i]))])
-                       for i in range(nb) if mine[i]], w)
+            prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), self._p(V["BR"], offR[i]),
+                           self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i])) for i in range(nb) if mine[i]], w)
             if self.mode == "parallel":
                 prog = self._forward_parallel_level(prog, l, V, lay, below)
             else:
