@@ -10,9 +10,12 @@ def summarise(path, skip=0):
     rows = list(csv.reader(lines[start:]))
     h, data = rows[0], rows[1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.OrderedDict()
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in data[skip:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         name = r[ki].split("(")[0].replace("void ", "")
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         a = agg.setdefault(name, [0, 0.0])
