@@ -80,9 +80,6 @@ struct DiagShared {
   double pv[PB];     // pivots d_j of the 64x64 block
 };
 
-#ifndef H2G_CHOL16_SHFL
-#define H2G_CHOL16_SHFL 1
-#endif
 __device__ __forceinline__ void chol16_warp(double* blk, double* lblk, double* piv, Chol16Shared& cs) {
   const int lane = threadIdx.x & 31;
   const int i = lane & 15, half = lane >> 4;
@@ -92,26 +89,6 @@ __device__ __forceinline__ void chol16_warp(double* blk, double* lblk, double* p
     const double m = k <= i ? blk[i * SD + k] : blk[k * SD + i];   // full symmetric row i
     x[k] = half ? (k == i ? 1.0 : 0.0) : m;
   }
-#if H2G_CHOL16_SHFL
-  // Register-only pivot steps: the pivot, the multiplier's numerator and row j
-  // (of the working matrix for lanes 0..15, of the inverse for lanes 16..31) come
-  // by warp shuffles — no shared-memory round trip or __syncwarp per pivot.
-#pragma unroll
-  for (int j = 0; j < DB; ++j) {
-    const double d = __shfl_sync(0xffffffffu, x[j], j);          // d_j (working lane j)
-    const double xc = __shfl_sync(0xffffffffu, x[j], i);         // working lane i's column-j value
-    const int src = (lane & 16) | j;                              // row j of my half
-    double t[DB];
-#pragma unroll
-    for (int k = 0; k < DB; ++k) t[k] = __shfl_sync(0xffffffffu, x[k], src);
-    const double lj = xc * fast_rcp(d);
-    const bool act = i > j;
-#pragma unroll
-    for (int k = 0; k < DB; ++k)
-      if (act && (half ? (k <= j) : (k > j))) x[k] = fma(-lj, t[k], x[k]);
-    if (act && !half) x[j] = lj;           // multiplier l_ij; lane j keeps its pivot d_j in x[j]
-  }
-#else
 #pragma unroll
   for (int j = 0; j < DB; ++j) {
     const int buf = j & 1;
@@ -133,7 +110,6 @@ __device__ __forceinline__ void chol16_warp(double* blk, double* lblk, double* p
     }
     if (act && !half) x[j] = lj;           // multiplier l_ij; lane j keeps its pivot d_j in x[j]
   }
-#endif
   double di = x[0];
 #pragma unroll
   for (int k = 1; k < DB; ++k)
