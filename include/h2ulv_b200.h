@@ -116,12 +116,15 @@ int h2g_chol_panel_fused_max(void);
  * (L_qq -> H, L_qq^-1 -> Linv + 4096 q, pivot status -> d_npd exactly like
  * h2g_chol_panel), every row below it (rest of RR and the SR rows) updated
  * and solved against L_qq^-T in place; then the single Schur update
- * SS -= L(s) L(s)^T on the lower 64 x 64 tiles of the k x k corner.  For
- * levels with many boxes: no per-panel launches and no inter-CTA waits.
+ * SS -= L(s) L(s)^T on the lower 64 x 64 tiles of the k x k corner.  With Q
+ * the rows of V = q_red L^-T (diag_trsm) are formed in the same panel loop.
+ * For levels with many boxes: no per-panel launches and no inter-CTA waits.
  */
 typedef struct h2g_cholbox_desc {
   double* H;          /* n x n, ld ldh; RR = H[:r, :r], SR = H[r:, :r], SS = H[r:, r:] (lower parts used) */
   double* Linv;       /* ceil(r / 64) blocks of 64 x 64 */
+  const double* Q;    /* optional (NULL: none): q_full (n x n, ld ldh) -> V = q_red L^-T ... */
+  double* R;          /* ... into R[:, :r] (ld ldh), panel by panel with the rows of H */
   int32_t n, r;
   int32_t ldh, npd_slot;
 } h2g_cholbox_desc;

@@ -41,8 +41,8 @@ KBLOCK_DT = np.dtype([("rows", "<u8"), ("cols", "<u8"), ("out", "<u8"), ("m", "<
 SYMCHECK_DT = np.dtype([("A", "<u8"), ("n", "<i4"), ("lda", "<i4")])
 TRIINV_DT = np.dtype([("L", "<u8"), ("Linv", "<u8"), ("n", "<i4"), ("ldl", "<i4"), ("tile_start", "<i4"),
                       ("status_slot", "<i4")])
-CHOLBOX_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("n", "<i4"), ("r", "<i4"), ("ldh", "<i4"),
-                       ("npd_slot", "<i4")])
+CHOLBOX_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("Q", "<u8"), ("R", "<u8"), ("n", "<i4"), ("r", "<i4"),
+                       ("ldh", "<i4"), ("npd_slot", "<i4")])
 XFORM_DT = np.dtype([("Q", "<u8"), ("x", "<u8"), ("y1", "<u8"), ("y2", "<u8"), ("n", "<i4"), ("split", "<i4"),
                      ("ldq", "<i4"), ("tile_start", "<i4")])
 STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", "<i4"), ("descs", "<u8"),
@@ -51,7 +51,7 @@ STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", 
 
 assert GEMM_DT.itemsize == 72 and COPY_DT.itemsize == 40 and CHOLP_DT.itemsize == 48 and ROWS_DT.itemsize == 72
 assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 32
-assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 32 and XFORM_DT.itemsize == 48
+assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 48 and XFORM_DT.itemsize == 48
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 80
 
 STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "COPY": 5, "MEMCPY": 6,

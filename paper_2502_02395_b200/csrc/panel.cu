@@ -854,19 +854,28 @@ __global__ void __launch_bounds__(RW_THREADS, 3) chol_box_kernel(const h2g_cholb
       Lq[(size_t)i * PB + x] = R1[i * SD + x];
     }
     __syncthreads();
-    // ---- row chunks below the diagonal block (rest of RR, then all SR rows)
+    // ---- row chunks below the diagonal block (rest of RR, then all SR rows) and, with P.Q, the rows
+    // of V = q_red L^-T (diag_trsm, ulv_factor.py:223-234): the same left-looking step
+    //   out[c, p:p+b] = (X[c, p:p+b] - Y[c, 0:p] L[p:p+b, 0:p]^T) L_qq^-T
+    // with (X, Y, out) = (H, L, L) for the rows of H and (Q, V, V) for the rows of V
     const bool wact = wn * 16 < b;
     const int kend = wact ? min(16 * (wn + 1), (b + 3) & ~3) : 0;   // Linv[n][k] = 0 for k > n, k >= b
+    const int nv = P.Q ? n : 0;                   // rows of V formed by this CTA
+    const int c_begin = p + b, n_chunks = (n - c_begin + PB - 1) / PB + (nv + PB - 1) / PB;
 #pragma unroll 1
-    for (int c0 = p + b; c0 < n; c0 += PB) {
-      const int rows = min(PB, n - c0);
-      double* Hc = H + (size_t)c0 * ld;
-      cb_load_neg(acc, Hc + p, ld, rows, b);
-      cb_gemm_nt(acc, Hc, ld, rows, Hp, ld, b, p, tsm, wact);
+    for (int t = 0; t < n_chunks; ++t) {
+      const int th = (n - c_begin + PB - 1) / PB;
+      const bool vrow = t >= th;
+      const int c0 = vrow ? PB * (t - th) : c_begin + PB * t;
+      const int rows = min(PB, (vrow ? nv : n) - c0);
+      double* Y = (vrow ? P.R : H) + (size_t)c0 * ld;                 // solved columns 0..p of these rows
+      const double* X = (vrow ? P.Q : H) + (size_t)c0 * ld + p;       // right-hand side block
+      cb_load_neg(acc, X, ld, rows, b);
+      cb_gemm_nt(acc, Y, ld, rows, Hp, ld, b, p, tsm, wact);
       // L_qq^-1 (written above by this CTA; .cg reads it from L2) -> R1, C = -acc -> R0
 #pragma unroll 4
-      for (int t = tid; t < PB * PB / 2; t += RW_THREADS) {
-        const int i = t / (PB / 2), x = 2 * (t % (PB / 2));
+      for (int e = tid; e < PB * PB / 2; e += RW_THREADS) {
+        const int i = e / (PB / 2), x = 2 * (e % (PB / 2));
         cp_async16_cg(R1 + i * SD + x, Lq + (size_t)i * PB + x);
       }
       cp_async_commit();
@@ -894,7 +903,7 @@ __global__ void __launch_bounds__(RW_THREADS, 3) chol_box_kernel(const h2g_cholb
       for (int i = 0; i < 4; ++i) {
         const int m = wm * 32 + i * 8 + g;
         if (m >= rows) continue;
-        double* dst = Hc + (size_t)m * ld + p;
+        double* dst = Y + (size_t)m * ld + p;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int c = wn * 16 + j * 8 + 2 * tq;

@@ -184,24 +184,30 @@ class Program:
         return int(tiles.sum())
 
     def chol_box(self, descs, npd_ptr):
-        """descs: list of (H, Linv, n, r, ldh, npd_slot): the fused per-box partial Cholesky
-        (h2g_chol_box, one CTA per box)."""
+        """descs: list of (H, Linv, n, r, ldh, npd_slot[, Q, R]): the fused per-box partial Cholesky
+        (h2g_chol_box, one CTA per box); with Q / R also V = q_red L^-T into R."""
         descs = [d for d in descs if d[3] > 0]
         if not descs:
             return 0
         arr = np.zeros(len(descs), dtype=nat.CHOLBOX_DT)
-        for name, col in zip(("H", "Linv", "n", "r", "ldh", "npd_slot"), zip(*descs)):
+        for name, col in zip(("H", "Linv", "n", "r", "ldh", "npd_slot"), zip(*[d[:6] for d in descs])):
             arr[name] = col
+        if len(descs[0]) > 6:
+            arr["Q"] = [d[6] for d in descs]
+            arr["R"] = [d[7] for d in descs]
         role = self.role
         self.role = "factor"      # RR -> L(r), SR -> L(s) in place
         self._writes((d[0], d[2], d[3], d[4], False) for d in descs)
         self.role = "schur"       # the single SS -= L(s) L(s)^T
         self._writes((d[0] + 8 * (d[3] * d[4] + d[3]), d[2] - d[3], d[2] - d[3], d[4], True) for d in descs if d[2] > d[3])
+        self.role = "v"
+        self._writes((d[7], d[2], d[3], d[4], False) for d in descs if len(d) > 6)
         self.role = role
         n64, r64 = arr["n"].astype(np.int64), arr["r"].astype(np.int64)
         k64 = n64 - r64
-        fl = int((r64 ** 3 // 3 + r64 * r64 * k64 + 2 * k64 * k64 * r64).sum())   # chol + trsm of SR + Schur
-        self._add(nat.STEP["CHOL_BOX"], len(descs), len(descs), self._blob(arr), npd=npd_ptr, flops=fl)
+        fl = (r64 ** 3 // 3 + r64 * r64 * k64 + 2 * k64 * k64 * r64).sum()       # chol + trsm of SR + Schur
+        fl += np.where(arr["Q"] != 0, n64 * r64 * r64, 0).sum()                     # V = q_red L^-T
+        self._add(nat.STEP["CHOL_BOX"], len(descs), len(descs), self._blob(arr), npd=npd_ptr, flops=int(fl))
         return len(descs)
 
     def trsm_rows(self, descs):

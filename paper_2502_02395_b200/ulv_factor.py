@@ -636,19 +636,14 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
     if Qp and nmine >= CHOL_BOX_MIN and int(np.asarray(n)[mine].max()) <= CHOL_BOX_MAX_N:
         # many boxes: the whole elimination of a box in ONE CTA (h2g_chol_box), all boxes in
         # one launch — no panel-by-panel launch chain, REST or separate SYRK
+        # (V = q_red L^-T rides along in the same CTA, panel by panel: measured M1 lane ablation —
+        # the separate V launch cost 4.0 ms of wall time next to the upper levels)
         prog.chol_box([(Hp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), int(n[i]),
-                        slot0 + i) for i in range(nb) if mine[i] and r[i] > 0], npd_ptr)
+                        slot0 + i, Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]))
+                       for i in range(nb) if mine[i] and r[i] > 0], npd_ptr)
         prog.role = None
-        ev_fp = prog.event()
-        prog.record(ev_fp)
-        prog.lane = 4
-        prog.wait(ev_fp)
-        prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
-                         lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]), int(n[i]))
-                        for i in range(nb) if mine[i] and r[i] > 0])
         ev_v = prog.event()
         prog.record(ev_v)
-        prog.lane = 0
         return linv, loff, ev_v
     rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
     for q, p in enumerate(range(0, rmax, W)):
