@@ -243,6 +243,23 @@ def _exchange_blocks(plan, blocks, phase, level):
         cursor[own] = c + rows * cols
 
 
+def solve_merge_events(part, kdims, depth):
+    """The forward sweep's merge AllReduces: merging level l into a group-computed
+    level l-1 < L0, one per parent box whose group spans >= 2 ranks, over that
+    group, 8 d bytes per right-hand side (comm_sim.simulate_solve, comm_sim.py:138-147)."""
+    out = []
+    for l in range(depth, 0, -1):
+        if l - 1 >= part.L0:
+            continue
+        k = kdims[l]
+        for pbox in range(2 ** (l - 1)):
+            g = part.group(l - 1, pbox)
+            if g[1] - g[0] < 2:
+                continue
+            out.append(("forward", l - 1, "allreduce", g, 8 * int(k[2 * pbox] + k[2 * pbox + 1])))
+    return out
+
+
 def cross_pairs(part, l, pairs):
     """Near pairs (i, j) whose boxes are computed by different process groups."""
     return [(i, j) for (i, j) in pairs if part.group(l, i) != part.group(l, j)]

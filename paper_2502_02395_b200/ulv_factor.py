@@ -220,8 +220,11 @@ class FactorPlan:
             kdims = {l: lay.k for l, lay in dh2.levels.items()}
             for ev in merge_events(part, lists, kdims, dh2.depth):
                 self.merge_schedule.setdefault(ev[1] + 1, []).append(ev)
-            # the merge sub-communicators, created collectively in the same order on every rank
-            comm.make_groups([ev[3] for evs in self.merge_schedule.values() for ev in evs])
+            # the merge sub-communicators (factor: union groups of parent near blocks; solve: the
+            # parent boxes' groups), created collectively in the same order on every rank
+            comm.make_groups([ev[3] for evs in self.merge_schedule.values() for ev in evs] +
+                             [part.group(l, i) for l in range(min(part.L0, dh2.depth)) for i in range(2 ** l)
+                              if part.group(l, i)[1] - part.group(l, i)[0] >= 2])
         dev = dh2.device
         self.device = dev
         depth = self.depth

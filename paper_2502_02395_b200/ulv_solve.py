@@ -168,7 +168,23 @@ class SolvePlan:
             vec = self.v[l][name]
             m = self._mask(l, offkey)
             vec[:m.numel()].mul_(m)
-            self.fp.comm.all_reduce_(vec[:m.numel()], phase="solve", level=l)
+            if name == "BS" and l - 1 < self.fp.part.L0:
+                # merge into the group-computed parent level: one AllReduce per parent box over
+                # its process group, 8 d w bytes — simulate_solve's merge events (comm_sim.py:138-147)
+                self._merge_reduce(vec, l)
+            else:
+                self.fp.comm.all_reduce_(vec[:m.numel()], phase="solve", level=l)
+
+    def _merge_reduce(self, vec, l):
+        part, comm, w = self.fp.part, self.fp.comm, self.w
+        lay = self.fp.bufs[l].lay
+        offS = self.v[l]["offS"]
+        for pbox in range(2 ** (l - 1)):
+            g = part.group(l - 1, pbox)
+            if g[1] - g[0] < 2:
+                continue
+            a, b = int(offS[2 * pbox]) * w, (int(offS[2 * pbox + 1]) + int(lay.k[2 * pbox + 1])) * w
+            comm.group_all_reduce_(vec[a:b], g, phase="forward", level=l - 1)
 
     # -------------------------------------------------------------- pointers
     def _p(self, t, off_rows=0):

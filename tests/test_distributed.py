@@ -116,8 +116,8 @@ def _gpu_worker(rank, world, port, q, name):
         g = pkg.factorize(h2)
         xg = pkg.solve(g, ref["b"])
         root_err = float(np.abs(f.root - g.root).max())
-        merges = [["factor", e.level, e.kind, list(e.participants), e.bytes] for e in f.comm.trace
-                  if e.phase == "factor" and e.kind == "allreduce"]
+        merges = [[e.phase, e.level, e.kind, list(e.participants), e.bytes] for e in f.comm.trace
+                  if e.phase in ("factor", "forward") and e.kind == "allreduce"]
         q.put((rank, root_err, float(np.linalg.norm(x - xg) / np.linalg.norm(xg)),
                float(np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])), merges))
     except Exception as e:  # pragma: no cover - surfaced by the assertion below
@@ -140,13 +140,15 @@ def test_distributed_factor_solve_matches_single_gpu(name, world):
     for pr in procs:
         pr.join(timeout=60)
     import json
-    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name][str(world)]["factor"]
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name][str(world)]
+    golden = gold["factor"] + [e for e in gold["solve"] if e[0] == "forward" and e[2] == "allreduce"]
     for rank, root_err, xdiff, xref, merges in res:
         assert not isinstance(root_err, str), root_err
         assert root_err == 0.0          # identical tiles, identical arithmetic
         assert xdiff < 1e-12
         assert xref < 1e-8
-        # the merge AllReduces this rank took part in = the simulator's events containing it (f)4
+        # the merge AllReduces (factorization, forward sweep) this rank took part in = the
+        # simulator's events containing it, in order (f)4
         assert merges == [e for e in golden if e[3][0] <= rank < e[3][1]]
 
 
@@ -223,3 +225,19 @@ def test_subgroup_allreduce_gloo_world4():
     assert [r[1][0] for r in res] == [3.0, 3.0, 7.0, 7.0]
     assert [r[2][0] for r in res] == [0.0, 3.0, 3.0, 3.0]          # rank 0, 3 outside (1, 3)
     assert res[1][3] == [("allreduce", (0, 2), 24), ("allreduce", (1, 3), 16)]
+
+
+@pytest.mark.parametrize("name", ["h2_cube512_rank16", "h2_sphere1024_yukawa_tol", "h2_cube1024_sampled", "c2"])
+def test_solve_merge_allreduces_equal_comm_sim(name):
+    """The forward sweep's merge AllReduces (distributed.solve_merge_events, what
+    SolvePlan._merge_reduce executes) equal simulate_solve's forward "allreduce" events."""
+    import json
+
+    from paper_2502_02395_b200.distributed import solve_merge_events
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name]
+    tree, lists, kdims = _structure(name)
+    for p, tr in golden.items():
+        part = Partition(int(p), tree.depth)
+        ours = [[ph, lvl, kind, list(g), nb] for (ph, lvl, kind, g, nb) in solve_merge_events(part, kdims, tree.depth)]
+        want = [e for e in tr["solve"] if e[0] == "forward" and e[2] == "allreduce"]
+        assert ours == want, p
