@@ -59,6 +59,20 @@ def choose_tile_cfg(ms, ns, flags, sms=148, trans_b=False, ks=None):
 
 _TILE32_RATIO = float(os.environ.get("H2G_TILE32_RATIO", "1.5"))
 _TILE32_ALL = float(os.environ.get("H2G_TILE32_ALL", "1.5"))
+# split a launch whose problems prefer different tile shapes into a 64x64 launch and a 32x32
+# launch (each problem goes where its own padding is smaller); 0 disables
+_SPLIT_RATIO = float(os.environ.get("H2G_GEMM_SPLIT", "1.5"))
+
+
+def split_by_tile(problems):
+    """(problems for 64x64 tiles, problems for 32x32 tiles): a problem goes to the 32x32
+    launch when its 64x64 tiles would execute more than _SPLIT_RATIO x the 32x32 tiles'
+    work (ragged sizes of the upper-level boxes)."""
+    big, small = [], []
+    for p in problems:
+        m, n, f = int(p[3]), int(p[4]), int(p[9])
+        (small if 4 * gemm_tiles(m, n, f, 2) > _SPLIT_RATIO * gemm_tiles(m, n, f, 9) else big).append(p)
+    return big, small
 
 
 def copy_tiles(rows, cols):
@@ -135,6 +149,10 @@ class Program:
         rows = [p for p in problems if p[3] > 0 and p[4] > 0]
         if not rows:
             return 0
+        if tile_cfg is None and _SPLIT_RATIO > 0 and len(rows) > 1:
+            big, small = split_by_tile(rows)
+            if big and small:
+                return self.gemm(trans_a, trans_b, big) + self.gemm(trans_a, trans_b, small, tile_cfg=9)
         arr = np.zeros(len(rows), dtype=nat.GEMM_DT)
         cols = list(zip(*rows))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
@@ -195,6 +213,7 @@ class Program:
         if len(descs[0]) > 6:
             arr["Q"] = [d[6] for d in descs]
             arr["R"] = [d[7] for d in descs]
+            descs = [d if d[6] else d[:6] for d in descs]
         role = self.role
         self.role = "factor"      # RR -> L(r), SR -> L(s) in place
         self._writes((d[0], d[2], d[3], d[4], False) for d in descs)

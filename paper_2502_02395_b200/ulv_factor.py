@@ -55,6 +55,7 @@ F64 = torch.float64
 # size <= CHOL_BOX_MAX_N; the panel-step chain otherwise (few large boxes: the upper levels)
 CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
+CHOL_BOX_V = os.environ.get("H2G_CHOL_BOX_V", "0") == "1"
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -639,14 +640,26 @@ def partial_cholesky_steps(prog, device, npd_ptr, Hp, Rp, qo, n, r, slot0, mine=
     if Qp and nmine >= CHOL_BOX_MIN and int(np.asarray(n)[mine].max()) <= CHOL_BOX_MAX_N:
         # many boxes: the whole elimination of a box in ONE CTA (h2g_chol_box), all boxes in
         # one launch — no panel-by-panel launch chain, REST or separate SYRK
-        # (V = q_red L^-T rides along in the same CTA, panel by panel: measured M1 lane ablation —
-        # the separate V launch cost 4.0 ms of wall time next to the upper levels)
+        # V = q_red L^-T: in the same CTA, panel by panel (H2G_CHOL_BOX_V=1), or one trsm_rows
+        # launch on lane 4 (default).  M1: 27.10 vs 26.80 ms — the GPU is saturated either way
+        # (the separate launch costs 4.0 ms of wall time in the lane ablation, the fused rows 3.2 ms
+        # of critical-lane time).
+        fuse_v = CHOL_BOX_V
         prog.chol_box([(Hp + 8 * int(qo[i]), lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), int(n[i]),
-                        slot0 + i, Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]))
+                        slot0 + i) + ((Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i])) if fuse_v else (0, 0))
                        for i in range(nb) if mine[i] and r[i] > 0], npd_ptr)
         prog.role = None
+        if not fuse_v:
+            ev_fp = prog.event()
+            prog.record(ev_fp)
+            prog.lane = 4
+            prog.wait(ev_fp)
+            prog.trsm_rows([(Hp + 8 * int(qo[i]), Qp + 8 * int(qo[i]), Rp + 8 * int(qo[i]),
+                             lp + 8 * int(loff[i]) * W * W, int(n[i]), int(r[i]), 0, int(nblk[i]), int(n[i]),
+                             int(n[i])) for i in range(nb) if mine[i] and r[i] > 0])
         ev_v = prog.event()
         prog.record(ev_v)
+        prog.lane = 0
         return linv, loff, ev_v
     rest_ev = []                      # rest_ev[q]: REST(q) done (None: no REST launch)
     for q, p in enumerate(range(0, rmax, W)):

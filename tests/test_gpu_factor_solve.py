@@ -162,3 +162,24 @@ def test_fused_box_cholesky_matches_reference(pkg, name, monkeypatch):
     x = pkg.solve(f, ref["b"])
     assert _rel(x, ref["x"]) < RTOL_X
     ulv_factor.clear_cache()
+
+
+@pytest.mark.parametrize("name", H2_FIXTURES[:2])
+def test_fused_box_with_v_matches_reference(pkg, name, monkeypatch):
+    """h2g_chol_box with V = q_red L^-T formed in the same CTA (H2G_CHOL_BOX_V)."""
+    from paper_2502_02395_b200 import ulv_factor
+    monkeypatch.setattr(ulv_factor, "CHOL_BOX_MIN", 1)
+    monkeypatch.setattr(ulv_factor, "CHOL_BOX_V", True)
+    ulv_factor.clear_cache()
+    h2 = load_h2(name)
+    ref = reference_factors(name)
+    f = pkg.factorize(h2)
+    for (l, i, j), v in ref["lr_off"].items():
+        assert _rel(f.levels[l].lr_off[(i, j)], v) < RTOL_BLOCK, (l, i, j)
+    for l in f.levels:
+        for i, v in f.levels[l].v.items():
+            b = h2.bases[(l, i)]
+            lr = f.levels[l].lr_diag[i]
+            assert np.allclose(v @ lr.T, b.q_red, atol=1e-10), (l, i)
+    assert _rel(pkg.solve(f, ref["b"]), ref["x"]) < RTOL_X
+    ulv_factor.clear_cache()
