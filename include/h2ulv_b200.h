@@ -238,6 +238,23 @@ typedef struct h2g_xform_desc {
 int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w, int vec16,
                 void* stream);
 
+/* h2g_xform_n: out = Q [xr; xs] for every box (Q n x n row-major, ld ldq; xr
+ * the first r entries, xs the other n - r, each n x w / ld w; n <= 4096): the
+ * basis transform of the backward sweep, full_i = q_red x_R + q_skel x_S
+ * (ulv_solve.py:178-181).  One CTA per 32 output rows (d_tile_map as above);
+ * vec16 as for h2g_xform_t.
+ */
+typedef struct h2g_xform_n_desc {
+  const double* Q;
+  const double* xr;
+  const double* xs;
+  double* out;
+  int32_t n, r, ldq, tile_start;
+} h2g_xform_n_desc;
+
+int h2g_xform_n(const h2g_xform_n_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w, int vec16,
+                void* stream);
+
 /* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
  * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
  * leading dimension ldl, Linv the inverses of its 64 x 64 diagonal blocks
@@ -368,6 +385,7 @@ enum {
   H2G_STEP_TRIINV = 16,     /* descs/map = triinv descs/tile map; npd = status */
   H2G_STEP_CHOL_BOX = 17,   /* descs = cholbox descs; npd = status */
   H2G_STEP_XFORM_T = 18,    /* descs/map = xform descs/tile map; arg = w; count < 0: 16-byte loads */
+  H2G_STEP_XFORM_N = 19,    /* descs/map = xform_n descs/tile map; arg = w; count < 0: 16-byte loads */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

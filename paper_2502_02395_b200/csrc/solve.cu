@@ -8,7 +8,10 @@
 
 namespace h2g {
 
-constexpr int GV_THREADS = 512;
+#ifndef H2G_GV_THREADS
+#define H2G_GV_THREADS 512
+#endif
+constexpr int GV_THREADS = H2G_GV_THREADS;
 constexpr int GV_CHUNK = 64;    // output rows per CTA (small: many CTAs for memory-level parallelism)
 constexpr int GV_W = 4;         // RHS columns per pass
 #ifndef H2G_GV_MINB
@@ -29,7 +32,7 @@ __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) 
 }
 
 // y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t
-__global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
+__global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
                                                                   const h2g_gemv_term* __restrict__ terms, int w) {
   __shared__ double acc[GV_CHUNK * GV_W];
   __shared__ double red[GV_THREADS / 32][GV_CHUNK];
@@ -272,7 +275,65 @@ __global__ void __launch_bounds__(XT_THREADS) xform_t_kernel(const h2g_xform_des
   }
 }
 
+// Basis transform of the backward sweep, full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]
+// (ulv_solve.py:178-181): a CTA owns 32 output rows of one box, [x_R; x_S] is staged in
+// shared memory, each warp takes 4 rows with the lanes across the columns (16-byte loads
+// when the rows are aligned), one shuffle reduction per row.
+constexpr int XN_ROWS = 32, XN_WARPS = 8, XN_THREADS = 32 * XN_WARPS, XN_MAXN = 4096;
+template <bool VEC>
+__global__ void __launch_bounds__(XN_THREADS) xform_n_kernel(const h2g_xform_n_desc* __restrict__ descs,
+                                                             const int32_t* __restrict__ tile_map, int w) {
+  __shared__ __align__(16) double xs[XN_MAXN];
+  const h2g_xform_n_desc D = descs[tile_map[blockIdx.x]];
+  const int r0 = (blockIdx.x - D.tile_start) * XN_ROWS;
+  const int n = D.n, r = D.r, ld = D.ldq;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < w; ++j) {
+    for (int c = threadIdx.x; c < n; c += XN_THREADS)
+      xs[c] = c < r ? D.xr[(size_t)c * w + j] : D.xs[(size_t)(c - r) * w + j];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < XN_ROWS / XN_WARPS; ++u) {
+      const int row = r0 + warp * (XN_ROWS / XN_WARPS) + u;
+      if (row >= n) break;
+      const double* q = D.Q + (size_t)row * ld;
+      double s0 = 0.0, s1 = 0.0;
+      if (VEC) {
+#pragma unroll 4
+        for (int c = 2 * lane; c < n; c += 64) {
+          if (c + 1 < n) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(q + c));
+            s0 = fma(a.x, xs[c], s0);
+            s1 = fma(a.y, xs[c + 1], s1);
+          } else {
+            s0 = fma(__ldg(q + c), xs[c], s0);
+          }
+        }
+      } else {
+#pragma unroll 4
+        for (int c = lane; c < n; c += 32) s0 = fma(__ldg(q + c), xs[c], s0);
+      }
+      double v = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) D.out[(size_t)row * w + j] = v;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace h2g
+
+extern "C" int h2g_xform_n(const h2g_xform_n_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w,
+                           int vec16, void* stream) {
+  if (total_tiles <= 0) return H2G_OK;
+  if (!d_descs || !d_tile_map || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_xform_n: bad argument");
+  if (vec16)
+    h2g::xform_n_kernel<true><<<total_tiles, h2g::XN_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+  else
+    h2g::xform_n_kernel<false><<<total_tiles, h2g::XN_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+  return h2g_check_launch("xform_n");
+}
 
 extern "C" int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w,
                            int vec16, void* stream) {

@@ -341,6 +341,26 @@ class Program:
                   self._blob(tmap), arg=w, nbytes=nbytes)
         return int(tiles.sum())
 
+    def xform_n(self, descs, w):
+        """descs: list of (Q, xr, xs, out, n, r, ldq): out = Q [xr; xs] (h2g_xform_n)."""
+        descs = [d for d in descs if d[4] > 0]
+        if not descs:
+            return 0
+        if max(d[4] for d in descs) > 4096:
+            raise ValueError("h2g_xform_n: box size above 4096")
+        arr = np.zeros(len(descs), dtype=nat.XFORMN_DT)
+        for name, col in zip(("Q", "xr", "xs", "out", "n", "r", "ldq"), zip(*descs)):
+            arr[name] = col
+        tiles = -(-arr["n"].astype(np.int64) // 32)
+        arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
+        vec = bool(((arr["Q"] % 16) == 0).all() and ((arr["ldq"] % 2) == 0).all())
+        n64 = arr["n"].astype(np.int64)
+        nbytes = 8 * int((n64 * n64).sum()) + 16 * int(n64.sum()) * w
+        self._add(nat.STEP["XFORM_N"], -len(descs) if vec else len(descs), int(tiles.sum()), self._blob(arr),
+                  self._blob(tmap), arg=w, nbytes=nbytes)
+        return int(tiles.sum())
+
     def trsv(self, descs, trans, w):
         """descs: list of (L, Linv, x, n, ldl)."""
         descs = [d for d in descs if d[3] > 0]

@@ -371,20 +371,11 @@ class SolvePlan:
                 prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in nbr], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
-            # B3  full_i = q_red x_R + q_skel x_S
+            # B3  full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]
             q = fp.dh2.q[l]
-            outs = []
-            for i in range(nb):
-                if not mine[i]:
-                    continue
-                qi = q.data_ptr() + 8 * int(lay.qoff[i])
-                terms = []
-                if r[i] > 0:
-                    terms.append((qi, self._p(V["XR"], offR[i]), int(n[i]), 0, int(r[i])))
-                if k[i] > 0:
-                    terms.append((qi + 8 * int(r[i]), self._p(xs, offS[i]), int(n[i]), 0, int(k[i])))
-                outs.append((self._p(V["FULL"], offX[i]), 0, 0, int(n[i]), 0, nat.GEMV_PLUS, terms))
-            prog.gemv(outs, w)
+            prog.xform_n([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(V["XR"], offR[i]), self._p(xs, offS[i]),
+                           self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
+                          for i in range(nb) if mine[i]], w)
             xs = V["FULL"]
         if self.dist and depth >= 1:
             prog = self._cut(prog, ("FULL", depth, "offX"))     # assemble x on every rank
