@@ -16,7 +16,6 @@ segments of level l-1 (n_p = k_2p + k_2p+1), so the merge
 `segs[p] = vstack(b_S,2p, b_S,2p+1)` (ulv_solve.py:113) costs nothing.
 """
 
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,8 +26,6 @@ from . import _native as nat
 from .program import Program
 
 F64 = torch.float64
-# levels with at most this many boxes solve their triangles with explicit inverses (GEMV)
-_EXPLICIT_MAX = int(os.environ.get("H2G_SOLVE_EXPLICIT_MAX", "2048"))
 
 
 @dataclass
@@ -101,7 +98,7 @@ class SolvePlan:
         W = nat.PANEL_WIDTH
         prog = Program(dev)
         self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
-        self.linv, self.loff, self.winv = {}, {}, {}
+        self.linv, self.loff = {}, {}
         for l in range(fp.depth, 0, -1):
             B = fp.bufs[l]
             lay = B.lay
@@ -113,18 +110,6 @@ class SolvePlan:
             prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
                           int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
                         self._tri_status.data_ptr())
-            if lay.nb <= _EXPLICIT_MAX:
-                # explicit W_i = L_i^-T (upper triangular, r_i x r_i) by the row solve of the identity:
-                # the level's triangular solves become grouped GEMVs (many CTAs per box instead of one
-                # CTA walking r_i / 64 blocks)
-                r64 = np.asarray(lay.r, dtype=np.int64)
-                woff = np.concatenate([[0], np.cumsum(r64 * r64)[:-1]]).astype(np.int64)
-                wt = torch.zeros(max(int((r64 * r64).sum()), 1), dtype=F64, device=dev)
-                self.winv[l] = (wt, woff)
-                prog.trsm_rows([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, wt.data_ptr() + 8 * int(woff[i]),
-                                 lt.data_ptr() + 8 * int(loff[i]) * W * W, int(lay.r[i]), int(lay.r[i]), 0,
-                                 int(nblk[i]), int(lay.n[i]), int(lay.r[i]))
-                                for i in range(lay.nb) if mine[i] and lay.r[i] > 0])
         d = fp.root_dim
         nb0 = -(-d // W)
         self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
@@ -234,33 +219,6 @@ class SolvePlan:
         return (B.H.data_ptr() + 8 * int(lay.qoff[i]), self.linv[l].data_ptr() + 8 * int(self.loff[l][i]) * 4096, x,
                 int(lay.r[i]), int(lay.n[i]))
 
-    def _tri(self, prog, l, boxes, src, dst, trans, scratch=None):
-        """dst_i = L_i^-1 src_i (trans 0) or L_i^-T src_i (trans 1) for the given boxes of level l
-        (segments at offR).  Levels with an explicit W_i = L_i^-T: one grouped GEMV
-        (dst_i = W_i^T src_i / W_i src_i); src == dst goes through `scratch`.  Otherwise the
-        blocked TRSV in place on dst (src copied first)."""
-        w = self.w
-        V = self.v[l]
-        offR = V["offR"]
-        r = self.fp.bufs[l].lay.r
-        boxes = [i for i in boxes if r[i] > 0]
-        if not boxes:
-            return
-        if l in self.winv:
-            wt, woff = self.winv[l]
-            if src is dst:
-                for i in boxes:
-                    prog.memcpy(self._p(scratch, offR[i]), self._p(src, offR[i]), 8 * int(r[i]) * w)
-                src = scratch
-            prog.gemv([(self._p(dst, offR[i]), 0, 0, int(r[i]), 0, nat.GEMV_PLUS,
-                        [(wt.data_ptr() + 8 * int(woff[i]), self._p(src, offR[i]), int(r[i]), 1 - trans, int(r[i]))])
-                       for i in boxes], w)
-            return
-        if src is not dst:
-            for i in boxes:
-                prog.memcpy(self._p(dst, offR[i]), self._p(src, offR[i]), 8 * int(r[i]) * w)
-        prog.trsv([self._tr(l, i, self._p(dst, offR[i])) for i in boxes], trans, w)
-
     def _root_solve(self, prog, y, x, trans):
         """y = L_00^-1 x (trans 0) or L_00^-T x (trans 1) with the root's explicit
         W = L_00^-T from the factorization: one grouped GEMV instead of a TRSV."""
@@ -308,11 +266,8 @@ class SolvePlan:
         mine = self._mine(l)
         dist = self.dist
         # P1  z_i = L_ii^-1 b_R,i
-        if l not in self.winv:
-            prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
-            self._tri(prog, l, [i for i in range(nb) if mine[i]], V["Z"], V["Z"], 0)
-        else:
-            self._tri(prog, l, [i for i in range(nb) if mine[i]], V["BR"], V["Z"], 0)
+        prog.memcpy(V["Z"].data_ptr(), V["BR"].data_ptr(), 8 * int(r.sum()) * w)
+        prog.trsv([self._tr(l, i, self._p(V["Z"], offR[i])) for i in range(nb) if mine[i]], 0, w)
         if dist:
             prog = self._cut(prog, ("Z", l, "offR"))
         # P2  t_i = b_R,i - sum_{j<i near} L(r)_ij z_j ;  P3  y_i = L_ii^-1 t_i.
@@ -327,7 +282,7 @@ class SolvePlan:
                      for j in below[i] if r[j] > 0]
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
         prog.gemv(outs, w)
-        self._tri(prog, l, nbr, V["Y"], V["Y"], 0, scratch=V["Z2"])
+        prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in nbr], 0, w)
         if dist:
             prog = self._cut(prog, ("Y", l, "offR"))
         # P4  b_S,a -= sum_b L(s)_ab y_b
@@ -360,7 +315,7 @@ class SolvePlan:
         _, above = _near_sets(lay)
         prog.memcpy(V["Y"].data_ptr(), V["BR"].data_ptr(), 8 * int(lay.r.sum()) * w)
         for i in range(lay.nb):
-            self._tri(prog, l, [i], V["Y"], V["Y"], 0, scratch=V["Z2"])
+            prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i]))], 0, w)
             outs = []
             for j in above[i]:
                 if lay.r[i] == 0 or lay.r[j] == 0:
@@ -400,11 +355,8 @@ class SolvePlan:
             prog.gemv(outs, w)
             if self.mode == "parallel":
                 _, above = _near_sets(lay)
-                if l not in self.winv:
-                    prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
-                    self._tri(prog, l, [i for i in range(nb) if mine[i]], V["Z2"], V["Z2"], 1)
-                else:
-                    self._tri(prog, l, [i for i in range(nb) if mine[i]], V["YB"], V["Z2"], 1)
+                prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
+                prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
                 if dist:
                     prog = self._cut(prog, ("Z2", l, "offR"))
                 # boxes without upper near neighbours: x_R,i = z2_i (same TRSV, same input)
@@ -416,7 +368,7 @@ class SolvePlan:
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
                 prog.gemv(outs, w)
-                self._tri(prog, l, nbr, V["XR"], V["XR"], 1, scratch=V["Z"])
+                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in nbr], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
             # B3  full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]
@@ -441,7 +393,7 @@ class SolvePlan:
                       int(lay.r[j])) for j in above[i] if lay.r[j] > 0]
             if terms:
                 prog.gemv([(self._p(V["XR"], offR[i]), 0, self._p(V["XR"], offR[i]), int(lay.r[i]), 0, 0, terms)], w)
-            self._tri(prog, l, [i], V["XR"], V["XR"], 1, scratch=V["Z"])
+            prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i]))], 1, w)
 
     # -------------------------------------------------------------- run
     def run_forward(self, stream=None):
