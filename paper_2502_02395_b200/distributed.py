@@ -1,29 +1,33 @@
 """Multi-GPU factorization and solve: boxes sharded over ranks, top levels
-replicated (arXiv 2502.02395 §5; the reference only SIMULATES this plan in
-comm_sim.py:1-186 — here the data really moves).
+computed by process groups (arXiv 2502.02395 §5; the reference only SIMULATES
+this plan in comm_sim.py:1-186 — here the data really moves).
 
 Ownership follows the reference's ProcAssignment (comm_sim.py:17-37): with
-P = 2^L0 ranks, rank g owns box i of level l >= L0 iff i >> (l - L0) == g
-(contiguous leaf ranges); levels < L0 and the root are computed redundantly
-by every rank (replicated_work, comm_sim.py:151-167).
+P = 2^L0 ranks, rank g owns box i of a level l >= L0 iff i >> (l - L0) == g
+(contiguous leaf ranges); a box of a level l < L0 is computed by its subtree's
+process group [i P/2^l, (i+1) P/2^l), so every rank computes one box per such
+level and the root (replicated_work, comm_sim.py:151-167).
 
 Exchanges (one process per GPU, torch.distributed; NCCL over NVLink on a
-multi-GPU node, gloo through host memory in the CPU tests):
+multi-GPU node, gloo through host memory in the tests):
   factorization
-    halo_v(l)     after the diagonal phase of a distributed level: the
-                  [V_j | q_skel_j] block of every box j that is the column of a
-                  near pair whose row box lives on another rank (all_gather of
-                  the packed exports)
-    boundary(L0)  after level L0: every rank receives all level-L0 Schur blocks
-                  (H_i, T_ij) and assembles the replicated parent level — the
-                  reference's merge AllReduce (Eq. 34, comm_sim.simulate_factor)
-                  done as one all_gather
-    solve_halo    cross-pair off-diagonal factor blocks (T_ij, L(s)_ji) also
-                  land on the column box's owner, so the solve only moves vectors
-  solve           per distributed level, the owned segments of each
-                  intermediate vector are summed across ranks (all_reduce of a
-                  masked level vector; comm_sim.simulate_solve's neighbour
-                  reduce/broadcast + merge AllReduce)
+    halo_v(l)     after the diagonal phase of a level: V_j (n_j x r_j) of every
+                  box j that is the column of a near pair whose row box another
+                  group computes (one all_gather; packing / unpacking are
+                  cached block-copy programs)
+    merge(l)      merging level l into a group-computed level l-1 < L0: each
+                  rank writes the child blocks it contributes into zeroed parent
+                  blocks, then ONE AllReduce per parent near block over the union
+                  group of its two boxes (Eq. 34) — the event list of
+                  comm_sim.simulate_factor exactly (merge_events, golden-tested)
+    solve_halo    cross-group off-diagonal factor blocks (T_ij[:, :r_j], L(s)_ji)
+                  also land on the column box's group, so the solve only moves
+                  vectors
+  solve           forward merges into group-computed levels: one AllReduce per
+                  parent box over its group (simulate_solve's merge events);
+                  within a level the segments each rank contributes are summed
+                  across ranks (all_reduce of a masked level vector — simpler
+                  than simulate_solve's per-pair neighbour reduce / broadcast)
 """
 
 import math
@@ -182,6 +186,20 @@ class Comm:
         dist.all_gather(out, t, group=self.group)
         return out
 
+    def all_gather_into(self, out, t, phase="factor", level=-1):
+        """out (world x t.numel(), contiguous) <- every rank's t."""
+        import torch.distributed as dist
+
+        self._log(phase, level, "all_gather", t.numel() * t.element_size() * self.world)
+        if self.host_staged:
+            h = t.cpu()
+            parts = [torch.empty_like(h) for _ in range(self.world)]
+            dist.all_gather(parts, h, group=self.group)
+            out.copy_(torch.cat(parts).to(out.device))
+        else:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
+
     def all_reduce_(self, t, op="sum", phase="solve", level=-1):
         import torch.distributed as dist
 
@@ -212,23 +230,71 @@ def _view(t, off, rows, cols, ld):
     return t.as_strided((rows, cols), (ld, 1), t.storage_offset() + off)
 
 
-def _exchange_blocks(plan, blocks, phase, level):
+class _ExchangeProgram:
+    """Static pack / unpack of one exchange: ONE block-copy launch gathers this rank's
+    exports into the send buffer, ONE scatters the other ranks' blocks out of the
+    gathered buffer (h2g_block_copy; built once per plan and exchange)."""
+
+    def __init__(self, plan, blocks):
+        comm, dev = plan.comm, plan.device
+        sizes = np.zeros(comm.world, dtype=np.int64)
+        for own, _, _, rows, cols, _ in blocks:
+            sizes[own] += rows * cols
+        self.cap = int(sizes.max())
+        if self.cap == 0:
+            return
+        self.send = torch.zeros(self.cap, dtype=F64, device=dev)
+        self.recv = torch.zeros(comm.world * self.cap, dtype=F64, device=dev)
+        pack, unpack = [], []
+        cursor = np.zeros(comm.world, dtype=np.int64)
+        for own, t, off, rows, cols, ld in blocks:
+            c = int(cursor[own])
+            if rows * cols:
+                ptr = t.data_ptr() + 8 * int(off)
+                if own == comm.rank:
+                    pack.append((ptr, self.send.data_ptr() + 8 * c, rows, cols, ld, cols, 0))
+                else:
+                    unpack.append((self.recv.data_ptr() + 8 * (own * self.cap + c), ptr, rows, cols, cols, ld, 0))
+            cursor[own] = c + rows * cols
+        self.pack = Program(dev)
+        self.pack.copy(pack)
+        self.pack.finalize()
+        self.unpack = Program(dev)
+        self.unpack.copy(unpack)
+        self.unpack.finalize()
+
+    def run(self, comm, phase, level):
+        if self.cap == 0:
+            return
+        self.pack.run()
+        comm.all_gather_into(self.recv, self.send, phase=phase, level=level)
+        self.unpack.run()
+
+
+def _exchange_blocks(plan, blocks, phase, level, tag=None):
     """all_gather of per-rank block exports.
 
     blocks: list of (owner_rank, flat device tensor, offset, rows, cols, ld) —
-    strided sub-blocks (only the slabs the receiver reads, e.g. the k x k SS
-    corner of H_i, not all of H_i); every rank lists the same blocks in the
-    same order; after the call each rank's copy of every block equals its
-    owner's."""
+    strided sub-blocks (only the slabs the receiver reads, e.g. V_j = R_j[:, :r_j],
+    not all of R_j); every rank lists the same blocks in the same order; after the
+    call each rank's copy of every block equals its owner's.  On the GPU the
+    packing is a cached pair of block-copy programs (tag = the exchange)."""
     comm = plan.comm
-    dev = plan.device
+    if plan.device.type == "cuda":
+        cache = plan.__dict__.setdefault("_exchange_programs", {})
+        key = tag if tag is not None else id(blocks)
+        if key not in cache:
+            cache[key] = _ExchangeProgram(plan, blocks)
+        cache[key].run(comm, phase, level)
+        return
+    # host tensors (the CPU unit test of the exchange pattern)
     sizes = np.zeros(comm.world, dtype=np.int64)
     for own, _, _, rows, cols, _ in blocks:
         sizes[own] += rows * cols
     cap = int(sizes.max())
     if cap == 0:
         return
-    send = torch.zeros(cap, dtype=F64, device=dev)
+    send = torch.zeros(cap, dtype=F64, device=plan.device)
     pos = 0
     for own, t, off, rows, cols, ld in blocks:
         if own == comm.rank and rows * cols:
@@ -306,11 +372,11 @@ def run_exchange(plan, seg):
     if plan.comm.host_staged:
         torch.cuda.current_stream(plan.device).synchronize()
     if kind == "halo_v":
-        _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l)
+        _exchange_blocks(plan, _halo_v_blocks(plan, l), "factor", l, tag=seg)
     elif kind == "merge":
         _merge_allreduce(plan, l)
     elif kind == "solve_halo":
-        _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1)
+        _exchange_blocks(plan, _solve_halo_blocks(plan), "factor", -1, tag=seg)
     else:
         raise ValueError(f"unknown exchange {kind}")
 
