@@ -37,7 +37,8 @@ enum {
   H2G_OK = 0,
   H2G_EINVAL = 1,   /* bad argument (null pointer, negative size, ...)   */
   H2G_ECUDA = 2,    /* a CUDA runtime call or launch failed               */
-  H2G_ESTEP = 3     /* unknown step kind in a program                     */
+  H2G_ESTEP = 3,    /* unknown step kind in a program                     */
+  H2G_ENPD = 4      /* the factorization met a non-positive pivot (status) */
 };
 
 /* ---- grouped GEMM ---------------------------------------------------------
@@ -425,6 +426,33 @@ int h2g_run_program_timed(const h2g_step* steps, int nsteps, void* stream, float
 int h2g_graph_capture(const h2g_step* steps, int nsteps, void* stream, void* ctx, void** exec_out);
 int h2g_graph_launch(void* exec, void* stream);
 int h2g_graph_destroy(void* exec);
+
+/* ---- factorization session (handle-level entry) -------------------------------
+ * A session owns one planned factorization: its step program (planned once by
+ * the host for a structure, e.g. paper_2502_02395_b200.ulv_factor.FactorPlan,
+ * which also owns the device buffers the descriptors point into), captured
+ * into a CUDA graph with its own lanes, plus the device pivot-status array
+ * (one int32 per box of every level and the root, INT32_MAX = no failure;
+ * the program resets it first).  Levels are numbered like the reference:
+ * level l holds 2^l boxes, its statuses start at slot_base[l] (l = 0 is the
+ * root, one slot).
+ *   h2g_session_factor_async: enqueue one factorization on `stream`.
+ *   h2g_session_status: wait for it and decode the statuses the way the
+ *     reference reports a breakdown — the deepest failing level first, the
+ *     first failing box of it — into *status; returns H2G_ENPD when a pivot
+ *     failed (NotPositiveDefiniteError(pivot, level, box), dense_core.py:60-63,
+ *     ulv_factor.py:218), H2G_OK otherwise.
+ */
+typedef struct h2g_npd_status {
+  int32_t failed;
+  int32_t pivot, level, box;
+} h2g_npd_status;
+
+int h2g_session_create(const h2g_step* steps, int nsteps, int n_events, int32_t* d_npd, int depth,
+                       const int32_t* slot_base, void* stream, void** session_out);
+int h2g_session_factor_async(void* session, void* stream);
+int h2g_session_status(void* session, void* stream, h2g_npd_status* status);
+int h2g_session_destroy(void* session);
 
 int h2g_abi_version(void);
 const char* h2g_last_error(void);

@@ -56,6 +56,8 @@ assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.it
 assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 48 and XFORM_DT.itemsize == 48 and XFORMN_DT.itemsize == 48
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 80
 
+NPD_STATUS_DT = np.dtype([("failed", "<i4"), ("pivot", "<i4"), ("level", "<i4"), ("box", "<i4")])
+H2G_ENPD = 4
 STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "COPY": 5, "MEMCPY": 6,
         "QR_PANEL": 7, "BASIS": 8, "GEMV": 9, "TRSV": 10, "KBLOCK": 11, "NOP": 12, "CHOL_PANEL": 13, "TRSM_ROWS": 14,
         "SYMCHECK": 15, "TRIINV": 16, "CHOL_BOX": 17, "XFORM_T": 18, "XFORM_N": 19}
@@ -72,7 +74,8 @@ EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_chol_panel_tiles", "h2g_ch
            "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
-           "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n"]
+           "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n",
+           "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy"]
 
 _LIB = None
 
@@ -117,6 +120,10 @@ def load_library(path=LIB_PATH):
         "h2g_chol_box": (i32, [vp, i32, vp, vp]),
         "h2g_xform_t": (i32, [vp, vp, i32, i32, i32, vp]),
         "h2g_xform_n": (i32, [vp, vp, i32, i32, i32, vp]),
+        "h2g_session_create": (i32, [vp, i32, i32, vp, i32, vp, vp, ctypes.POINTER(vp)]),
+        "h2g_session_factor_async": (i32, [vp, vp]),
+        "h2g_session_status": (i32, [vp, vp, vp]),
+        "h2g_session_destroy": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -135,6 +142,10 @@ def lib():
     if not torch.cuda.is_available():
         raise NativeUnavailableError("no CUDA device: the H2-ULV path runs only on the GPU (no CPU fallback)")
     return load_library()
+
+
+def ctypes_void_p():
+    return ctypes.c_void_p
 
 
 def check(rc, what="h2g call"):

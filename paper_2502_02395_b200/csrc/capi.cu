@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <climits>
 #include <vector>
 
 #include "common.cuh"
@@ -233,5 +235,73 @@ extern "C" int h2g_graph_launch(void* exec, void* stream) {
 
 extern "C" int h2g_graph_destroy(void* exec) {
   if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return H2G_OK;
+}
+
+// ------------------------------------------------------------------ factorization session
+struct Session {
+  void* ctx = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int32_t* d_npd = nullptr;
+  int depth = 0;
+  std::vector<int32_t> slot_base;   // level l -> first slot (l = 0: the root)
+  std::vector<int32_t> host;
+};
+
+extern "C" int h2g_session_create(const h2g_step* steps, int nsteps, int n_events, int32_t* d_npd, int depth,
+                                  const int32_t* slot_base, void* stream, void** session_out) {
+  if (!steps || nsteps <= 0 || !d_npd || !slot_base || depth < 0 || !session_out)
+    return h2g_set_error(H2G_EINVAL, "h2g_session_create: bad arguments");
+  Session* s = new Session();
+  s->d_npd = d_npd;
+  s->depth = depth;
+  s->slot_base.assign(slot_base, slot_base + depth + 1);
+  int rc = h2g_exec_ctx_create(n_events > 0 ? n_events : 1, &s->ctx);
+  void* exec = nullptr;
+  if (!rc) rc = h2g_graph_capture(steps, nsteps, stream, s->ctx, &exec);
+  if (rc) {
+    h2g_session_destroy(s);
+    return rc;
+  }
+  s->graph = (cudaGraphExec_t)exec;
+  int total = 0;
+  for (int l = 0; l <= depth; ++l) total = std::max(total, slot_base[l] + (l ? (1 << l) : 1));
+  s->host.resize(total);
+  *session_out = s;
+  return H2G_OK;
+}
+
+extern "C" int h2g_session_factor_async(void* session, void* stream) {
+  Session* s = (Session*)session;
+  if (!s || !s->graph) return h2g_set_error(H2G_EINVAL, "h2g_session_factor_async: null session");
+  return h2g_graph_launch(s->graph, stream);
+}
+
+extern "C" int h2g_session_status(void* session, void* stream, h2g_npd_status* status) {
+  Session* s = (Session*)session;
+  if (!s || !status) return h2g_set_error(H2G_EINVAL, "h2g_session_status: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(s->host.data(), s->d_npd, s->host.size() * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return h2g_set_error(H2G_ECUDA, "h2g_session_status: %s", cudaGetErrorString(e));
+  *status = h2g_npd_status{0, 0, 0, 0};
+  for (int l = s->depth; l >= 0; --l) {          // deepest level first, then the root
+    const int base = s->slot_base[l], cnt = l ? (1 << l) : 1;
+    for (int b = 0; b < cnt; ++b)
+      if (s->host[base + b] != INT32_MAX) {
+        *status = h2g_npd_status{1, s->host[base + b], l, b};
+        return h2g_set_error(H2G_ENPD, "non-positive pivot %d at level %d, box %d", s->host[base + b], l, b);
+      }
+  }
+  return H2G_OK;
+}
+
+extern "C" int h2g_session_destroy(void* session) {
+  Session* s = (Session*)session;
+  if (!s) return H2G_OK;
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->ctx) h2g_exec_ctx_destroy(s->ctx);
+  delete s;
   return H2G_OK;
 }

@@ -199,6 +199,50 @@ class _LevelBuffers:
     pass
 
 
+class _Session:
+    """ctypes handle of h2g_session_* (include/h2ulv_b200.h): the plan's single program
+    captured into a CUDA graph, launched asynchronously; the pivot statuses are decoded
+    natively into (pivot, level, box) — the NotPositiveDefiniteError contract."""
+
+    def __init__(self, plan):
+        import ctypes
+
+        prog = plan.program
+        lib = nat.lib()
+        base = np.zeros(plan.depth + 1, dtype=np.int32)
+        for l, b in plan.slot_base.items():
+            base[l] = b
+        self._base = base
+        side = torch.cuda.Stream(device=plan.device)
+        torch.cuda.current_stream(plan.device).synchronize()
+        h = ctypes.c_void_p()
+        nat.check(lib.h2g_session_create(prog.steps.ctypes.data_as(ctypes.c_void_p), len(prog.steps),
+                                         max(prog.n_events, 1), ctypes.c_void_p(plan.npd.data_ptr()), plan.depth,
+                                         base.ctypes.data_as(ctypes.c_void_p), nat.stream_ptr(side),
+                                         ctypes.byref(h)), "h2g_session_create")
+        self.handle = h
+        self._status = np.zeros(1, dtype=nat.NPD_STATUS_DT)
+
+    def launch(self, stream=None):
+        nat.check(nat.lib().h2g_session_factor_async(self.handle, nat.stream_ptr(stream)), "h2g_session_factor_async")
+
+    def status(self, stream=None):
+        """None, or (pivot, level, box) of the reported breakdown (synchronizes)."""
+        rc = nat.lib().h2g_session_status(self.handle, nat.stream_ptr(stream),
+                                          self._status.ctypes.data_as(nat.ctypes_void_p()))
+        if rc == nat.H2G_ENPD:
+            st = self._status[0]
+            return int(st["pivot"]), int(st["level"]), int(st["box"])
+        nat.check(rc, "h2g_session_status")
+        return None
+
+    def __del__(self):
+        try:
+            nat.load_library().h2g_session_destroy(self.handle)
+        except Exception:
+            pass
+
+
 class FactorPlan:
     """Device buffers + the static step program(s) of one factorization.
 
@@ -211,6 +255,7 @@ class FactorPlan:
         self.dh2 = dh2
         self.depth = dh2.depth
         self.generation = 0      # bumped whenever the buffers receive new factors (solve inverses follow)
+        self._session = None     # native factorization session (single program), see capture()
         self.part = part
         self.comm = comm
         self.dist = part is not None and part.p > 1
@@ -513,6 +558,9 @@ class FactorPlan:
     # ------------------------------------------------------------------ run / check
     def run(self, stream=None):
         self.generation += 1
+        if self._session is not None:
+            self._session.launch(stream)
+            return
         if self.program is not None:
             self.program.launch(stream)
             return
@@ -557,12 +605,24 @@ class FactorPlan:
         return on_level, finish
 
     def capture(self):
-        """CUDA-graph every program segment (collectives stay outside)."""
+        """Single program (one GPU): a native factorization session (h2g_session_create:
+        the program captured into one CUDA graph, pivot statuses decoded in C).
+        Segmented plans (distributed / streamed): a CUDA graph per program segment,
+        the collectives outside."""
+        if self.program is not None and not self.dist:
+            if self._session is None:
+                self._session = _Session(self)
+            return
         for seg in self.segments:
             if isinstance(seg, Program) and seg.graph is None:
                 seg.capture()
 
     def check_pivots(self):
+        if self._session is not None:
+            st = self._session.status()
+            if st is not None:
+                raise NotPositiveDefiniteError(st[0], level=st[1], box=st[2])
+            return
         if self.comm is not None and self.part is not None and self.part.p > 1:
             self.comm.allreduce_min_(self.npd)
         npd = self.npd.cpu().numpy()
