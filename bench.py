@@ -559,7 +559,7 @@ def main():
                 "data": "synthetic (uniform cube, seed 0)" if c["shape"] == "cube" else "synthetic (sphere, seed 0)",
                 "config": {"workload": workload_name(args.config, c),
                            "parallelism": (f"sharded{world}: boxes of levels >= log2 P split by contiguous leaf "
-                                           f"ranges, top levels + root replicated, {backend} exchanges")
+                                           f"ranges, levels < log2 P by subtree process groups (merge AllReduces per parent near block), {backend} exchanges")
                            if world > 1 else "single GPU",
                            "flops_per_step": flops, "padded_flops": plan.flops["total_padded"],
                            "factor_seconds": ms * 1e-3, "solve_ms_host": solve_ms, "residual": res,
