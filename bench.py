@@ -25,8 +25,10 @@ part of the reference metric).
 
 Multi-GPU (`torchrun ... bench.py --gpus N`): ONE factorization sharded over
 the ranks (distributed.py: boxes of the levels >= log2 N split by contiguous
-leaf ranges, NCCL all_gather of halo / boundary blocks, top levels replicated);
-strong scaling, time = max over ranks.
+leaf ranges, the levels above computed by subtree process groups, NCCL
+all_gather of the V halo and one AllReduce per parent near block at the
+merges — comm_sim.simulate_factor's events); strong scaling, time = max over
+ranks.
 `--impl reference` times the CPU oracle port (the reference is pure Python and
 does not travel to the GPU box) on rank 0 only; each step factors one sampled
 sub-hierarchy (the sample rotates over the 2^L0 subtrees), the warm-up steps
