@@ -64,8 +64,6 @@ typedef struct h2g_gemm_problem {
   int32_t tile_start;
   int32_t flags;
   double alpha, beta;
-  const double* Cin;  /* optional (NULL: C): the beta * Cin term is read from here (ld ldcin) */
-  int32_t ldcin, pad_;
 } h2g_gemm_problem;
 
 int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg); /* tiles one problem needs */
@@ -364,34 +362,6 @@ int h2g_sym_check(const h2g_symcheck_desc* d_descs, int count, unsigned long lon
 int h2g_tri_inv(const h2g_triinv_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int32_t* d_status,
                 void* stream);
 
-/* ---- two-sided basis transform in compact-WY form (diag_mul1/2) --------------
- * For a basis built by the device QR (q_full = [Q[:, k:] | Q[:, :k] S], Q the
- * product of k Householder reflectors, S the sign convention), H = q_full^T
- * A q_full is formed as A - U V^T - V U^T with U = A V T - V (T^T V^T A V T)/2
- * (4 n^2 k flops instead of 4 n^3) and relabelled; these two kernels are the
- * non-GEMM pieces:
- * h2g_wy_t: the k x k upper triangle T of Q = I - V T V^T from the 32-column
- *   panel factors T_p (h2g_qr_panel layout: 32 x 32 each, ld 32) and the Gram
- *   matrix G = V^T V (k x k, ld k); one CTA per box; kmax >= every k.
- * h2g_wy_signs: the signs s_j = sign(R_jj) (R: the factored Z, ld ldr) on the
- *   skeleton rows of H (SR) and both sides of its lower SS block.
- */
-typedef struct h2g_wyt_desc {
-  const double* Tp;
-  const double* G;
-  double* T;
-  int32_t k, pad_;
-} h2g_wyt_desc;
-
-typedef struct h2g_wysign_desc {
-  double* H;
-  const double* R;
-  int32_t r, k, ldh, ldr;
-} h2g_wysign_desc;
-
-int h2g_wy_t(const h2g_wyt_desc* d_descs, int count, int kmax, void* stream);
-int h2g_wy_signs(const h2g_wysign_desc* d_descs, int count, void* stream);
-
 /* ---- native executor ---------------------------------------------------------
  * A factorization is a static list of steps (one batched phase each); the
  * executor issues them back to back on `stream` without returning to
@@ -417,8 +387,6 @@ enum {
   H2G_STEP_CHOL_BOX = 17,   /* descs = cholbox descs; npd = status */
   H2G_STEP_XFORM_T = 18,    /* descs/map = xform descs/tile map; arg = w; count < 0: 16-byte loads */
   H2G_STEP_XFORM_N = 19,    /* descs/map = xform_n descs/tile map; arg = w; count < 0: 16-byte loads */
-  H2G_STEP_WY_T = 20,       /* descs = wyt descs; arg = kmax */
-  H2G_STEP_WY_SIGNS = 21,   /* descs = wysign descs */
   H2G_STEP_KBLOCK = 11   /* descs/map = kblock descs/tile map; aux = points,
                             npd = coincident flag; arg = family; shift/decay
                             in the two doubles                              */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("H2G_LIB_PATH") or os.path.join(HERE, "libh2ulv_b200.s
 # --- descriptor layouts (must match include/h2ulv_b200.h) -------------------------------
 GEMM_DT = np.dtype([("A", "<u8"), ("B", "<u8"), ("C", "<u8"), ("M", "<i4"), ("N", "<i4"), ("K", "<i4"),
                     ("lda", "<i4"), ("ldb", "<i4"), ("ldc", "<i4"), ("tile_start", "<i4"), ("flags", "<i4"),
-                    ("alpha", "<f8"), ("beta", "<f8"), ("Cin", "<u8"), ("ldcin", "<i4"), ("pad_", "<i4")])
+                    ("alpha", "<f8"), ("beta", "<f8")])
 CHOLP_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("ldh", "<i4"), ("ldl", "<i4"), ("n", "<i4"), ("p", "<i4"),
                      ("b", "<i4"), ("npd_slot", "<i4"), ("tile_start", "<i4"), ("pad_", "<i4")])
 ROWS_DT = np.dtype([("Lb", "<u8"), ("Xin", "<u8"), ("Xout", "<u8"), ("Linv", "<u8"), ("pad0_", "<u8"),
@@ -47,22 +47,20 @@ XFORM_DT = np.dtype([("Q", "<u8"), ("x", "<u8"), ("y1", "<u8"), ("y2", "<u8"), (
                      ("ldq", "<i4"), ("tile_start", "<i4")])
 XFORMN_DT = np.dtype([("Q", "<u8"), ("xr", "<u8"), ("xs", "<u8"), ("out", "<u8"), ("n", "<i4"), ("r", "<i4"),
                       ("ldq", "<i4"), ("tile_start", "<i4")])
-WYT_DT = np.dtype([("Tp", "<u8"), ("G", "<u8"), ("T", "<u8"), ("k", "<i4"), ("pad_", "<i4")])
-WYSIGN_DT = np.dtype([("H", "<u8"), ("R", "<u8"), ("r", "<i4"), ("k", "<i4"), ("ldh", "<i4"), ("ldr", "<i4")])
 STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", "<i4"), ("descs", "<u8"),
                     ("map", "<u8"), ("npd", "<u8"), ("aux", "<u8"), ("d0", "<f8"), ("d1", "<f8"),
                     ("lane", "<i4"), ("wait_ev", "<i4"), ("rec_ev", "<i4"), ("pad_", "<i4")])
 
-assert GEMM_DT.itemsize == 88 and COPY_DT.itemsize == 40 and CHOLP_DT.itemsize == 48 and ROWS_DT.itemsize == 72
+assert GEMM_DT.itemsize == 72 and COPY_DT.itemsize == 40 and CHOLP_DT.itemsize == 48 and ROWS_DT.itemsize == 72
 assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 32
-assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 48 and XFORM_DT.itemsize == 48 and XFORMN_DT.itemsize == 48 and WYT_DT.itemsize == 32 and WYSIGN_DT.itemsize == 32
+assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 48 and XFORM_DT.itemsize == 48 and XFORMN_DT.itemsize == 48
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 80
 
 NPD_STATUS_DT = np.dtype([("failed", "<i4"), ("pivot", "<i4"), ("level", "<i4"), ("box", "<i4")])
 H2G_ENPD = 4
 STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "COPY": 5, "MEMCPY": 6,
         "QR_PANEL": 7, "BASIS": 8, "GEMV": 9, "TRSV": 10, "KBLOCK": 11, "NOP": 12, "CHOL_PANEL": 13, "TRSM_ROWS": 14,
-        "SYMCHECK": 15, "TRIINV": 16, "CHOL_BOX": 17, "XFORM_T": 18, "XFORM_N": 19, "WY_T": 20, "WY_SIGNS": 21}
+        "SYMCHECK": 15, "TRIINV": 16, "CHOL_BOX": 17, "XFORM_T": 18, "XFORM_N": 19}
 GEMM_LOWER = 1
 GEMV_PLUS = 1
 GEMV_SPLIT = 2
@@ -77,7 +75,7 @@ EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_chol_panel_tiles", "h2g_ch
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
            "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n",
-           "h2g_wy_t", "h2g_wy_signs", "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy"]
+           "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy"]
 
 _LIB = None
 
@@ -122,8 +120,6 @@ def load_library(path=LIB_PATH):
         "h2g_chol_box": (i32, [vp, i32, vp, vp]),
         "h2g_xform_t": (i32, [vp, vp, i32, i32, i32, vp]),
         "h2g_xform_n": (i32, [vp, vp, i32, i32, i32, vp]),
-        "h2g_wy_t": (i32, [vp, i32, i32, vp]),
-        "h2g_wy_signs": (i32, [vp, i32, vp]),
         "h2g_session_create": (i32, [vp, i32, i32, vp, i32, vp, vp, ctypes.POINTER(vp)]),
         "h2g_session_factor_async": (i32, [vp, vp]),
         "h2g_session_status": (i32, [vp, vp, vp]),

@@ -82,86 +82,7 @@ __global__ void __launch_bounds__(BO_PB) tri_inv_kernel(const h2g_triinv_desc* _
   for (int i = 0; i < BO_PB; ++i) out[(size_t)i * BO_PB + j] = X[i][j];
 }
 
-// Compact-WY triangle of a box's complete Householder QR: Q = Q_1 ... Q_m with
-// Q_p = I - V_p T_p V_p^T (32-column panels, T_p from h2g_qr_panel) is
-// I - V T V^T with T (k x k upper) assembled panel by panel,
-//   T[0:c, c:c+b] = -T[0:c, 0:c] (V_{0:c}^T V_{c:c+b}) T_p        (c = 32 p)
-// from the Gram matrix G = V^T V.  One CTA per box.
-constexpr int WY_QB = 32;
-__global__ void __launch_bounds__(256) wy_t_kernel(const h2g_wyt_desc* __restrict__ descs) {
-  extern __shared__ double b1[];                 // (c x b) scratch, c < k
-  const h2g_wyt_desc D = descs[blockIdx.x];
-  const int k = D.k;
-  double* __restrict__ T = D.T;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e / k, j = e % k, pi = i / WY_QB, pj = j / WY_QB;
-    T[e] = (pi == pj && j >= i) ? D.Tp[(size_t)pi * WY_QB * WY_QB + (i % WY_QB) * WY_QB + (j % WY_QB)] : 0.0;
-  }
-  __syncthreads();
-  for (int c = WY_QB; c < k; c += WY_QB) {
-    const int b = min(WY_QB, k - c);
-    for (int e = threadIdx.x; e < c * b; e += blockDim.x) {      // B1 = G[0:c, c:c+b] T_p
-      const int i = e / b, j = e % b;
-      double acc = 0.0;
-      for (int t = 0; t <= j; ++t) acc = fma(D.G[(size_t)i * k + c + t], T[(size_t)(c + t) * k + c + j], acc);
-      b1[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < c * b; e += blockDim.x) {      // T[0:c, c:c+b] = -T[0:c, 0:c] B1
-      const int i = e / b, j = e % b;
-      double acc = 0.0;
-      for (int t = i; t < c; ++t) acc = fma(T[(size_t)i * k + t], b1[t * b + j], acc);
-      T[(size_t)i * k + c + j] = -acc;
-    }
-    __syncthreads();
-  }
-}
-
-// Sign convention of id_basis (dense_core.py:140-144): s_j = sign(R_jj) (0 -> +1) scales
-// q_skel's column j, so in H = q_full^T A q_full the skeleton rows carry s_a and the SS
-// block s_a s_b.  Applied to the SR rows and the lower SS block of H after the WY
-// transform; one CTA per box.
-__global__ void __launch_bounds__(256) wy_signs_kernel(const h2g_wysign_desc* __restrict__ descs) {
-  const h2g_wysign_desc D = descs[blockIdx.x];
-  const int r = D.r, k = D.k, ld = D.ldh;
-  for (int a = 0; a < k; ++a) {
-    const double ra = D.R[(size_t)a * D.ldr + a];
-    const double sa = ra < 0.0 ? -1.0 : 1.0;
-    double* row = D.H + (size_t)(r + a) * ld;
-    for (int c = threadIdx.x; c <= r + a; c += blockDim.x) {
-      double sc = 1.0;
-      if (c >= r) sc = D.R[(size_t)(c - r) * D.ldr + (c - r)] < 0.0 ? -1.0 : 1.0;
-      const double f = sa * sc;
-      if (f < 0.0) row[c] = -row[c];
-    }
-  }
-}
-
 }  // namespace h2g
-
-extern "C" int h2g_wy_t(const h2g_wyt_desc* d_descs, int count, int kmax, void* stream) {
-  if (count <= 0) return H2G_OK;
-  if (!d_descs) return h2g_set_error(H2G_EINVAL, "h2g_wy_t: null descriptors");
-  const int smem = (int)(sizeof(double) * (size_t)kmax * h2g::WY_QB);
-  if (smem > 200 * 1024) return h2g_set_error(H2G_EINVAL, "h2g_wy_t: k = %d too large", kmax);
-  static int attr_dev = -1, attr_smem = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev || smem > attr_smem) {
-    cudaFuncSetAttribute(h2g::wy_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_dev = dev;
-    attr_smem = smem;
-  }
-  h2g::wy_t_kernel<<<count, 256, smem, (cudaStream_t)stream>>>(d_descs);
-  return h2g_check_launch("wy_t");
-}
-
-extern "C" int h2g_wy_signs(const h2g_wysign_desc* d_descs, int count, void* stream) {
-  if (count <= 0) return H2G_OK;
-  if (!d_descs) return h2g_set_error(H2G_EINVAL, "h2g_wy_signs: null descriptors");
-  h2g::wy_signs_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(d_descs);
-  return h2g_check_launch("wy_signs");
-}
 
 extern "C" int h2g_sym_check(const h2g_symcheck_desc* d_descs, int count, unsigned long long* d_out, void* stream) {
   if (count <= 0) return H2G_OK;

@@ -79,10 +79,6 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
       return h2g_xform_t((const h2g_xform_desc*)s.descs, s.map, s.grid, s.arg, s.count < 0, st);
     case H2G_STEP_XFORM_N:
       return h2g_xform_n((const h2g_xform_n_desc*)s.descs, s.map, s.grid, s.arg, s.count < 0, st);
-    case H2G_STEP_WY_T:
-      return h2g_wy_t((const h2g_wyt_desc*)s.descs, s.count, s.arg, st);
-    case H2G_STEP_WY_SIGNS:
-      return h2g_wy_signs((const h2g_wysign_desc*)s.descs, s.count, st);
     case H2G_STEP_NOP:
       return H2G_OK;
     default:

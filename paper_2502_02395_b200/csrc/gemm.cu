@@ -81,8 +81,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   double* Cp = P.C;  // may alias A (in-place TRSM with N <= 64)
   const int ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
-  const double* Cin = P.Cin ? P.Cin : Cp;     // the beta term's source (default: C itself)
-  const int ldcin = P.Cin ? P.ldcin : ldc;
   // preload beta/alpha * C so the epilogue is a pure store
   // C preload scale beta/alpha: the common +-1 cases stay off the FP64 pipe (it is the DMMA pipe)
   const int cmode = (beta == 0.0 || alpha == 0.0) ? 0 : beta == alpha ? 1 : beta == -alpha ? 2 : 3;
@@ -94,7 +92,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       const int row = m0 + wm * C::WM + i * 8 + g;
       const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) acc[i][j][e] = (cmode && row < M && col + e < N) ? Cin[(size_t)row * ldcin + col + e] : 0.0;
+      for (int e = 0; e < 2; ++e) acc[i][j][e] = (cmode && row < M && col + e < N) ? Cp[(size_t)row * ldc + col + e] : 0.0;
     }
   if (cmode == 2) {
 #pragma unroll
@@ -202,7 +200,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
         double* cp = Cp + (size_t)row * ldc + col;
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (col + e < N) cp[e] = beta * Cin[(size_t)row * ldcin + col + e];
+          if (col + e < N) cp[e] = beta * cp[e];
       }
     }
     return;

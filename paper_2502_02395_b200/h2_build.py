@@ -385,7 +385,6 @@ def _construct(kernel, tree, lists, cfg, cloud, device, workers):
     _check_coincident(flag, kernel, cloud, [(eff[(depth, i)], eff[(depth, j)]) for (i, j) in aoff])
 
     dh2 = DeviceH2(device, depth, cloud.count, levels, q, s, leaf_a, aoff)
-    dh2.householder = lqs          # reflectors / panel factors / R of every basis: the WY diag transform
     h2._device = dh2
     h2._build_keep = (lqs, keep)
     h2._choice = choice

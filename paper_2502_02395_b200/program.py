@@ -145,7 +145,7 @@ class Program:
 
     # -- step constructors ------------------------------------------------------------
     def gemm(self, trans_a, trans_b, problems, tile_cfg=None):
-        """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta[, Cin, ldcin])."""
+        """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta)."""
         rows = [p for p in problems if p[3] > 0 and p[4] > 0]
         if not rows:
             return 0
@@ -154,12 +154,9 @@ class Program:
             if big and small:
                 return self.gemm(trans_a, trans_b, big) + self.gemm(trans_a, trans_b, small, tile_cfg=9)
         arr = np.zeros(len(rows), dtype=nat.GEMM_DT)
-        cols = list(zip(*[p[:12] for p in rows]))
+        cols = list(zip(*rows))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
             arr[name] = col
-        if any(len(p) > 12 for p in rows):         # optional (Cin, ldcin): the beta term's source
-            arr["Cin"] = [p[12] if len(p) > 12 else 0 for p in rows]
-            arr["ldcin"] = [p[13] if len(p) > 12 else 0 for p in rows]
         cfg = (choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b), ks=arr["K"])
                if tile_cfg is None else tile_cfg)
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
@@ -363,29 +360,6 @@ class Program:
         self._add(nat.STEP["XFORM_N"], -len(descs) if vec else len(descs), int(tiles.sum()), self._blob(arr),
                   self._blob(tmap), arg=w, nbytes=nbytes)
         return int(tiles.sum())
-
-    def wy_t(self, descs):
-        """descs: list of (Tp, G, T, k): the compact-WY triangle of each box's Q (h2g_wy_t)."""
-        descs = [d for d in descs if d[3] > 0]
-        if not descs:
-            return 0
-        arr = np.zeros(len(descs), dtype=nat.WYT_DT)
-        for name, col in zip(("Tp", "G", "T", "k"), zip(*descs)):
-            arr[name] = col
-        self._add(nat.STEP["WY_T"], len(descs), len(descs), self._blob(arr), arg=int(arr["k"].max()))
-        return len(descs)
-
-    def wy_signs(self, descs):
-        """descs: list of (H, R, r, k, ldh, ldr): id_basis's sign convention on H (h2g_wy_signs)."""
-        descs = [d for d in descs if d[3] > 0]
-        if not descs:
-            return 0
-        arr = np.zeros(len(descs), dtype=nat.WYSIGN_DT)
-        for name, col in zip(("H", "R", "r", "k", "ldh", "ldr"), zip(*descs)):
-            arr[name] = col
-        self._writes((d[0] + 8 * d[2] * d[4], d[3], d[2] + d[3], d[4], False) for d in descs)
-        self._add(nat.STEP["WY_SIGNS"], len(descs), len(descs), self._blob(arr))
-        return len(descs)
 
     def trsv(self, descs, trans, w):
         """descs: list of (L, Linv, x, n, ldl)."""

@@ -56,9 +56,6 @@ F64 = torch.float64
 CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 CHOL_BOX_V = os.environ.get("H2G_CHOL_BOX_V", "0") == "1"
-# compact-WY diag transform (device-QR bases): on when 4 n^2 k < WY_RATIO x 3 n^3 over a level's boxes
-WY_ENABLED = os.environ.get("H2G_WY", "1") != "0"
-WY_RATIO = float(os.environ.get("H2G_WY_RATIO", "0.6"))
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -358,25 +355,21 @@ class FactorPlan:
                 prog.record(ev_ss)
                 # ---- diagonal phase (lane 0 = the critical chain)
                 prog.lane = 0
-                lq = self._wy_level(l, lay, mine)
-                if lq is not None:
-                    self._wy_transform(prog, B, lq, a_off, ap, mine)
-                else:
-                    prob = []
-                    for i in range(nb):
-                        if not mine[i]:
-                            continue
-                        ni = int(n[i])
-                        prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
-                                     0, 1.0, 0.0))
-                    prog.gemm(0, 0, prob)
-                    # H = Q^T (A Q) is symmetric and only its lower half is ever read
-                    # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
-                    prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
-                             int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
-                    prog.role = "transform"
-                    prog.gemm(1, 0, prob)
-                    prog.role = None
+                prob = []
+                for i in range(nb):
+                    if not mine[i]:
+                        continue
+                    ni = int(n[i])
+                    prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
+                                 0, 1.0, 0.0))
+                prog.gemm(0, 0, prob)
+                # H = Q^T (A Q) is symmetric and only its lower half is ever read
+                # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
+                prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
+                         int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
+                prog.role = "transform"
+                prog.gemm(1, 0, prob)
+                prog.role = None
                 B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
                                                                     Qp=qp)
                 if self.dist and self._cross(l, lay):
@@ -463,88 +456,6 @@ class FactorPlan:
     # ------------------------------------------------------------------ steps
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
         return partial_cholesky_steps(prog, self.device, self.npd.data_ptr(), Hp, Rp, qo, n, r, slot0, mine, Qp)
-
-    def _wy_level(self, l, lay, mine):
-        """The level's LevelQR (reflectors V, panel factors T_p, R) when the compact-WY
-        transform applies: a basis from the device QR (GPU construct) and k small enough
-        that 4 n^2 k < WY_RATIO x 3 n^3 summed over the boxes."""
-        lqs = getattr(self.dh2, "householder", None)
-        if not WY_ENABLED or not lqs or l not in lqs:
-            return None
-        n, k = np.asarray(lay.n, dtype=np.int64)[mine], np.asarray(lay.k, dtype=np.int64)[mine]
-        if not k.size or int(k.max()) > 256 or int(k.max()) == 0:
-            return None
-        if (4 * n * n * k).sum() > WY_RATIO * (3 * n ** 3).sum():
-            return None
-        return lqs[l]
-
-    def _wy_transform(self, prog, B, lq, a_off, ap, mine):
-        """diag_mul1/2 (ulv_factor.py:189-200) for a basis from the device QR:
-        q_full = [Q[:, k:] | Q[:, :k] S] with Q = I - V T V^T (k Householder
-        reflectors), so H' = Q^T A Q = A - U V^T - V U^T, U = A V T - V Y / 2,
-        Y = T^T (V^T A V) T: 4 n^2 k flops (W = A V and one K = 2k lower NT GEMM)
-        instead of 4 n^3; H is H' relabelled ([red | skel] order: three block
-        copies) with id_basis's signs (h2g_wy_signs)."""
-        lay = B.lay
-        n, k, r, qo = lay.n, lay.k, lay.r, lay.qoff
-        dev = self.device
-        boxes = [i for i in range(lay.nb) if mine[i]]
-        nk = np.asarray(n, dtype=np.int64) * np.asarray(k, dtype=np.int64)
-        kk = np.asarray(k, dtype=np.int64) ** 2
-        o_nk = np.concatenate([[0], np.cumsum(nk)[:-1]])
-        o_kk = np.concatenate([[0], np.cumsum(kk)[:-1]])
-        buf = lambda m: torch.empty(max(int(m), 1), dtype=F64, device=dev)
-        Wb, Pb, Qb = buf(nk.sum()), buf(2 * nk.sum()), buf(2 * nk.sum())
-        Gb, Xb, Tb, Z1b, Yb = (buf(kk.sum()) for _ in range(5))
-        B.wy = (Wb, Pb, Qb, Gb, Xb, Tb, Z1b, Yb)
-        p_ = lambda t, off: t.data_ptr() + 8 * int(off)
-        Hp, Mp = B.H.data_ptr(), B.M.data_ptr()
-        wy = [i for i in boxes if k[i] > 0]
-        A = {i: ap + 8 * a_off[(i, i)] for i in boxes}
-        V = {i: lq.ptr(lq.V, lq.zoff[i]) for i in wy}
-        ni = {i: int(n[i]) for i in boxes}
-        ki = {i: int(k[i]) for i in boxes}
-        # W = A V ; G = V^T V, X = V^T W ; T ; Z1 = T^T X ; Y = Z1 T
-        prog.gemm(0, 0, [(A[i], V[i], p_(Wb, o_nk[i]), ni[i], ki[i], ni[i], ni[i], ki[i], ki[i], 0, 1.0, 0.0)
-                         for i in wy])
-        prog.gemm(1, 0, [x for i in wy for x in (
-            (V[i], V[i], p_(Gb, o_kk[i]), ki[i], ki[i], ni[i], ki[i], ki[i], ki[i], 0, 1.0, 0.0),
-            (V[i], p_(Wb, o_nk[i]), p_(Xb, o_kk[i]), ki[i], ki[i], ni[i], ki[i], ki[i], ki[i], 0, 1.0, 0.0))])
-        prog.wy_t([(lq.ptr(lq.T, lq.toff[i]), p_(Gb, o_kk[i]), p_(Tb, o_kk[i]), ki[i]) for i in wy])
-        prog.gemm(1, 0, [(p_(Tb, o_kk[i]), p_(Xb, o_kk[i]), p_(Z1b, o_kk[i]), ki[i], ki[i], ki[i], ki[i], ki[i],
-                          ki[i], 0, 1.0, 0.0) for i in wy])
-        prog.gemm(0, 0, [(p_(Z1b, o_kk[i]), p_(Tb, o_kk[i]), p_(Yb, o_kk[i]), ki[i], ki[i], ki[i], ki[i], ki[i],
-                          ki[i], 0, 1.0, 0.0) for i in wy])
-        # U = W T - V Y / 2 into P[:, :k] and Qm[:, k:];  V into P[:, k:] and Qm[:, :k]
-        P = {i: p_(Pb, 2 * o_nk[i]) for i in wy}
-        Q = {i: p_(Qb, 2 * o_nk[i]) for i in wy}
-        prog.gemm(0, 0, [x for i in wy for x in (
-            (p_(Wb, o_nk[i]), p_(Tb, o_kk[i]), P[i], ni[i], ki[i], ki[i], ki[i], ki[i], 2 * ki[i], 0, 1.0, 0.0),
-            (p_(Wb, o_nk[i]), p_(Tb, o_kk[i]), Q[i] + 8 * ki[i], ni[i], ki[i], ki[i], ki[i], ki[i], 2 * ki[i], 0,
-             1.0, 0.0))])
-        prog.gemm(0, 0, [x for i in wy for x in (
-            (V[i], p_(Yb, o_kk[i]), P[i], ni[i], ki[i], ki[i], ki[i], ki[i], 2 * ki[i], 0, -0.5, 1.0),
-            (V[i], p_(Yb, o_kk[i]), Q[i] + 8 * ki[i], ni[i], ki[i], ki[i], ki[i], ki[i], 2 * ki[i], 0, -0.5, 1.0))])
-        prog.copy([x for i in wy for x in ((V[i], P[i] + 8 * ki[i], ni[i], ki[i], ki[i], 2 * ki[i], 0),
-                                           (V[i], Q[i], ni[i], ki[i], ki[i], 2 * ki[i], 0))])
-        # H' (lower) = A - [U V] [V U]^T  into M
-        prog.gemm(0, 1, [(P[i], Q[i], Mp + 8 * int(qo[i]), ni[i], ni[i], 2 * ki[i], 2 * ki[i], 2 * ki[i], ni[i],
-                          nat.GEMM_LOWER, -1.0, 1.0, A[i], ni[i]) for i in wy])
-        # H = relabel(H'): RR <- H'[k:, k:], SR <- H'[k:, :k]^T, SS <- H'[:k, :k]; k = 0: H = A
-        prog.role = "transform"
-        descs = []
-        for i in boxes:
-            h, m, nn, kk_, rr = Hp + 8 * int(qo[i]), Mp + 8 * int(qo[i]), ni[i], ki[i], int(r[i])
-            if kk_ == 0:
-                descs.append((A[i], h, nn, nn, nn, nn, 0))
-                continue
-            descs.append((m + 8 * (kk_ * nn + kk_), h, rr, rr, nn, nn, 0))
-            descs.append((m + 8 * kk_ * nn, h + 8 * rr * nn, kk_, rr, nn, nn, 1))
-            descs.append((m, h + 8 * (rr * nn + rr), kk_, kk_, nn, nn, 0))
-        prog.copy(descs)
-        prog.role = "transform_fix"   # the sign convention completes the same sparsified block
-        prog.wy_signs([(Hp + 8 * int(qo[i]), lq.ptr(lq.Z, lq.zoff[i]), int(r[i]), ki[i], ni[i], ki[i]) for i in wy])
-        prog.role = None
 
     def _cholesky_steps(self, prog, ptr, d, ld, slot):
         """Root: full Cholesky of the merged d x d block (the solve forms its
@@ -926,7 +837,7 @@ def audit_writes(regions, writes):
             hit(g, "ss", role)
 
     for (_, role, ptr, rows, cols, ld, lower) in writes:
-        if rows <= 0 or cols <= 0 or role == "transform_fix":   # sign normalisation of the same init
+        if rows <= 0 or cols <= 0:
             continue
         g = bisect.bisect_right(starts, ptr) - 1
         if rows == 1 and cols == ld:            # flat copy: every region it overlaps, whole

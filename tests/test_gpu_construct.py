@@ -147,40 +147,3 @@ def test_c2_full_size_flops_and_residual(pkg):
     perm = h2.cloud.perm
     res = np.linalg.norm(pkg.h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b)
     assert res <= 10 * m["residual"], res
-
-
-@pytest.mark.parametrize("family,shape,n,leaf", [("laplace", "cube", 8192, 256), ("yukawa", "sphere", 8192, 128)])
-def test_wy_diag_transform_matches_explicit(pkg, family, shape, n, leaf, monkeypatch):
-    """The compact-WY diag transform (H = A - U V^T - V U^T from the device QR's reflectors,
-    relabelled, id_basis signs) gives the factors of the explicit q_full^T A q_full GEMMs."""
-    from paper_2502_02395_b200 import ulv_factor
-    gen = pkg.gen_uniform_cube if shape == "cube" else pkg.gen_sphere_surface
-    cloud = gen(n, seed=5)
-    tree = pkg.build_tree(cloud, leaf)
-    lists = pkg.build_interaction_lists(tree, 1.0)
-    cfg = pkg.BuildConfig(eta=1.0, leaf_max=leaf, tol=1e-8, s_far=256, s_near=256)
-    h2 = pkg.construct(pkg.KernelSpec(family=family, diagonal_shift=1e4), tree, lists, cfg, cloud)
-    b = np.random.default_rng(3).standard_normal(cloud.count)
-    out = {}
-    for wy in (True, False):
-        monkeypatch.setattr(ulv_factor, "WY_ENABLED", wy)
-        monkeypatch.setattr(ulv_factor, "WY_RATIO", 10.0)      # every level
-        ulv_factor.clear_cache()
-        f = pkg.factorize(h2)
-        used = any(getattr(B, "wy", None) is not None for B in f.device.bufs.values())
-        assert used == wy
-        out[wy] = (f, pkg.solve(f, b))
-        assert {k: f.audit[k] for k in ("offdiag_ss_post_init_writes", "rr_rs_sr_post_init_writes",
-                                        "diag_ss_update_counts")} == {"offdiag_ss_post_init_writes": 0,
-                                                                       "rr_rs_sr_post_init_writes": 0,
-                                                                       "diag_ss_update_counts": [1]}
-    fw, xw = out[True]
-    fe, xe = out[False]
-    rel = lambda a, c: np.linalg.norm(a - c) / max(np.linalg.norm(c), 1e-300)
-    for l in fe.levels:
-        for i in fe.levels[l].lr_diag:
-            assert rel(fw.levels[l].lr_diag[i], fe.levels[l].lr_diag[i]) < 1e-10, (l, i)
-            assert rel(fw.levels[l].ls[(i, i)], fe.levels[l].ls[(i, i)]) < 1e-9, (l, i)
-    assert rel(fw.root, fe.root) < 1e-10
-    assert rel(xw, xe) < 1e-10
-    ulv_factor.clear_cache()
