@@ -365,7 +365,10 @@ def main():
 
     kernel, cloud, tree, lists, cfg = build_problem(pkg, c)
     t0 = time.perf_counter()
-    h2 = pkg.construct(kernel, tree, lists, cfg, cloud, device=dev)
+    # every rank builds the (replicated) H²: share the host cores among the ranks of this node
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    workers = max(1, min(32, (os.cpu_count() or 1) // max(local_world, 1)))
+    h2 = pkg.construct(kernel, tree, lists, cfg, cloud, device=dev, workers=workers)
     construct_s = time.perf_counter() - t0
 
     comm = part = None
