@@ -230,6 +230,16 @@ def _view(t, off, rows, cols, ld):
     return t.as_strided((rows, cols), (ld, 1), t.storage_offset() + off)
 
 
+def _ptr(buf, off):
+    return buf.ptr(off) if hasattr(buf, "ptr") else buf.data_ptr() + 8 * int(off)
+
+
+def _has(buf, off):
+    if not hasattr(buf, "hoff"):
+        return True
+    return buf.lo <= int(off) < buf.hi or int(off) in buf.hoff
+
+
 class _ExchangeProgram:
     """Static pack / unpack of one exchange: ONE block-copy launch gathers this rank's
     exports into the send buffer, ONE scatters the other ranks' blocks out of the
@@ -250,11 +260,11 @@ class _ExchangeProgram:
         for own, t, off, rows, cols, ld in blocks:
             c = int(cursor[own])
             if rows * cols:
-                ptr = t.data_ptr() + 8 * int(off)
                 if own == comm.rank:
-                    pack.append((ptr, self.send.data_ptr() + 8 * c, rows, cols, ld, cols, 0))
-                else:
-                    unpack.append((self.recv.data_ptr() + 8 * (own * self.cap + c), ptr, rows, cols, cols, ld, 0))
+                    pack.append((_ptr(t, off), self.send.data_ptr() + 8 * c, rows, cols, ld, cols, 0))
+                elif _has(t, off):      # a rank keeps only the halo blocks it reads
+                    unpack.append((self.recv.data_ptr() + 8 * (own * self.cap + c), _ptr(t, off), rows, cols, cols,
+                                   ld, 0))
             cursor[own] = c + rows * cols
         self.pack = Program(dev)
         self.pack.copy(pack)

@@ -178,7 +178,7 @@ def plan_from_host_factors(factors):
             o = B.lsoff[(i, j)]
             LS[o:o + kj * ri] = np.asarray(lvl.ls[(j, i)], dtype=np.float64).reshape(-1)
         for dst, src in ((B.H, H), (B.T, T), (B.LSm, LS)):
-            dst.copy_(torch.from_numpy(src))
+            dst.tensor.copy_(torch.from_numpy(src))      # one GPU: the windows span everything
     d = plan.root_dim
     plan.root_buf[:d * d].copy_(torch.from_numpy(np.ascontiguousarray(factors.root, dtype=np.float64).reshape(-1)))
     plan.generation = 1
@@ -187,9 +187,12 @@ def plan_from_host_factors(factors):
 
 
 def _mat(t, off, rows, cols, ld, r0=0, c0=0):
-    """Strided view of a row-major block inside flat tensor `t`, as numpy."""
+    """Strided view of a row-major block inside flat tensor `t` (or a _Win, `off`
+    global), as numpy."""
     if rows == 0 or cols == 0:
         return np.zeros((rows, cols))
+    if isinstance(t, _Win):
+        off, t = t.local(off), t.tensor
     base = off + r0 * ld + c0
     v = t[base: base + (rows - 1) * ld + cols].as_strided((rows, cols), (ld, 1))
     return v.cpu().numpy().copy()
@@ -197,6 +200,42 @@ def _mat(t, off, rows, cols, ld, r0=0, c0=0):
 
 class _LevelBuffers:
     pass
+
+
+class _Win:
+    """A level buffer holding only what this rank touches: a contiguous window
+    [lo, hi) of the level's global offset space (the boxes / pairs it computes)
+    plus individually placed halo blocks (global start offset -> size: the V_j
+    it receives, the off-diagonal factor blocks of cross-group pairs).  One GPU:
+    the whole space, no halo.  `data_ptr()` is the VIRTUAL base, so
+    `data_ptr() + 8 * off` addresses window entries by their global offset;
+    `ptr(off)` also resolves halo blocks."""
+
+    def __init__(self, lo, hi, device, halo=None):
+        halo = {int(o): int(sz) for o, sz in (halo or {}).items() if not (lo <= o < hi)}
+        self.lo, self.hi = int(lo), int(hi)
+        self.hoff, acc = {}, max(self.hi - self.lo, 0)
+        for o in sorted(halo):
+            self.hoff[o] = acc
+            acc += halo[o]
+        self.tensor = torch.empty(max(acc, 1), dtype=F64, device=device)
+
+    def data_ptr(self):
+        return self.tensor.data_ptr() - 8 * self.lo
+
+    def ptr(self, off):
+        off = int(off)
+        if self.lo <= off < self.hi:
+            return self.tensor.data_ptr() + 8 * (off - self.lo)
+        return self.tensor.data_ptr() + 8 * self.hoff[off]
+
+    def local(self, off):
+        """Index into `tensor` of global offset `off` (window or halo block start)."""
+        off = int(off)
+        return off - self.lo if self.lo <= off < self.hi else self.hoff[off]
+
+    def numel(self):
+        return self.tensor.numel()
 
 
 class _Session:
@@ -312,10 +351,19 @@ class FactorPlan:
                 n, k, r = lay.n, lay.k, lay.r
                 nb = lay.nb
                 mine = self.mine(l)
-                qsz = max(lay.qsize, 1)
-                B.M = torch.empty(qsz, dtype=F64, device=dev)
-                B.H = torch.empty(qsz, dtype=F64, device=dev)
-                B.R = torch.empty(qsz, dtype=F64, device=dev)
+                # boxes this rank computes are contiguous (distributed.Partition): H, M and R hold
+                # only them (+ the V_j halo in R), the pair buffers only the own / received pairs
+                mi = np.flatnonzero(mine)
+                sq = np.asarray(n, dtype=np.int64) ** 2
+                wlo, whi = (int(lay.qoff[mi[0]]), int(lay.qoff[mi[-1]] + sq[mi[-1]])) if mi.size else (0, 0)
+                if not self.dist:
+                    wlo, whi = 0, max(lay.qsize, 1)
+                from .distributed import cross_pairs
+                cross = cross_pairs(self.part, l, lay.off_pairs) if self.dist else []
+                halo_r = {int(lay.qoff[j]): int(sq[j]) for (i, j) in cross if mine[i] and not mine[j]}
+                B.M = _Win(wlo, whi, dev)
+                B.H = _Win(wlo, whi, dev)
+                B.R = _Win(wlo, whi, dev, halo_r)
                 B.a, B.aoff = a_buf, a_off
                 qp, Hp, Rp, Mp = dh2.q[l].data_ptr(), B.H.data_ptr(), B.R.data_ptr(), B.M.data_ptr()
                 ap = a_buf.data_ptr()
@@ -334,9 +382,19 @@ class FactorPlan:
                     tacc += int(n[i] * n[j])
                     B.lsoff[(i, j)] = lacc
                     lacc += int(k[j] * r[i])
-                B.MO = torch.empty(max(tacc, 1), dtype=F64, device=dev)
-                B.T = torch.empty(max(tacc, 1), dtype=F64, device=dev)
-                B.LSm = torch.empty(max(lacc, 1), dtype=F64, device=dev)
+                own = [p for p in offp if mine[p[0]]]
+                if not self.dist:
+                    tw, lw = (0, max(tacc, 1)), (0, max(lacc, 1))
+                elif own:
+                    a_, b_ = own[0], own[-1]
+                    tw = (B.toff[a_], B.toff[b_] + int(n[b_[0]] * n[b_[1]]))
+                    lw = (B.lsoff[a_], B.lsoff[b_] + int(k[b_[1]] * r[b_[0]]))
+                else:
+                    tw, lw = (0, 0), (0, 0)
+                recv = [(i, j) for (i, j) in cross if mine[j] and not mine[i]]   # solve_halo targets
+                B.MO = _Win(tw[0], tw[1], dev)
+                B.T = _Win(tw[0], tw[1], dev, {B.toff[p]: int(n[p[0]] * n[p[1]]) for p in recv})
+                B.LSm = _Win(lw[0], lw[1], dev, {B.lsoff[p]: int(k[p[1]] * r[p[0]]) for p in recv})
                 MOp, Tp, LSp = B.MO.data_ptr(), B.T.data_ptr(), B.LSm.data_ptr()
                 own_off = [(i, j) for (i, j) in offp if mine[i]]
                 prog.lane = 2
@@ -384,7 +442,7 @@ class FactorPlan:
                 for ev in (ev_v, ev_ss):
                     if ev is not None:
                         prog.wait(ev)
-                prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], Rp + 8 * qo[j], MOp + 8 * B.toff[(i, j)],
+                prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], B.R.ptr(qo[j]), MOp + 8 * B.toff[(i, j)],
                                   int(n[i]), int(r[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
                                  for (i, j) in own_off])
                 prob = []
@@ -433,6 +491,10 @@ class FactorPlan:
         if not self.dist:
             return np.ones(nb, dtype=bool)
         return self.part.owned_mask(l, self.comm.rank)
+
+    def device_bytes(self):
+        """Bytes of the per-level factorization buffers this rank holds (H, M, R, MO, T, L(s) mirror)."""
+        return sum(8 * getattr(B, x).numel() for B in self.bufs.values() for x in ("H", "M", "R", "MO", "T", "LSm"))
 
     def _cross(self, l, lay):
         from .distributed import cross_pairs
@@ -649,10 +711,12 @@ class FactorPlan:
         nb = lay.nb
         lvl = ULVLevel()
         lvl.dims = {i: (int(r[i]), int(k[i])) for i in range(nb)}
-        lvl.lr_diag = _LazyBlocks(range(nb), lambda i: np.tril(_mat(B.H, int(qo[i]), int(r[i]), int(r[i]), int(n[i]))))
-        lvl.v = _LazyBlocks(range(nb), lambda i: _mat(B.R, int(qo[i]), int(n[i]), int(r[i]), int(n[i])))
-        lvl.lr_off = _LazyBlocks(lay.off_pairs, lambda p: _mat(B.T, B.toff[p], int(r[p[0]]), int(r[p[1]]),
-                                                               int(n[p[1]])))
+        mine = self.mine(l)           # distributed: only the blocks this rank computed
+        boxes = [i for i in range(nb) if mine[i]]
+        pairs = [p for p in lay.off_pairs if mine[p[0]]]
+        lvl.lr_diag = _LazyBlocks(boxes, lambda i: np.tril(_mat(B.H, int(qo[i]), int(r[i]), int(r[i]), int(n[i]))))
+        lvl.v = _LazyBlocks(boxes, lambda i: _mat(B.R, int(qo[i]), int(n[i]), int(r[i]), int(n[i])))
+        lvl.lr_off = _LazyBlocks(pairs, lambda p: _mat(B.T, B.toff[p], int(r[p[0]]), int(r[p[1]]), int(n[p[1]])))
 
         def ls_fetch(key):
             a, b = key
@@ -662,7 +726,7 @@ class FactorPlan:
                 return _mat(B.T, B.toff[(a, b)], int(k[a]), int(r[b]), int(n[b]), r0=int(r[a]))
             return _mat(B.LSm, B.lsoff[(b, a)], int(k[a]), int(r[b]), int(r[b]))
 
-        keys = [(i, i) for i in range(nb)] + list(lay.off_pairs) + [(j, i) for (i, j) in lay.off_pairs]
+        keys = [(i, i) for i in boxes] + list(pairs) + [(j, i) for (i, j) in pairs]
         lvl.ls = _LazyBlocks(keys, ls_fetch)
         return lvl
 

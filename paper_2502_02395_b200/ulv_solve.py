@@ -198,8 +198,8 @@ class SolvePlan:
         if a == b:
             return B.H.data_ptr() + 8 * int(lay.qoff[a] + r[a] * n[a]), int(n[a])
         if a > b:
-            return B.T.data_ptr() + 8 * int(B.toff[(a, b)] + r[a] * n[b]), int(n[b])
-        return B.LSm.data_ptr() + 8 * int(B.lsoff[(b, a)]), int(r[b])
+            return B.T.ptr(B.toff[(a, b)]) + 8 * int(r[a] * n[b]), int(n[b])
+        return B.LSm.ptr(B.lsoff[(b, a)]), int(r[b])
 
     def _ls_keys(self, lay):
         keys = [(i, i) for i in range(lay.nb)] + list(lay.off_pairs) + [(j, i) for (i, j) in lay.off_pairs]
@@ -278,7 +278,7 @@ class SolvePlan:
         nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in below[i])]
         outs = []
         for i in nbr:
-            terms = [(B.T.data_ptr() + 8 * int(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
+            terms = [(B.T.ptr(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
                      for j in below[i] if r[j] > 0]
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
         prog.gemv(outs, w)
@@ -321,7 +321,7 @@ class SolvePlan:
                 if lay.r[i] == 0 or lay.r[j] == 0:
                     continue
                 outs.append((self._p(V["Y"], offR[j]), 0, self._p(V["Y"], offR[j]), int(lay.r[j]), 0, 0,
-                             [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Y"], offR[i]), int(lay.n[i]), 0,
+                             [(B.T.ptr(B.toff[(j, i)]), self._p(V["Y"], offR[i]), int(lay.n[i]), 0,
                                int(lay.r[i]))]))
             prog.gemv(outs, w)
             self._ls_update_forward(prog, l, V, lay, only_b=i)
@@ -347,6 +347,8 @@ class SolvePlan:
             # B1  y_R,i -= sum_a L(s)_ai^T x_S,a
             src = {}
             for (a, b) in self._ls_keys(lay):
+                if not mine[b]:
+                    continue          # the column box is computed elsewhere (its blocks may not be here)
                 ptr, ld = self._ls(l, a, b)
                 src.setdefault(b, []).append((a, (ptr, self._p(xs, offS[a]), ld, 1, int(k[a]))))
             outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0,
@@ -364,7 +366,7 @@ class SolvePlan:
                 nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in above[i])]
                 outs = []
                 for i in nbr:
-                    terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
+                    terms = [(B.T.ptr(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
                 prog.gemv(outs, w)
@@ -389,7 +391,7 @@ class SolvePlan:
         _, above = _near_sets(lay)
         prog.memcpy(V["XR"].data_ptr(), V["YB"].data_ptr(), 8 * int(lay.r.sum()) * w)
         for i in reversed(range(lay.nb)):
-            terms = [(B.T.data_ptr() + 8 * int(B.toff[(j, i)]), self._p(V["XR"], offR[j]), int(lay.n[i]), 1,
+            terms = [(B.T.ptr(B.toff[(j, i)]), self._p(V["XR"], offR[j]), int(lay.n[i]), 1,
                       int(lay.r[j])) for j in above[i] if lay.r[j] > 0]
             if terms:
                 prog.gemv([(self._p(V["XR"], offR[i]), 0, self._p(V["XR"], offR[i]), int(lay.r[i]), 0, 0, terms)], w)

@@ -118,10 +118,11 @@ def _gpu_worker(rank, world, port, q, name):
         root_err = float(np.abs(f.root - g.root).max())
         merges = [[e.phase, e.level, e.kind, list(e.participants), e.bytes] for e in f.comm.trace
                   if e.phase in ("factor", "forward") and e.kind == "allreduce"]
+        frac = f.device.device_bytes() / g.device.device_bytes()
         q.put((rank, root_err, float(np.linalg.norm(x - xg) / np.linalg.norm(xg)),
-               float(np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])), merges))
+               float(np.linalg.norm(x - ref["x"]) / np.linalg.norm(ref["x"])), merges, frac))
     except Exception as e:  # pragma: no cover - surfaced by the assertion below
-        q.put((rank, repr(e), None, None, None))
+        q.put((rank, repr(e), None, None, None, None))
     finally:
         dist.destroy_process_group()
 
@@ -142,7 +143,7 @@ def test_distributed_factor_solve_matches_single_gpu(name, world):
     import json
     gold = json.load(open(os.path.join(ROOT, "tests", "golden", "comm_sim.json")))[name][str(world)]
     golden = gold["factor"] + [e for e in gold["solve"] if e[0] == "forward" and e[2] == "allreduce"]
-    for rank, root_err, xdiff, xref, merges in res:
+    for rank, root_err, xdiff, xref, merges, frac in res:
         assert not isinstance(root_err, str), root_err
         assert root_err == 0.0          # identical tiles, identical arithmetic
         assert xdiff < 1e-12
@@ -150,6 +151,8 @@ def test_distributed_factor_solve_matches_single_gpu(name, world):
         # the merge AllReduces (factorization, forward sweep) this rank took part in = the
         # simulator's events containing it, in order (f)4
         assert merges == [e for e in golden if e[3][0] <= rank < e[3][1]]
+        # per-rank factorization buffers: the computed boxes / pairs plus the halo, not the whole level
+        assert frac < {2: 0.75, 4: 0.5}[world], frac
 
 
 def _structure(name):
