@@ -36,7 +36,10 @@ struct GemmCfg {
 
 // The three configurations the planner chooses from (program.choose_tile_cfg; tile shapes,
 // stage counts and the m16n8k16 variant measured in profiles/r01_gemm_tile_configs*.jsonl):
-using Cfg64b = GemmCfg<64, 64, 2, 2, 4, 2>;     // cfg 2: 4 CTAs/SM, <= 128 registers, 2 stages (transforms)
+#ifndef H2G_GEMM_STAGES
+#define H2G_GEMM_STAGES 2
+#endif
+using Cfg64b = GemmCfg<64, 64, 2, 2, 4, H2G_GEMM_STAGES>;   // cfg 2: 4 CTAs/SM, <= 128 registers (transforms)
 using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // cfg 7: 3 CTAs/SM (170 registers), 2 stages (K <= 64 updates)
 using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // cfg 9: small / ragged problems, 32x32 tiles, 6 CTAs/SM
 
