@@ -126,3 +126,24 @@ def test_breakdown_edges_like_reference(pkg, name):
     assert (e.value.pivot, e.value.level, e.value.box) == (want["pivot"], want["level"], want["box"])
     del h2
     clear_cache()
+
+
+def test_m1_root_breakdown_at_shift_1e5(pkg):
+    """the reference at the metric's N = 1M with shift 1e5 (instead of 2e6)
+    factors all 12 levels and breaks down at the ROOT (level 0, pivot 60).  Same
+    structure through the GPU construct; the breakdown is raised from the native
+    session's status decode with the reference's (pivot, level, box)."""
+    from paper_2502_02395_b200.ulv_factor import clear_cache
+
+    clear_cache()
+    cloud = pkg.gen_uniform_cube(1048576, seed=0)
+    tree = pkg.build_tree(cloud, 256)
+    lists = pkg.build_interaction_lists(tree, 1.0)
+    bc = pkg.BuildConfig(eta=1.0, leaf_max=256, tol=1e-8, s_far=512, s_near=512, seed=0)
+    h2 = pkg.construct(pkg.KernelSpec(family="laplace", diagonal_shift=1e5), tree, lists, bc, cloud)
+    with pytest.raises(pkg.NotPositiveDefiniteError) as e:
+        pkg.factorize(h2)
+    assert (e.value.level, e.value.box) == (0, 0)
+    assert e.value.pivot == 60
+    del h2
+    clear_cache()
