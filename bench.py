@@ -77,6 +77,7 @@ CONFIGS = {
     "m1_tol10": dict(shape="cube", n=1048576, leaf=256, family="laplace", shift=2e6, tol=1e-10, s_far=512,
                      s_near=512),
     "m2": dict(shape="cube", n=2097152, leaf=256, family="laplace", shift=4e6, tol=1e-8, s_far=512, s_near=512),
+    "m4": dict(shape="cube", n=4194304, leaf=256, family="laplace", shift=8e6, tol=1e-8, s_far=512, s_near=512),
 }
 
 
