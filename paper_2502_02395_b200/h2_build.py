@@ -479,8 +479,8 @@ def to_pinned_host(h2):
     out = H2Matrix(tree=h2.tree, lists=h2.lists, kernel=h2.kernel, cloud=h2.cloud, config=h2.config)
     out.skeletons, out.eff_points, out.build_flops = h2.skeletons, h2.eff_points, dict(h2.build_flops)
     base_of = {(kind, l): base for kind, l, base, _ in regions}
-    expected = []
-    bases, near, cpl = {}, {}, {}
+    flag = [False]
+    bases, near, cpl = _TrackedDict(), _TrackedDict(), _TrackedDict()
     for l, lay in dh2.levels.items():
         b0 = base_of[("q", l)]
         lq = lqs[l]
@@ -488,51 +488,90 @@ def to_pinned_host(h2):
         for i in range(lay.nb):
             n, k = int(lay.n[i]), int(lay.k[i])
             r, o = n - k, b0 + int(lay.qoff[i])
-            qr = arena[o:o + n * r].reshape(n, r)
-            qs = arena[o + n * r:o + n * n].reshape(n, k)
             c = h2._choice[(l, i)]
             fr = fr_all[lq.foff[i]:lq.foff[i] + k * k].reshape(k, k)
-            bd = BasisDecomposition(q_skel=qs, q_red=qr, rank=k, frame=fr,
-                                    skeleton=c.skeleton if c is not None else np.zeros(0, dtype=np.int64))
-            bases[(l, i)] = bd
-            expected.append(("bases", (l, i), (bd, qr, qs)))
+            bd = _TrackedBasis(q_skel=arena[o + n * r:o + n * n].reshape(n, k),
+                               q_red=arena[o:o + n * r].reshape(n, r), rank=k, frame=fr,
+                               skeleton=c.skeleton if c is not None else np.zeros(0, dtype=np.int64))
+            object.__setattr__(bd, "_flag", flag)
+            dict.__setitem__(bases, (l, i), bd)
         s0 = base_of[("s", l)]
         for (i, j), o in lay.soff.items():
             blk = arena[s0 + o:s0 + o + int(lay.k[i] * lay.k[j])].reshape(int(lay.k[i]), int(lay.k[j]))
-            cpl[(l, i, j)] = blk
-            expected.append(("couplings", (l, i, j), blk))
+            dict.__setitem__(cpl, (l, i, j), blk)
     a0, leaf = base_of[("a", depth)], dh2.levels[depth]
     for (i, j), o in dh2.aoff.items():
         blk = arena[a0 + o:a0 + o + int(leaf.n[i] * leaf.n[j])].reshape(int(leaf.n[i]), int(leaf.n[j]))
-        near[(depth, i, j)] = blk
-        expected.append(("near_blocks", (depth, i, j), blk))
+        dict.__setitem__(near, (depth, i, j), blk)
+    for d in (bases, near, cpl):
+        d._flag = flag
     out.bases, out.near_blocks, out.couplings = bases, near, cpl
-    out._arena = PinnedArena(arena_t, dh2.signature(), expected)
+    out._arena = PinnedArena(arena_t, dh2.signature(),
+                             {"bases": bases, "near_blocks": near, "couplings": cpl}, flag)
     return out
 
 
-class PinnedArena:
-    """The pinned buffer behind a `to_pinned_host` matrix plus the objects it
-    handed out; `intact(h2)` is true while every block of `h2` is still one of
-    them (a replaced block sends factorize back to the gather path)."""
+class _TrackedDict(dict):
+    """dict that flags its arena when an entry is replaced, added or removed."""
 
-    def __init__(self, tensor, signature, expected):
+    _flag = None
+
+    def _mark(self):
+        if self._flag is not None:
+            self._flag[0] = True
+
+    def __setitem__(self, key, value):
+        self._mark()
+        super().__setitem__(key, value)
+
+    def __delitem__(self, key):
+        self._mark()
+        super().__delitem__(key)
+
+    def _mutator(name):
+        def f(self, *a, **kw):
+            self._mark()
+            return getattr(dict, name)(self, *a, **kw)
+        f.__name__ = name
+        return f
+
+    pop = _mutator("pop")
+    popitem = _mutator("popitem")
+    clear = _mutator("clear")
+    update = _mutator("update")
+    setdefault = _mutator("setdefault")
+    __ior__ = _mutator("__ior__")
+    del _mutator
+
+
+class _TrackedBasis(BasisDecomposition):
+    """BasisDecomposition whose q_red / q_skel are arena views: rebinding either flags the arena."""
+
+    _flag = None
+
+    def __setattr__(self, name, value):
+        if name in ("q_red", "q_skel") and self._flag is not None:
+            self._flag[0] = True
+        object.__setattr__(self, name, value)
+
+
+class PinnedArena:
+    """The pinned buffer behind a `to_pinned_host` matrix plus the containers it
+    handed out.  `intact(h2)` is true while `h2` still holds those containers and
+    no block in them was rebound (a rebound block sends factorize back to the
+    gather path).  O(1): the containers flag their own mutation.  In-place edits
+    of a block's values write through to the buffer, so they stay intact."""
+
+    def __init__(self, tensor, signature, containers, flag):
         self.tensor = tensor
         self.signature = signature
-        self.expected = expected
+        self.containers = containers      # attribute name -> _TrackedDict handed out
+        self._flag = flag                 # [bool], shared with the containers and bases
 
     def intact(self, h2):
-        try:
-            for name, key, obj in self.expected:
-                cur = getattr(h2, name)[key]
-                if name == "bases":
-                    if cur is not obj[0] or cur.q_red is not obj[1] or cur.q_skel is not obj[2]:
-                        return False
-                elif cur is not obj:
-                    return False
-        except KeyError:
+        if self._flag[0]:
             return False
-        return True
+        return all(getattr(h2, name, None) is d for name, d in self.containers.items())
 
 
 # --------------------------------------------------------------------------- matvec

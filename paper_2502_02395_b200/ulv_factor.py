@@ -1061,7 +1061,7 @@ def _factorize_streamed(h2):
     from .h2_device import _signature
 
     arena = getattr(h2, "_arena", None)
-    if arena is not None:      # a to_pinned_host matrix carries its structure signature
+    if arena is not None and arena.intact(h2):   # a to_pinned_host matrix carries its signature
         key = ("stream", arena.signature)
     else:
         key = ("stream", _signature(h2.tree.depth, h2.count, DeviceH2.layouts_from_host(h2)))

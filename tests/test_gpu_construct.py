@@ -134,6 +134,40 @@ def test_device_matvec_matches_host(pkg, family, shape):
         assert np.array_equal(pkg.h2_matvec(to_pinned_host(h2), x), y)
 
 
+def test_pinned_host_arena_tracks_rebinds(pkg):
+    """to_pinned_host: factorize streams from the pinned buffer while the matrix is
+    intact; rebinding a block (dict entry or basis attribute) falls back to the
+    gather path, with the same bits for the same values; in-place edits write
+    through to the buffer and keep it intact."""
+    from paper_2502_02395_b200.h2_build import to_pinned_host
+
+    cloud = pkg.gen_uniform_cube(4096, seed=5)
+    tree = pkg.build_tree(cloud, 128)
+    lists = pkg.build_interaction_lists(tree, 1.0)
+    cfg = pkg.BuildConfig(eta=1.0, leaf_max=128, tol=1e-8, s_far=256, s_near=256)
+    h2 = pkg.construct(pkg.KernelSpec(family="laplace", diagonal_shift=1e4), tree, lists, cfg, cloud)
+    b = np.random.default_rng(2).standard_normal(cloud.count)
+    x0 = pkg.solve(pkg.factorize(h2), b)
+    host = to_pinned_host(h2)
+    assert host._arena.intact(host)
+    assert np.array_equal(pkg.solve(pkg.factorize(host), b), x0)
+    key = next(iter(host.near_blocks))
+    host.near_blocks[key][0, 0] += 0.0                      # in place: still the arena
+    assert host._arena.intact(host)
+    host.near_blocks[key] = host.near_blocks[key].copy()     # rebound entry
+    assert not host._arena.intact(host)
+    assert np.array_equal(pkg.solve(pkg.factorize(host), b), x0)
+    host2 = to_pinned_host(h2)
+    bd = next(iter(host2.bases.values()))
+    bd.q_red = bd.q_red.copy()                               # rebound basis factor
+    assert not host2._arena.intact(host2)
+    assert np.array_equal(pkg.solve(pkg.factorize(host2), b), x0)
+    host3 = to_pinned_host(h2)
+    host3.couplings = dict(host3.couplings)                  # replaced container
+    assert not host3._arena.intact(host3)
+    assert np.array_equal(pkg.solve(pkg.factorize(host3), b), x0)
+
+
 def test_c2_full_size_flops_and_residual(pkg):
     """BASELINE.json configs[1] (C2, N = 65536, sampled 512/512, shift 1e5) at full
     size: the reference's flop report exactly and the solve residual (reference

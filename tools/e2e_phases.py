@@ -1,0 +1,36 @@
+"""Host/device phases of the bench's e2e step (factorize(pinned host H2) + solve(b)) at a config."""
+import sys
+import time
+
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+
+import bench
+import paper_2502_02395_b200 as pkg
+from paper_2502_02395_b200 import ulv_factor
+from paper_2502_02395_b200.h2_build import to_pinned_host
+
+c = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "m1"]
+kernel, cloud, tree, lists, cfg = bench.build_problem(pkg, c)
+h2 = pkg.construct(kernel, tree, lists, cfg, cloud)
+hh = to_pinned_host(h2)
+b = np.random.default_rng(1).standard_normal(c["n"])
+
+
+def T():
+    torch.cuda.synchronize()
+    return time.perf_counter()
+
+
+for rep in range(4):
+    t0 = T()
+    ok = hh._arena.intact(hh)
+    t1 = time.perf_counter()
+    f = pkg.factorize(hh)
+    t2 = T()
+    x = pkg.solve(f, b)
+    t3 = T()
+    print(f"rep {rep}: intact {1e3 * (t1 - t0):.1f} ms (={ok})  factorize {1e3 * (t2 - t1):.1f} ms  "
+          f"solve {1e3 * (t3 - t2):.1f} ms  total {1e3 * (t3 - t0):.1f}", flush=True)
+    del f
