@@ -36,6 +36,7 @@ choose the BLAS thread count.
 """
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -335,6 +336,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="m1", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-exact-residual", action="store_true",
+                    help="skip the direct-sum ||A_exact x - b|| (N^2 kernel evaluations, ~1 s at N = 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -492,6 +495,16 @@ def main():
     solve_ms = (time.perf_counter() - ts0) / 3 * 1e3     # host wall, incl. b / x transfers
     perm = cloud.perm
     res = float(np.linalg.norm(h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b))
+    exact = None
+    if rank == 0 and not args.no_exact_residual:
+        # ||A_exact x - b|| / ||b|| by the GPU direct sum (no N^2 matrix): the true accuracy
+        from paper_2502_02395_b200.direct_sum import exact_residual
+
+        torch.cuda.synchronize(dev)
+        tx0 = time.perf_counter()
+        exact = {"residual": exact_residual(kernel, cloud, x, b, device=dev)}
+        exact["seconds"] = time.perf_counter() - tx0
+        exact["pairs_per_s"] = float(c["n"]) ** 2 / exact["seconds"]
     solve = None
     if world == 1:
         # device-timed forward + backward sweeps (graph replays), operands in HBM
@@ -515,35 +528,6 @@ def main():
                  "note": "SURVEY §8(d) bytes (w = 1): every basis / factor block read once per sweep; "
                          "forward + backward CUDA graphs replayed back to back, CUDA events"}
 
-    # ---- e2e through the public API with host buffers (the H² blocks in pinned host memory)
-    from paper_2502_02395_b200.h2_build import to_pinned_host
-
-    h2_host = to_pinned_host(h2)
-    hb = h2d_bytes(h2_host) + b.nbytes
-    e2e_times = []
-    for s_ in range(1 + args.e2e_steps):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        fe = factor_fn(h2_host)
-        xe = solve_fn(fe, b)
-        torch.cuda.synchronize(dev)
-        if s_:
-            e2e_times.append(time.perf_counter() - t0)
-        del fe
-    e2e_s = float(np.mean(e2e_times))
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
-           "d2h_bytes_per_step": int(xe.nbytes + plan.npd.numel() * 4), "seconds_per_step": e2e_s,
-           "includes": "factorize(h2): the reference's numpy H2Matrix data model, its blocks in one pinned host "
-                       "buffer (to_pinned_host); H2D of bases / leaf near blocks / couplings level by level on a "
-                       "copy stream, each level's factorization graph queued behind its level's copies (upload "
-                       "and factorization overlap), pivot-status D2H; solve(b): H2D b, forward/backward graphs, "
-                       "D2H x. The symbolic part (layout, descriptors, CUDA graphs) is cached per structure, the "
-                       "numeric upload is redone every step"}
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSampler(host_copy(pkg, h2))
@@ -557,6 +541,51 @@ def main():
                "sample": smp.describe(args.config) + f" (box 0 here); oracle/h2ulv_oracle.py, fastest of "
                          f"{thread_candidates()} BLAS threads: {th} threads, {dt:.2f} s for {fl:.3e} flops"}
 
+    # ---- e2e through the public API with host buffers (the H² blocks in pinned host memory)
+    from paper_2502_02395_b200.h2_build import to_pinned_host
+
+    padded, root_dim, npd_n = plan.flops["total_padded"], plan.root_dim, plan.npd.numel()
+    launches = sum(pg.kernel_launches for pg in progs) * args.steps
+    # the e2e leg builds its own (streamed) plan: release the device-resident one first
+    # so the largest configs hold one factorization in HBM at a time
+    sp = f = plan = progs = work = None
+    gc.collect()
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    e2e = None
+    h2_host = to_pinned_host(h2)
+    hb = h2d_bytes(h2_host) + b.nbytes
+    l2_note = (f"inputs > L2 (leaf near blocks + bases {h2d_bytes(h2_host) / 1e9:.2f} GB per step "
+               f"vs 126 MB L2)")
+    if args.e2e_steps > 0:     # the device-built H² is not needed any more: free its HBM too
+        h2 = None
+        gc.collect()
+        torch.cuda.empty_cache()
+    e2e_times = []
+    for s_ in range(1 + args.e2e_steps if args.e2e_steps > 0 else 0):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        fe = factor_fn(h2_host)
+        xe = solve_fn(fe, b)
+        torch.cuda.synchronize(dev)
+        if s_:
+            e2e_times.append(time.perf_counter() - t0)
+        del fe
+    if e2e_times:
+        e2e_s = float(np.mean(e2e_times))
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(hb),
+           "d2h_bytes_per_step": int(xe.nbytes + npd_n * 4), "seconds_per_step": e2e_s,
+           "includes": "factorize(h2): the reference's numpy H2Matrix data model, its blocks in one pinned host "
+                       "buffer (to_pinned_host); H2D of bases / leaf near blocks / couplings level by level on a "
+                       "copy stream, each level's factorization graph queued behind its level's copies (upload "
+                       "and factorization overlap), pivot-status D2H; solve(b): H2D b, forward/backward graphs, "
+                       "D2H x. The symbolic part (layout, descriptors, CUDA graphs) is cached per structure, the "
+                       "numeric upload is redone every step"}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -567,14 +596,14 @@ def main():
                            "parallelism": (f"sharded{world}: boxes of levels >= log2 P split by contiguous leaf "
                                            f"ranges, levels < log2 P by subtree process groups (merge AllReduces per parent near block), {backend} exchanges")
                            if world > 1 else "single GPU",
-                           "flops_per_step": flops, "padded_flops": plan.flops["total_padded"],
+                           "flops_per_step": flops, "padded_flops": padded,
                            "factor_seconds": ms * 1e-3, "solve_ms_host": solve_ms, "residual": res,
+                           "exact_residual": exact,
                            "construct_seconds": construct_s, "eager_ms_per_step": eager_ms,
-                           "l2": f"inputs > L2 (leaf near blocks + bases {h2d_bytes(h2_host) / 1e9:.2f} GB per step "
-                                 f"vs 126 MB L2)",
-                           "depth": tree.depth, "root_dim": plan.root_dim},
+                           "l2": l2_note,
+                           "depth": tree.depth, "root_dim": root_dim},
                 "roofline": roofline, "solve": solve, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": sum(pg.kernel_launches for pg in progs) * args.steps}
+                "gpu_launches": launches}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -190,6 +190,7 @@ int h2g_block_copy(const h2g_copy_desc* d_descs, const int32_t* d_tile_map,
  * rows [split, m) -> y2 (the basis transform of _transform_in,
  * ulv_solve.py:33-41, split = r).  Terms of output o are
  * d_terms[term_begin .. term_end).  With H2G_GEMV_PLUS the sum is added.
+ * A term with A == NULL is the identity (K = m): x_t is added as is.
  * Each output is split into 64-row chunks, one CTA each (chunk_start =
  * running sum of ceil(m / 64)).
  * Replaces the per-box numpy products of _forward/_backward
@@ -331,6 +332,21 @@ typedef struct h2g_kblock_desc {
 int h2g_kernel_blocks(const h2g_kblock_desc* d_descs, const int32_t* d_tile_map, int total_tiles,
                       const double* d_points, int family, double shift, double decay,
                       int64_t* d_coincident, void* stream);
+
+/* ---- direct-sum exact-kernel product -------------------------
+ * y = A x for the EXACT kernel matrix of n points (row-major n x 3, the
+ * cloud's tree order): A_ij = K(|p_i - p_j|) for i != j with the families of
+ * h2g_kernel_blocks, A_ii = shift (oracle.dense_assemble + a dense product,
+ * oracle.py:34-64, without forming A).  x, y row-major n x nrhs.
+ * d_work >= h2g_direct_matvec_workspace(n) doubles (current device); the
+ * partial sums are reduced in a fixed order, so y is deterministic.  A
+ * second point at distance 0 from any point sets d_coincident[0] = 1
+ * (CoincidentPointsError on the host).  Two launches per 4 columns.
+ */
+int64_t h2g_direct_matvec_workspace(int64_t n);
+int h2g_direct_matvec(const double* d_points, const double* d_x, double* d_y, int64_t n, int nrhs, int family,
+                      double shift, double decay, double* d_work, int64_t work_elems, int64_t* d_coincident,
+                      void* stream);
 
 /* ---- single-block API support (dense_core.cholesky / tri_solve) -------------
  * h2g_sym_check: one CTA per matrix; d_out[2q] = max_{i>j} |A_ij - A_ji|,

@@ -17,6 +17,8 @@ scipy 1.18.1 / numpy 2.3.5 with scipy-openblas 0.3.30 in this image):
   h2_matvec      h2_build.py:232-282
   complete_qr    dense_core.py:136-148 (the ① complementary basis)
   flop model     dense_core.py:166-181 / 229-248
+  dense_assemble oracle.py:34-40 (the dense kernel matrix, capped) and the
+                 exact residual / refinement checks built on it
 
 Parity pinned: tests/test_oracle.py checks this module against golden
 vectors produced by running the reference itself (tests/golden/make_golden.py):
@@ -338,6 +340,27 @@ def residual(h2, x, b):
     """||A x - b|| / ||b|| through the H² matvec in tree order (cli.py:199-205)."""
     perm = h2.cloud.perm
     r = h2_matvec(h2, np.asarray(x)[perm]) - np.asarray(b)[perm]
+    return float(np.linalg.norm(r) / np.linalg.norm(b))
+
+
+DENSE_CAP = 16384
+
+
+def dense_assemble(kernel, cloud, cap=DENSE_CAP):
+    """Full N x N kernel matrix in the cloud's current (tree) order
+    (oracle.py:34-40: gen_block over all points, capped)."""
+    from paper_2502_02395_b200 import kernels
+
+    n = cloud.count
+    if n > cap:
+        raise ValueError(f"N = {n} exceeds the dense-oracle cap {cap}")
+    idx = np.arange(n, dtype=np.int64)
+    return kernels.gen_block(kernel, idx, idx, cloud)
+
+
+def exact_residual(a_tree, perm, x, b):
+    """||A x - b|| / ||b|| with the dense matrix A in tree order, x / b in input order."""
+    r = a_tree @ np.asarray(x)[perm] - np.asarray(b)[perm]
     return float(np.linalg.norm(r) / np.linalg.norm(b))
 
 

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libh2ulv_b200.so")
-SOURCES = ["capi.cu", "gemm.cu", "panel.cu", "gather.cu", "solve.cu", "qr.cu", "kblock.cu", "blockops.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "panel.cu", "gather.cu", "solve.cu", "qr.cu", "kblock.cu", "blockops.cu", "directsum.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]

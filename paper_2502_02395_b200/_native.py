@@ -75,7 +75,8 @@ EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_chol_panel_tiles", "h2g_ch
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
            "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n",
-           "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy"]
+           "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy",
+           "h2g_direct_matvec_workspace", "h2g_direct_matvec"]
 
 _LIB = None
 
@@ -124,6 +125,9 @@ def load_library(path=LIB_PATH):
         "h2g_session_factor_async": (i32, [vp, vp]),
         "h2g_session_status": (i32, [vp, vp, vp]),
         "h2g_session_destroy": (i32, [vp]),
+        "h2g_direct_matvec_workspace": (ctypes.c_int64, [ctypes.c_int64]),
+        "h2g_direct_matvec": (i32, [vp, vp, vp, ctypes.c_int64, i32, i32, ctypes.c_double, ctypes.c_double, vp,
+                                    ctypes.c_int64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

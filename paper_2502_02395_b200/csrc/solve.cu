@@ -54,7 +54,14 @@ __global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) ge
       const double* __restrict__ A = T.A;
       const double* __restrict__ x = T.x;
       const int K = T.K, lda = T.lda;
-      if (!T.trans) {
+      if (A == nullptr) {
+        // identity term (K == m): acc += x[rows of this chunk]
+        for (int e = tid; e < nr * wc; e += GV_THREADS) {
+          const int rr = e / wc, j = e % wc;
+          acc[rr * GV_W + j] += x[(size_t)(r0 + rr) * w + j0 + j];
+        }
+        __syncthreads();
+      } else if (!T.trans) {
         // A is m x K: warp per output row, lanes over the contiguous K axis
         for (int rr = warp; rr < nr; rr += NW) {
           const double* arow = A + (size_t)(r0 + rr) * lda;

@@ -302,11 +302,65 @@ class Program:
         self._add(nat.STEP["BASIS"], len(descs), len(descs), self._blob(arr))
         return len(descs)
 
-    def gemv(self, outs, w):
-        """outs: list of (y, y2, init, m, split, flags, [terms...]) with terms (A, x, lda, trans, K)."""
+    def gemv(self, outs, w, balance=0):
+        """outs: list of (y, y2, init, m, split, flags, [terms...]) with terms (A, x, lda, trans, K).
+
+        balance > 0: when the launch has fewer than `balance` 64-row chunks (CTAs), outputs
+        with several terms are split into contiguous term groups of about equal bytes, each
+        summed into its own partial vector by one launch, and a second launch forms
+        y = init -/+ (P_1 + ... + P_p) with identity terms.  The summation order is fixed
+        by the structure (term order, then group order), so results stay deterministic."""
         outs = [o for o in outs if o[3] > 0]
         if not outs:
             return 0
+        if balance:
+            outs, final = self._balance_gemv(outs, w, balance)
+            n = self._gemv_step(outs, w)
+            if final:
+                self._gemv_step(final, w)
+            return n
+        return self._gemv_step(outs, w)
+
+    def _balance_gemv(self, outs, w, target):
+        chunk = nat.GEMV_CHUNK
+        nchunks = sum(-(-int(o[3]) // chunk) for o in outs)
+        if nchunks >= target:
+            return outs, []
+        obytes = [8 * int(o[3]) * sum(int(t[4]) for t in o[6]) for o in outs]
+        per_cta = max(sum(obytes) / target, 1.0)
+        plan = []
+        for o, by in zip(outs, obytes):
+            m, terms = int(o[3]), o[6]
+            p = min(len(terms), max(1, int(round(by / (per_cta * -(-m // chunk))))))
+            if p <= 1:
+                plan.append((o, None))
+                continue
+            tb = np.cumsum([8 * m * int(t[4]) for t in terms], dtype=np.float64)
+            cuts = sorted({int(np.searchsorted(tb, by * q / p, side="left")) for q in range(1, p)})
+            bounds = [0] + [c + 1 for c in cuts if 0 <= c < len(terms) - 1] + [len(terms)]
+            groups = [terms[a:b] for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+            plan.append((o, groups) if len(groups) > 1 else (o, None))
+        elems = sum(int(o[3]) * w * len(g) for o, g in plan if g)
+        if elems == 0:
+            return outs, []
+        part = torch.empty(elems, dtype=torch.float64, device=self.device)
+        self._keep.append(part)
+        base = part.data_ptr()
+        new, final = [], []
+        for o, groups in plan:
+            if groups is None:
+                new.append(o)
+                continue
+            y, y2, init, m, split, flags, _ = o
+            ids = []
+            for g in groups:
+                new.append((base, 0, 0, m, 0, nat.GEMV_PLUS, list(g)))
+                ids.append((0, base, 0, 0, m))
+                base += 8 * int(m) * w
+            final.append((y, y2, init, m, split, flags, ids))
+        return new, final
+
+    def _gemv_step(self, outs, w):
         oarr = np.zeros(len(outs), dtype=nat.GEMV_OUT_DT)
         tl = []
         chunks = 0

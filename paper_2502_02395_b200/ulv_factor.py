@@ -177,7 +177,18 @@ def plan_from_host_factors(factors):
             kj = nj - rj
             o = B.lsoff[(i, j)]
             LS[o:o + kj * ri] = np.asarray(lvl.ls[(j, i)], dtype=np.float64).reshape(-1)
-        for dst, src in ((B.H, H), (B.T, T), (B.LSm, LS)):
+        bufs = [(B.H, H), (B.T, T), (B.LSm, LS)]
+        vs = getattr(lvl, "v", None) or {}
+        if plan.has_v and all(i in vs for i in range(lay.nb) if r[i] > 0):
+            R = np.zeros(B.R.numel())        # V_i (n_i x r_i, ulv_factor.py:31) where the factorization puts it
+            for i in range(lay.nb):
+                ni, ri = int(n[i]), int(r[i])
+                if ri:
+                    R[int(lay.qoff[i]):int(lay.qoff[i]) + ni * ni].reshape(ni, ni)[:, :ri] = vs[i]
+            bufs.append((B.R, R))
+        else:
+            plan.has_v = False
+        for dst, src in bufs:
             dst.tensor.copy_(torch.from_numpy(src))      # one GPU: the windows span everything
     d = plan.root_dim
     plan.root_buf[:d * d].copy_(torch.from_numpy(np.ascontiguousarray(factors.root, dtype=np.float64).reshape(-1)))
@@ -294,6 +305,7 @@ class FactorPlan:
         self.dh2 = dh2
         self.depth = dh2.depth
         self.generation = 0      # bumped whenever the buffers receive new factors (solve inverses follow)
+        self.has_v = True        # R holds V_i = q_red L^-T (the factorization forms it; host uploads may not)
         self._session = None     # native factorization session (single program), see capture()
         self.part = part
         self.comm = comm

@@ -16,6 +16,7 @@ segments of level l-1 (n_p = k_2p + k_2p+1), so the merge
 `segs[p] = vstack(b_S,2p, b_S,2p+1)` (ulv_solve.py:113) costs nothing.
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -24,6 +25,10 @@ import torch
 from .trace import ranged
 from . import _native as nat
 from .program import Program
+
+# grouped GEMVs with fewer 64-row chunks than this are split over their terms
+# (Program.gemv balance): the upper levels' few outputs with many neighbour terms
+GEMV_BALANCE = int(os.environ.get("H2G_GEMV_BALANCE", "296"))
 
 F64 = torch.float64
 
@@ -75,6 +80,13 @@ class SolvePlan:
                              offS=np.concatenate([[0], np.cumsum(lay.k)[:-1]]).astype(np.int64),
                              offX=np.concatenate([[0], np.cumsum(lay.n)[:-1]]).astype(np.int64))
         self.dist = fplan.part is not None and fplan.part.p > 1
+        # The stored V_i = q_red L_ii^-T (ulv_factor.py:31) folds triangular solves into the
+        # basis transforms: backward B3 q_red L_ii^-T t + q_skel x_S = [V_i | q_skel] [t; x_S]
+        # on every level, and on levels whose boxes have no near neighbour (every third level
+        # of a cube tree, the N = 1M leaf among them) forward P1 z_i = V_i^T b_i = y_i too, so
+        # such a level has no TRSV at all.  The prepare step puts q_skel next to V_i in R.
+        self.use_v = mode == "parallel" and fplan.has_v
+        self.fused = {l: self.use_v and not fplan.bufs[l].lay.off_pairs for l in range(depth, 0, -1)}
         self._build_prepare()
         self._segs = []
         self._masks = {}
@@ -91,8 +103,9 @@ class SolvePlan:
         diagonal blocks of every L(r)_ii; the root's explicit W = L_00^-T by
         the row solve of the identity), not taken from the Cholesky's own
         by-products.  The solve is then a pure function of the factor blocks
-        (lr_diag, lr_off, ls, root) — like the reference's — so factors read
-        back from storage solve to the same bits (test_storage.py:90-98)."""
+        (lr_diag, lr_off, ls, v, root; ulv_factor.py:27-43) — like the
+        reference's — so factors read back from storage solve to the same bits
+        (test_storage.py:90-98)."""
         fp = self.fp
         dev = self.device
         W = nat.PANEL_WIDTH
@@ -107,9 +120,16 @@ class SolvePlan:
             lt = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
             self.linv[l], self.loff[l] = lt, loff
             mine = self._mine(l)
+            # (also on fused levels: it is what detects a singular L(r)_ii, SingularTriangularError)
             prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
                           int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
                         self._tri_status.data_ptr())
+            if self.use_v:
+                # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
+                q = fp.dh2.q[l]
+                prog.copy([(q.data_ptr() + 8 * int(lay.qoff[i] + lay.r[i]), B.R.ptr(int(lay.qoff[i] + lay.r[i])),
+                            int(lay.n[i]), int(lay.k[i]), int(lay.n[i]), int(lay.n[i]), 0)
+                           for i in range(lay.nb) if mine[i] and lay.k[i] > 0])
         d = fp.root_dim
         nb0 = -(-d // W)
         self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
@@ -244,6 +264,30 @@ class SolvePlan:
             below, _ = _near_sets(lay)
             q = fp.dh2.q[l]
             mine = self._mine(l)
+            if self.fused[l]:
+                # G1 + P1 + P3 of a level without near neighbours: [y_R; b_S] = [V | q_skel]^T seg
+                R = fp.bufs[l].R
+                prog.xform_t([(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Y"], offR[i]),
+                               self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
+                              for i in range(nb) if mine[i]], w)
+                if self.dist:
+                    prog = self._cut(prog, ("Y", l, "offR"))
+                self._ls_update_forward(prog, l, V, lay, owned=mine)     # P4
+                if self.dist and l - 1 < fp.part.L0:
+                    prog = self._cut(prog, ("BS", l, "offS"))
+                xin = V["BS"]
+                continue
+            if self.use_v:
+                # G1 + P1: [z; b_S] = [V | q_skel]^T seg  (z_i = L_ii^-1 q_red^T seg_i)
+                R = fp.bufs[l].R
+                prog.xform_t([(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Z"], offR[i]),
+                               self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
+                              for i in range(nb) if mine[i]], w)
+                prog = self._forward_parallel_level_v(prog, l, V, lay, below)
+                if self.dist and l - 1 < fp.part.L0:
+                    prog = self._cut(prog, ("BS", l, "offS"))
+                xin = V["BS"]
+                continue
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
             prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), self._p(V["BR"], offR[i]),
                            self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i])) for i in range(nb) if mine[i]], w)
@@ -281,12 +325,38 @@ class SolvePlan:
             terms = [(B.T.ptr(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
                      for j in below[i] if r[j] > 0]
             outs.append((self._p(V["Y"], offR[i]), 0, self._p(V["BR"], offR[i]), int(r[i]), 0, 0, terms))
-        prog.gemv(outs, w)
+        prog.gemv(outs, w, balance=GEMV_BALANCE)
         prog.trsv([self._tr(l, i, self._p(V["Y"], offR[i])) for i in nbr], 0, w)
         if dist:
             prog = self._cut(prog, ("Y", l, "offR"))
         # P4  b_S,a -= sum_b L(s)_ab y_b
         self._ls_update_forward(prog, l, V, lay, owned=mine)
+        return prog
+
+    def _forward_parallel_level_v(self, prog, l, V, lay, below):
+        """P1-P3 with Z = L^-1 b_R already formed through V (the transform):
+        y_i = L_ii^-1 (b_R,i - u_i) = z_i - L_ii^-1 u_i, u_i = sum_{j<i near} L(r)_ij z_j,
+        so only the boxes with lower near neighbours run a TRSV (on u_i)."""
+        w = self.w
+        n, r, nb = lay.n, lay.r, lay.nb
+        offR = V["offR"]
+        B = self.fp.bufs[l]
+        mine = self._mine(l)
+        if self.dist:
+            prog = self._cut(prog, ("Z", l, "offR"))
+        prog.memcpy(V["Y"].data_ptr(), V["Z"].data_ptr(), 8 * int(r.sum()) * w)
+        nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in below[i])]
+        if nbr:
+            U = V["BR"]          # free on this path: holds u_i, then L_ii^-1 u_i
+            prog.gemv([(self._p(U, offR[i]), 0, 0, int(r[i]), 0, nat.GEMV_PLUS,
+                        [(B.T.ptr(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
+                         for j in below[i] if r[j] > 0]) for i in nbr], w, balance=GEMV_BALANCE)
+            prog.trsv([self._tr(l, i, self._p(U, offR[i])) for i in nbr], 0, w)
+            prog.gemv([(self._p(V["Y"], offR[i]), 0, self._p(V["Z"], offR[i]), int(r[i]), 0, 0,
+                        [(0, self._p(U, offR[i]), 0, 0, int(r[i]))]) for i in nbr], w)
+        if self.dist:
+            prog = self._cut(prog, ("Y", l, "offR"))
+        self._ls_update_forward(prog, l, V, lay, owned=mine)     # P4
         return prog
 
     def _ls_update_forward(self, prog, l, V, lay, only_b=None, owned=None):
@@ -305,7 +375,7 @@ class SolvePlan:
         outs = [(self._p(V["BS"], offS[a]), 0, self._p(V["BS"], offS[a]), int(lay.k[a]), 0, 0,
                  [tm for _, tm in sorted(t, key=lambda x: x[0])])
                 for a, t in sorted(terms.items())]
-        prog.gemv(outs, w)
+        prog.gemv(outs, w, balance=GEMV_BALANCE)
 
     def _forward_naive_level(self, prog, l, V, lay):
         """Algorithm 3 order (ulv_solve.py:90-97): box by box."""
@@ -323,7 +393,7 @@ class SolvePlan:
                 outs.append((self._p(V["Y"], offR[j]), 0, self._p(V["Y"], offR[j]), int(lay.r[j]), 0, 0,
                              [(B.T.ptr(B.toff[(j, i)]), self._p(V["Y"], offR[i]), int(lay.n[i]), 0,
                                int(lay.r[i]))]))
-            prog.gemv(outs, w)
+            prog.gemv(outs, w, balance=GEMV_BALANCE)
             self._ls_update_forward(prog, l, V, lay, only_b=i)
 
     # -------------------------------------------------------------- backward
@@ -354,28 +424,44 @@ class SolvePlan:
             outs = [(self._p(V["YB"], offR[i]), 0, self._p(V["Y"], offR[i]), int(r[i]), 0, 0,
                      [tm for _, tm in sorted(src.get(i, []), key=lambda x: x[0])])
                     for i in range(nb) if mine[i]]
-            prog.gemv(outs, w)
+            prog.gemv(outs, w, balance=GEMV_BALANCE)
+            if self.fused[l]:
+                # B2 + B3 without near neighbours: full_i = [V_i | q_skel_i] [y_R,i; x_S,i]
+                R = B.R
+                prog.xform_n([(R.ptr(int(lay.qoff[i])), self._p(V["YB"], offR[i]), self._p(xs, offS[i]),
+                               self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
+                              for i in range(nb) if mine[i]], w)
+                xs = V["FULL"]
+                continue
             if self.mode == "parallel":
                 _, above = _near_sets(lay)
                 prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
                 prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
                 if dist:
                     prog = self._cut(prog, ("Z2", l, "offR"))
-                # boxes without upper near neighbours: x_R,i = z2_i (same TRSV, same input)
-                prog.memcpy(V["XR"].data_ptr(), V["Z2"].data_ptr(), 8 * int(r.sum()) * w)
+                # boxes without upper near neighbours: x_R,i = z2_i (same TRSV, same input);
+                # with V, XR carries t_i = y_R,i instead (B3 applies L^-T through V)
+                prog.memcpy(V["XR"].data_ptr(), (V["YB"] if self.use_v else V["Z2"]).data_ptr(),
+                            8 * int(r.sum()) * w)
                 nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in above[i])]
                 outs = []
                 for i in nbr:
                     terms = [(B.T.ptr(B.toff[(j, i)]), self._p(V["Z2"], offR[j]), int(n[i]), 1,
                               int(r[j])) for j in above[i] if r[j] > 0]
                     outs.append((self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0, terms))
-                prog.gemv(outs, w)
-                prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in nbr], 1, w)
+                prog.gemv(outs, w, balance=GEMV_BALANCE)
+                if not self.use_v:
+                    prog.trsv([self._tr(l, i, self._p(V["XR"], offR[i])) for i in nbr], 1, w)
             else:
                 self._backward_naive_level(prog, l, V, lay)
-            # B3  full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]
-            q = fp.dh2.q[l]
-            prog.xform_n([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(V["XR"], offR[i]), self._p(xs, offS[i]),
+            # B3  full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]; with the stored V_i
+            # (use_v): x_R,i = L_ii^-T t_i, so q_red x_R,i = V_i t_i and full_i = [V_i | q_skel_i] [t_i; x_S,i]
+            # — XR holds t_i (the second TRSV is not run)
+            if self.use_v:
+                qptr = {i: B.R.ptr(int(lay.qoff[i])) for i in range(nb) if mine[i]}
+            else:
+                qptr = {i: fp.dh2.q[l].data_ptr() + 8 * int(lay.qoff[i]) for i in range(nb) if mine[i]}
+            prog.xform_n([(qptr[i], self._p(V["XR"], offR[i]), self._p(xs, offS[i]),
                            self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
                           for i in range(nb) if mine[i]], w)
             xs = V["FULL"]
