@@ -191,6 +191,8 @@ int h2g_block_copy(const h2g_copy_desc* d_descs, const int32_t* d_tile_map,
  * ulv_solve.py:33-41, split = r).  Terms of output o are
  * d_terms[term_begin .. term_end).  With H2G_GEMV_PLUS the sum is added.
  * A term with A == NULL is the identity (K = m): x_t is added as is.
+ * d_chunk_map (optional, NULL = binary search over chunk_start): output index
+ * of every chunk.
  * Each output is split into 64-row chunks, one CTA each (chunk_start =
  * running sum of ceil(m / 64)).
  * Replaces the per-box numpy products of _forward/_backward
@@ -219,7 +221,7 @@ typedef struct h2g_gemv_out {
 } h2g_gemv_out;
 
 int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
-                     int total_chunks, int w, void* stream);
+                     const int32_t* d_chunk_map, int total_chunks, int w, void* stream);
 
 /* h2g_xform_t: [y1; y2] = Q^T x for every box (Q n x n row-major, ld ldq;
  * x n x w, ld w; rows [0, split) of the result -> y1, rows [split, n) -> y2):
@@ -416,7 +418,7 @@ typedef struct h2g_step {
   const void* descs;  /* device descriptor array */
   const int32_t* map; /* device tile / CTA map */
   int32_t* npd;       /* PANEL: device pivot-status array */
-  const void* aux;    /* KBLOCK: device points (N x 3) */
+  const void* aux;    /* KBLOCK: device points (N x 3); GEMV: chunk -> output map */
   double d0, d1;      /* KBLOCK: shift, decay */
   int32_t lane;       /* 0: the caller's stream, 1..4: the context's side streams */
   int32_t wait_ev;    /* event index to wait on before the step, or -1 */

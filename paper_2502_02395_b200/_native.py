@@ -101,7 +101,7 @@ def load_library(path=LIB_PATH):
         "h2g_trsm_rows": (i32, [vp, vp, i32, vp]),
         "h2g_copy_tiles": (i32, [i32, i32]),
         "h2g_block_copy": (i32, [vp, vp, i32, vp]),
-        "h2g_gemv_grouped": (i32, [vp, i32, vp, i32, i32, vp]),
+        "h2g_gemv_grouped": (i32, [vp, i32, vp, vp, i32, i32, vp]),
         "h2g_trsv_batched": (i32, [vp, i32, i32, i32, vp]),
         "h2g_qr_panel": (i32, [vp, i32, i32, vp]),
         "h2g_basis_finish": (i32, [vp, i32, vp]),

@@ -58,7 +58,8 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_BASIS:
       return h2g_basis_finish((const h2g_basis_desc*)s.descs, s.count, st);
     case H2G_STEP_GEMV:
-      return h2g_gemv_grouped((const h2g_gemv_out*)s.descs, s.count, (const h2g_gemv_term*)s.map, s.grid, s.arg, st);
+      return h2g_gemv_grouped((const h2g_gemv_out*)s.descs, s.count, (const h2g_gemv_term*)s.map,
+                              (const int32_t*)s.aux, s.grid, s.arg, st);
     case H2G_STEP_TRSV:
       return h2g_trsv_batched((const h2g_trsv_desc*)s.descs, s.count, s.arg, s.grid, st);  // grid = w
     case H2G_STEP_KBLOCK:

@@ -21,6 +21,9 @@ constexpr int GV_W = 4;         // RHS columns per pass
 #define H2G_GV_UNROLL 4         // rows of a transposed operand in flight per warp
 #endif
 constexpr int GV_UNROLL = H2G_GV_UNROLL;
+#ifndef H2G_GEMV_MINB
+#define H2G_GEMV_MINB H2G_GV_MINB   // resident CTAs of 512 threads the grouped GEMV is compiled for
+#endif
 
 __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) {
   int lo = 0, hi = n - 1;
@@ -31,12 +34,16 @@ __device__ __forceinline__ int find_out(const h2g_gemv_out* outs, int n, int x) 
   return lo;
 }
 
-// y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t
-__global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
-                                                                  const h2g_gemv_term* __restrict__ terms, int w) {
-  __shared__ double acc[GV_CHUNK * GV_W];
+// y[r0:r0+nr] (w columns) = init -/+ sum_t op(A_t) x_t, GW right-hand sides per pass
+// (GW = 1: the single-vector solve; 4 otherwise)
+template <int GW>
+__global__ void __launch_bounds__(GV_THREADS, H2G_GEMV_MINB * 512 / GV_THREADS) gemv_grouped_kernel(const h2g_gemv_out* __restrict__ outs, int n_outs,
+                                                                  const h2g_gemv_term* __restrict__ terms,
+                                                                  const int32_t* __restrict__ chunk_map, int w) {
+  __shared__ double acc[GV_CHUNK * GW];
   __shared__ double red[GV_THREADS / 32][GV_CHUNK];
-  const int oi = find_out(outs, n_outs, blockIdx.x);
+  // the host-built chunk -> output map saves the dependent binary-search loads at CTA start
+  const int oi = chunk_map ? chunk_map[blockIdx.x] : find_out(outs, n_outs, blockIdx.x);
   const h2g_gemv_out O = outs[oi];
   const int r0 = (blockIdx.x - O.chunk_start) * GV_CHUNK;
   const int nr = min(GV_CHUNK, O.m - r0);
@@ -45,9 +52,9 @@ __global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) ge
   const double sign = (O.flags & H2G_GEMV_PLUS) ? 1.0 : -1.0;
   const bool split = (O.flags & H2G_GEMV_SPLIT) != 0;
 
-  for (int j0 = 0; j0 < w; j0 += GV_W) {
-    const int wc = min(GV_W, w - j0);
-    for (int e = tid; e < GV_CHUNK * GV_W; e += GV_THREADS) acc[e] = 0.0;
+  for (int j0 = 0; j0 < w; j0 += GW) {
+    const int wc = min(GW, w - j0);
+    for (int e = tid; e < GV_CHUNK * GW; e += GV_THREADS) acc[e] = 0.0;
     __syncthreads();
     for (int ti = O.term_begin; ti < O.term_end; ++ti) {
       const h2g_gemv_term T = terms[ti];
@@ -58,28 +65,45 @@ __global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) ge
         // identity term (K == m): acc += x[rows of this chunk]
         for (int e = tid; e < nr * wc; e += GV_THREADS) {
           const int rr = e / wc, j = e % wc;
-          acc[rr * GV_W + j] += x[(size_t)(r0 + rr) * w + j0 + j];
+          acc[rr * GW + j] += x[(size_t)(r0 + rr) * w + j0 + j];
         }
         __syncthreads();
       } else if (!T.trans) {
-        // A is m x K: warp per output row, lanes over the contiguous K axis
-        for (int rr = warp; rr < nr; rr += NW) {
+        // A is m x K: a warp owns two output rows at a time (twice the loads in flight),
+        // lanes over the contiguous K axis
+        for (int rr = 2 * warp; rr < nr; rr += 2 * NW) {
+          const bool two = rr + 1 < nr;
           const double* arow = A + (size_t)(r0 + rr) * lda;
-          double s[GV_W] = {0.0, 0.0, 0.0, 0.0};
+          const double* brow = two ? arow + lda : arow;
+          double s[GW];
+          double t[GW];
+#pragma unroll
+          for (int j = 0; j < GW; ++j) s[j] = t[j] = 0.0;
 #pragma unroll 4
           for (int c = lane; c < K; c += 32) {
             const double a = arow[c];
+            const double b = brow[c];
             const double* xc = x + (size_t)c * w + j0;
 #pragma unroll
-            for (int j = 0; j < GV_W; ++j)
-              if (j < wc) s[j] += a * xc[j];
+            for (int j = 0; j < GW; ++j)
+              if (j < wc) {
+                const double xv = xc[j];
+                s[j] += a * xv;
+                t[j] += b * xv;
+              }
           }
 #pragma unroll
-          for (int j = 0; j < GV_W; ++j) {
-            double v = s[j];
+          for (int j = 0; j < GW; ++j) {
+            double v = s[j], u = t[j];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0 && j < wc) acc[rr * GV_W + j] += v;
+            for (int o = 16; o > 0; o >>= 1) {
+              v += __shfl_xor_sync(0xffffffffu, v, o);
+              u += __shfl_xor_sync(0xffffffffu, u, o);
+            }
+            if (lane == 0 && j < wc) {
+              acc[rr * GW + j] += v;
+              if (two) acc[(rr + 1) * GW + j] += u;
+            }
           }
         }
         __syncthreads();
@@ -106,7 +130,7 @@ __global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) ge
             double v = 0.0;
 #pragma unroll
             for (int q = 0; q < NW; ++q) v += red[q][rr];
-            acc[rr * GV_W + j] += v;
+            acc[rr * GW + j] += v;
           }
           __syncthreads();
         }
@@ -115,7 +139,7 @@ __global__ void __launch_bounds__(GV_THREADS, H2G_GV_MINB * 512 / GV_THREADS) ge
     for (int e = tid; e < nr * wc; e += GV_THREADS) {
       const int rr = e / wc, j = e % wc;
       const int r = r0 + rr;
-      double v = sign * acc[rr * GV_W + j];
+      double v = sign * acc[rr * GW + j];
       if (O.init) v += O.init[(size_t)r * w + j0 + j];
       if (split && r >= O.split) O.y2[(size_t)(r - O.split) * w + j0 + j] = v;
       else O.y[(size_t)r * w + j0 + j] = v;
@@ -353,11 +377,16 @@ extern "C" int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_
   return h2g_check_launch("xform_t");
 }
 
-extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms, int total_chunks,
-                                int w, void* stream) {
+extern "C" int h2g_gemv_grouped(const h2g_gemv_out* d_outs, int n_outs, const h2g_gemv_term* d_terms,
+                                const int32_t* d_chunk_map, int total_chunks, int w, void* stream) {
   if (n_outs <= 0 || total_chunks <= 0) return H2G_OK;
   if (!d_outs || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_gemv_grouped: bad argument");
-  h2g::gemv_grouped_kernel<<<total_chunks, h2g::GV_THREADS, 0, (cudaStream_t)stream>>>(d_outs, n_outs, d_terms, w);
+  if (w == 1)
+    h2g::gemv_grouped_kernel<1><<<total_chunks, h2g::GV_THREADS, 0, (cudaStream_t)stream>>>(d_outs, n_outs, d_terms,
+                                                                                           d_chunk_map, w);
+  else
+    h2g::gemv_grouped_kernel<h2g::GV_W><<<total_chunks, h2g::GV_THREADS, 0, (cudaStream_t)stream>>>(
+        d_outs, n_outs, d_terms, d_chunk_map, w);
   return h2g_check_launch("gemv_grouped");
 }
 

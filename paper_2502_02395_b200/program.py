@@ -331,10 +331,25 @@ class Program:
         plan = []
         for o, by in zip(outs, obytes):
             m, terms = int(o[3]), o[6]
-            p = min(len(terms), max(1, int(round(by / (per_cta * -(-m // chunk))))))
+            ktot = sum(int(t[4]) for t in terms)
+            p = min(max(1, ktot // 64), max(1, int(round(by / (per_cta * -(-m // chunk))))))
             if p <= 1:
                 plan.append((o, None))
                 continue
+            if p > len(terms):
+                # cut the terms along K (64-multiples) so that p groups can be formed
+                kp = -(-ktot // p)
+                kp = -(-kp // 64) * 64
+                cut = []
+                for (a, x, lda, trans, k) in terms:
+                    if not a:                    # identity term: K must stay = m
+                        cut.append((a, x, lda, trans, k))
+                        continue
+                    for k0 in range(0, int(k), kp):
+                        kk = min(kp, int(k) - k0)
+                        step = 8 * k0 * (int(lda) if trans else 1)
+                        cut.append((a + step, x + 8 * k0 * w, lda, trans, kk))
+                terms = cut
             tb = np.cumsum([8 * m * int(t[4]) for t in terms], dtype=np.float64)
             cuts = sorted({int(np.searchsorted(tb, by * q / p, side="left")) for q in range(1, p)})
             bounds = [0] + [c + 1 for c in cuts if 0 <= c < len(terms) - 1] + [len(terms)]
@@ -373,7 +388,10 @@ class Program:
         tarr = np.zeros(max(len(tl), 1), dtype=nat.GEMV_TERM_DT)
         for q, (a, x, lda, trans, k) in enumerate(tl):
             tarr[q] = (a, x, lda, trans, k, 0)
-        self._add(nat.STEP["GEMV"], len(outs), chunks, self._blob(oarr), self._blob(tarr), arg=w, nbytes=nbytes)
+        cmap = np.repeat(np.arange(len(outs), dtype=np.int32),
+                         [-(-int(o[3]) // nat.GEMV_CHUNK) for o in outs])
+        self._add(nat.STEP["GEMV"], len(outs), chunks, self._blob(oarr), self._blob(tarr), arg=w, nbytes=nbytes,
+                  aux=("blob", self._blob(cmap)))
         return len(outs)
 
     def xform_t(self, descs, w):
@@ -497,7 +515,8 @@ class Program:
             steps[q]["descs"] = resolve(st["descs"])
             steps[q]["map"] = resolve(st["map"])
             steps[q]["npd"] = st["npd"]
-            steps[q]["aux"] = st["aux"]
+            aux = st["aux"]
+            steps[q]["aux"] = base + offs[aux[1]] if isinstance(aux, tuple) else aux
             steps[q]["d0"] = st["d0"]
             steps[q]["d1"] = st["d1"]
             steps[q]["lane"] = st["lane"]

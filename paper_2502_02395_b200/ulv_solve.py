@@ -28,7 +28,9 @@ from .program import Program
 
 # grouped GEMVs with fewer 64-row chunks than this are split over their terms
 # (Program.gemv balance): the upper levels' few outputs with many neighbour terms
-GEMV_BALANCE = int(os.environ.get("H2G_GEMV_BALANCE", "296"))
+GEMV_BALANCE = int(os.environ.get("H2G_GEMV_BALANCE", "592"))
+# levels whose transform kernels would launch fewer CTAs than this run them as balanced GEMVs
+XFORM_MIN_CTAS = int(os.environ.get("H2G_XFORM_MIN_CTAS", "592"))
 
 F64 = torch.float64
 
@@ -267,7 +269,7 @@ class SolvePlan:
             if self.fused[l]:
                 # G1 + P1 + P3 of a level without near neighbours: [y_R; b_S] = [V | q_skel]^T seg
                 R = fp.bufs[l].R
-                prog.xform_t([(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Y"], offR[i]),
+                self._xform_t(prog, [(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Y"], offR[i]),
                                self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
                               for i in range(nb) if mine[i]], w)
                 if self.dist:
@@ -280,7 +282,7 @@ class SolvePlan:
             if self.use_v:
                 # G1 + P1: [z; b_S] = [V | q_skel]^T seg  (z_i = L_ii^-1 q_red^T seg_i)
                 R = fp.bufs[l].R
-                prog.xform_t([(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Z"], offR[i]),
+                self._xform_t(prog, [(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Z"], offR[i]),
                                self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
                               for i in range(nb) if mine[i]], w)
                 prog = self._forward_parallel_level_v(prog, l, V, lay, below)
@@ -289,7 +291,7 @@ class SolvePlan:
                 xin = V["BS"]
                 continue
             # G1: [b_R; b_S] = q_full^T seg   (_transform_in, ulv_solve.py:33-41)
-            prog.xform_t([(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), self._p(V["BR"], offR[i]),
+            self._xform_t(prog, [(q.data_ptr() + 8 * int(lay.qoff[i]), self._p(xin, offX[i]), self._p(V["BR"], offR[i]),
                            self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i])) for i in range(nb) if mine[i]], w)
             if self.mode == "parallel":
                 prog = self._forward_parallel_level(prog, l, V, lay, below)
@@ -332,6 +334,29 @@ class SolvePlan:
         # P4  b_S,a -= sum_b L(s)_ab y_b
         self._ls_update_forward(prog, l, V, lay, owned=mine)
         return prog
+
+    def _xform_t(self, prog, descs, w):
+        """[y1; y2] = Q^T x per box: the column-chunked transform kernel when the level
+        fills the GPU, else a balanced grouped GEMV (SPLIT rows r | k) whose rows (the K
+        axis) are spread over many CTAs — the upper levels' few large boxes."""
+        descs = [d for d in descs if d[4] > 0]
+        if sum(-(-int(d[4]) // 128) for d in descs) >= XFORM_MIN_CTAS:
+            prog.xform_t(descs, w)
+            return
+        prog.gemv([(y1, y2, 0, n, split, nat.GEMV_PLUS | nat.GEMV_SPLIT, [(q, x, ldq, 1, n)])
+                   for (q, x, y1, y2, n, split, ldq) in descs], w, balance=GEMV_BALANCE)
+
+    def _xform_n(self, prog, descs, w):
+        """out = Q [xr; xs] per box (see _xform_t for the choice of kernel)."""
+        descs = [d for d in descs if d[4] > 0]
+        if sum(-(-int(d[4]) // 32) for d in descs) >= XFORM_MIN_CTAS:
+            prog.xform_n(descs, w)
+            return
+        outs = []
+        for (q, xr, xs, out, n, r, ldq) in descs:
+            terms = ([(q, xr, ldq, 0, r)] if r > 0 else []) + ([(q + 8 * r, xs, ldq, 0, n - r)] if n > r else [])
+            outs.append((out, 0, 0, n, 0, nat.GEMV_PLUS, terms))
+        prog.gemv(outs, w, balance=GEMV_BALANCE)
 
     def _forward_parallel_level_v(self, prog, l, V, lay, below):
         """P1-P3 with Z = L^-1 b_R already formed through V (the transform):
@@ -428,7 +453,7 @@ class SolvePlan:
             if self.fused[l]:
                 # B2 + B3 without near neighbours: full_i = [V_i | q_skel_i] [y_R,i; x_S,i]
                 R = B.R
-                prog.xform_n([(R.ptr(int(lay.qoff[i])), self._p(V["YB"], offR[i]), self._p(xs, offS[i]),
+                self._xform_n(prog, [(R.ptr(int(lay.qoff[i])), self._p(V["YB"], offR[i]), self._p(xs, offS[i]),
                                self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
                               for i in range(nb) if mine[i]], w)
                 xs = V["FULL"]
@@ -461,7 +486,7 @@ class SolvePlan:
                 qptr = {i: B.R.ptr(int(lay.qoff[i])) for i in range(nb) if mine[i]}
             else:
                 qptr = {i: fp.dh2.q[l].data_ptr() + 8 * int(lay.qoff[i]) for i in range(nb) if mine[i]}
-            prog.xform_n([(qptr[i], self._p(V["XR"], offR[i]), self._p(xs, offS[i]),
+            self._xform_n(prog, [(qptr[i], self._p(V["XR"], offR[i]), self._p(xs, offS[i]),
                            self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
                           for i in range(nb) if mine[i]], w)
             xs = V["FULL"]
