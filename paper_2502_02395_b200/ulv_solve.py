@@ -31,6 +31,8 @@ from .program import Program
 GEMV_BALANCE = int(os.environ.get("H2G_GEMV_BALANCE", "592"))
 # levels whose transform kernels would launch fewer CTAs than this run them as balanced GEMVs
 XFORM_MIN_CTAS = int(os.environ.get("H2G_XFORM_MIN_CTAS", "592"))
+# levels with at most this many boxes solve with explicit triangular inverses (see SolvePlan.winv)
+WINV_MAX_BOXES = int(os.environ.get("H2G_SOLVE_WINV_MAX_BOXES", "128"))
 
 F64 = torch.float64
 
@@ -89,6 +91,15 @@ class SolvePlan:
         # such a level has no TRSV at all.  The prepare step puts q_skel next to V_i in R.
         self.use_v = mode == "parallel" and fplan.has_v
         self.fused = {l: self.use_v and not fplan.bufs[l].lay.off_pairs for l in range(depth, 0, -1)}
+        # levels with few boxes: a one-CTA-per-box TRSV is a long serial chain on a few SMs, so
+        # they get explicit Wt_i = L_ii^-T (from the stored L, in the prepare step) and every
+        # triangular solve becomes a balanced GEMV
+        self.winv = {}
+        for l in range(depth, 0, -1):
+            lay = fplan.bufs[l].lay
+            mine = fplan.mine(l)
+            nbox = int(sum(1 for i in range(lay.nb) if mine[i] and lay.r[i] > 0))
+            self.winv[l] = self.use_v and not self.fused[l] and 0 < nbox <= WINV_MAX_BOXES
         self._build_prepare()
         self._segs = []
         self._masks = {}
@@ -113,7 +124,7 @@ class SolvePlan:
         W = nat.PANEL_WIDTH
         prog = Program(dev)
         self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
-        self.linv, self.loff = {}, {}
+        self.linv, self.loff, self.wt = {}, {}, {}
         for l in range(fp.depth, 0, -1):
             B = fp.bufs[l]
             lay = B.lay
@@ -126,12 +137,33 @@ class SolvePlan:
             prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
                           int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
                         self._tri_status.data_ptr())
+            if self.winv[l]:
+                roff = np.concatenate([[0], np.cumsum(np.asarray(lay.r, dtype=np.int64) ** 2)[:-1]])
+                wt = torch.zeros(max(int((np.asarray(lay.r, dtype=np.int64) ** 2).sum()), 1), dtype=F64, device=dev)
+                self.wt[l] = (wt, roff)
+                prog.trsm_rows([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, wt.data_ptr() + 8 * int(roff[i]),
+                                 lt.data_ptr() + 8 * int(loff[i]) * W * W, int(lay.r[i]), int(lay.r[i]), 0,
+                                 int(nblk[i]), int(lay.n[i]), int(lay.r[i]))
+                                for i in range(lay.nb) if mine[i] and lay.r[i] > 0])
             if self.use_v:
                 # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
                 q = fp.dh2.q[l]
                 prog.copy([(q.data_ptr() + 8 * int(lay.qoff[i] + lay.r[i]), B.R.ptr(int(lay.qoff[i] + lay.r[i])),
                             int(lay.n[i]), int(lay.k[i]), int(lay.n[i]), int(lay.n[i]), 0)
                            for i in range(lay.nb) if mine[i] and lay.k[i] > 0])
+                if self.fused[l]:
+                    # no near neighbours: L(s)_ii is the only L(s) block of box i, so P4
+                    # (b_S -= L(s)_ii y) and B1 (y_R -= L(s)_ii^T x_S) fold into the transforms
+                    # through q_skel~ = q_skel - V_i L(s)_ii^T:  b_S - L(s) V^T b = q_skel~^T b,
+                    # V (y - L(s)^T x_S) + q_skel x_S = V y + q_skel~ x_S
+                    gm = []
+                    for i in range(lay.nb):
+                        ni, ri, ki = int(lay.n[i]), int(lay.r[i]), int(lay.k[i])
+                        if mine[i] and ri > 0 and ki > 0:
+                            o = int(lay.qoff[i])
+                            gm.append((B.R.ptr(o), B.H.data_ptr() + 8 * (o + ri * ni), B.R.ptr(o + ri),
+                                       ni, ki, ri, ni, ni, ni, 0, -1.0, 1.0))
+                    prog.gemm(0, 1, gm)
         d = fp.root_dim
         nb0 = -(-d // W)
         self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
@@ -267,14 +299,14 @@ class SolvePlan:
             q = fp.dh2.q[l]
             mine = self._mine(l)
             if self.fused[l]:
-                # G1 + P1 + P3 of a level without near neighbours: [y_R; b_S] = [V | q_skel]^T seg
+                # G1 + P1-P4 of a level without near neighbours: [y_R; b_S] = [V | q_skel~]^T seg
                 R = fp.bufs[l].R
                 self._xform_t(prog, [(R.ptr(int(lay.qoff[i])), self._p(xin, offX[i]), self._p(V["Y"], offR[i]),
                                self._p(V["BS"], offS[i]), int(n[i]), int(r[i]), int(n[i]))
                               for i in range(nb) if mine[i]], w)
                 if self.dist:
                     prog = self._cut(prog, ("Y", l, "offR"))
-                self._ls_update_forward(prog, l, V, lay, owned=mine)     # P4
+                # (P4 is in the transform: R carries q_skel~, see _build_prepare)
                 if self.dist and l - 1 < fp.part.L0:
                     prog = self._cut(prog, ("BS", l, "offS"))
                 xin = V["BS"]
@@ -376,9 +408,15 @@ class SolvePlan:
             prog.gemv([(self._p(U, offR[i]), 0, 0, int(r[i]), 0, nat.GEMV_PLUS,
                         [(B.T.ptr(B.toff[(i, j)]), self._p(V["Z"], offR[j]), int(n[j]), 0, int(r[j]))
                          for j in below[i] if r[j] > 0]) for i in nbr], w, balance=GEMV_BALANCE)
-            prog.trsv([self._tr(l, i, self._p(U, offR[i])) for i in nbr], 0, w)
-            prog.gemv([(self._p(V["Y"], offR[i]), 0, self._p(V["Z"], offR[i]), int(r[i]), 0, 0,
-                        [(0, self._p(U, offR[i]), 0, 0, int(r[i]))]) for i in nbr], w)
+            if self.winv[l]:          # y_i = z_i - L_ii^-1 u_i = z_i - Wt_i^T u_i
+                wt, roff = self.wt[l]
+                prog.gemv([(self._p(V["Y"], offR[i]), 0, self._p(V["Z"], offR[i]), int(r[i]), 0, 0,
+                            [(wt.data_ptr() + 8 * int(roff[i]), self._p(U, offR[i]), int(r[i]), 1, int(r[i]))])
+                           for i in nbr], w, balance=GEMV_BALANCE)
+            else:
+                prog.trsv([self._tr(l, i, self._p(U, offR[i])) for i in nbr], 0, w)
+                prog.gemv([(self._p(V["Y"], offR[i]), 0, self._p(V["Z"], offR[i]), int(r[i]), 0, 0,
+                            [(0, self._p(U, offR[i]), 0, 0, int(r[i]))]) for i in nbr], w)
         if self.dist:
             prog = self._cut(prog, ("Y", l, "offR"))
         self._ls_update_forward(prog, l, V, lay, owned=mine)     # P4
@@ -439,6 +477,13 @@ class SolvePlan:
             dist = self.dist
             if dist and l >= 2:
                 prog = self._cut(prog, ("FULL", l - 1, "offX"))   # x_S of neighbours computed elsewhere
+            if self.fused[l]:
+                # B1-B3 without near neighbours: full_i = [V_i | q_skel~_i] [y_R,i; x_S,i]
+                self._xform_n(prog, [(B.R.ptr(int(lay.qoff[i])), self._p(V["Y"], offR[i]), self._p(xs, offS[i]),
+                                      self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
+                                     for i in range(nb) if mine[i]], w)
+                xs = V["FULL"]
+                continue
             # B1  y_R,i -= sum_a L(s)_ai^T x_S,a
             src = {}
             for (a, b) in self._ls_keys(lay):
@@ -450,18 +495,16 @@ class SolvePlan:
                      [tm for _, tm in sorted(src.get(i, []), key=lambda x: x[0])])
                     for i in range(nb) if mine[i]]
             prog.gemv(outs, w, balance=GEMV_BALANCE)
-            if self.fused[l]:
-                # B2 + B3 without near neighbours: full_i = [V_i | q_skel_i] [y_R,i; x_S,i]
-                R = B.R
-                self._xform_n(prog, [(R.ptr(int(lay.qoff[i])), self._p(V["YB"], offR[i]), self._p(xs, offS[i]),
-                               self._p(V["FULL"], offX[i]), int(n[i]), int(r[i]), int(n[i]))
-                              for i in range(nb) if mine[i]], w)
-                xs = V["FULL"]
-                continue
             if self.mode == "parallel":
                 _, above = _near_sets(lay)
-                prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
-                prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
+                if self.winv[l]:      # z2_i = L_ii^-T y_i = Wt_i y_i
+                    wt, roff = self.wt[l]
+                    prog.gemv([(self._p(V["Z2"], offR[i]), 0, 0, int(r[i]), 0, nat.GEMV_PLUS,
+                                [(wt.data_ptr() + 8 * int(roff[i]), self._p(V["YB"], offR[i]), int(r[i]), 0,
+                                  int(r[i]))]) for i in range(nb) if mine[i] and r[i] > 0], w, balance=GEMV_BALANCE)
+                else:
+                    prog.memcpy(V["Z2"].data_ptr(), V["YB"].data_ptr(), 8 * int(r.sum()) * w)
+                    prog.trsv([self._tr(l, i, self._p(V["Z2"], offR[i])) for i in range(nb) if mine[i]], 1, w)
                 if dist:
                     prog = self._cut(prog, ("Z2", l, "offR"))
                 # boxes without upper near neighbours: x_R,i = z2_i (same TRSV, same input);

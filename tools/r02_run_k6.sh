@@ -1,0 +1,7 @@
+set -x
+T=r02k6
+timeout 1800 python -m pytest tests/test_gpu_factor_solve.py tests/test_gpu_storage.py tests/test_distributed.py tests/test_gpu_block_api.py -x -q > gpurun_out/${T}_pytest.log 2>&1
+for v in 32 0 128; do
+  H2G_SOLVE_WINV_MAX_BOXES=$v timeout 600 python bench.py --steps 10 --e2e-steps 0 --no-cpu-baseline --no-exact-residual > gpurun_out/${T}_bench_w$v.json 2> gpurun_out/${T}_bench_w$v.err
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/${T}_solve_launches.csv python tools/profile_solve.py m1 > gpurun_out/${T}_solve_prof.log 2>&1
