@@ -523,8 +523,14 @@ def main():
         torch.cuda.synchronize(dev)
         s_ms = e0.elapsed_time(e1) / args.steps
         sb = solve_bytes(plan)
+        # bytes the steps of THIS path move (basis / factor blocks as the programs count them):
+        # below the formula on neighbour-free levels (V replaces q_red, no L read), above it
+        # where explicit inverses are read whole
+        pb = sum(int(wk[2]) for pg in (sp.fwd, sp.bwd) if pg is not None for wk in pg.work)
         solve = {"ms": s_ms, "algorithmic_bytes": sb, "gbs": sb / (s_ms * 1e-3) / 1e9,
                  "hbm_peak_gbs": HBM_PEAK_GBS, "frac": sb / (s_ms * 1e-3) / 1e9 / HBM_PEAK_GBS,
+                 "path_bytes": pb, "path_gbs": pb / (s_ms * 1e-3) / 1e9,
+                 "path_frac": pb / (s_ms * 1e-3) / 1e9 / HBM_PEAK_GBS,
                  "note": "SURVEY §8(d) bytes (w = 1): every basis / factor block read once per sweep; "
                          "forward + backward CUDA graphs replayed back to back, CUDA events"}
 

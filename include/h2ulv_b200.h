@@ -245,8 +245,9 @@ int h2g_xform_t(const h2g_xform_desc* d_descs, const int32_t* d_tile_map, int to
 /* h2g_xform_n: out = Q [xr; xs] for every box (Q n x n row-major, ld ldq; xr
  * the first r entries, xs the other n - r, each n x w / ld w; n <= 4096): the
  * basis transform of the backward sweep, full_i = q_red x_R + q_skel x_S
- * (ulv_solve.py:178-181).  One CTA per 32 output rows (d_tile_map as above);
- * vec16 as for h2g_xform_t.
+ * (ulv_solve.py:178-181).  One CTA per h2g_xform_n_rows() output rows
+ * (d_tile_map as above); vec16 as for h2g_xform_t; max_n = the largest n of
+ * the launch (sizes the shared x staging; the step carries it in d0).
  */
 typedef struct h2g_xform_n_desc {
   const double* Q;
@@ -257,7 +258,8 @@ typedef struct h2g_xform_n_desc {
 } h2g_xform_n_desc;
 
 int h2g_xform_n(const h2g_xform_n_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w, int vec16,
-                void* stream);
+                int max_n, void* stream);
+int h2g_xform_n_rows(void);
 
 /* h2g_trsv_batched: x_i <- L_i^-1 x_i (trans=0) or L_i^-T x_i (trans=1) for
  * every box, one CTA per box; L_i is the lower r_i x r_i factor stored with
@@ -419,7 +421,7 @@ typedef struct h2g_step {
   const int32_t* map; /* device tile / CTA map */
   int32_t* npd;       /* PANEL: device pivot-status array */
   const void* aux;    /* KBLOCK: device points (N x 3); GEMV: chunk -> output map */
-  double d0, d1;      /* KBLOCK: shift, decay */
+  double d0, d1;      /* KBLOCK: shift, decay; XFORM_N: d0 = largest box n */
   int32_t lane;       /* 0: the caller's stream, 1..4: the context's side streams */
   int32_t wait_ev;    /* event index to wait on before the step, or -1 */
   int32_t rec_ev;     /* event index to record after the step, or -1 */

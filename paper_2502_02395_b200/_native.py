@@ -74,7 +74,7 @@ EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_chol_panel_tiles", "h2g_ch
            "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
-           "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n",
+           "h2g_last_error", "h2g_device_sm_count", "h2g_sym_check", "h2g_tri_inv", "h2g_chol_box", "h2g_xform_t", "h2g_xform_n", "h2g_xform_n_rows",
            "h2g_session_create", "h2g_session_factor_async", "h2g_session_status", "h2g_session_destroy",
            "h2g_direct_matvec_workspace", "h2g_direct_matvec"]
 
@@ -120,7 +120,8 @@ def load_library(path=LIB_PATH):
         "h2g_tri_inv": (i32, [vp, vp, i32, vp, vp]),
         "h2g_chol_box": (i32, [vp, i32, vp, vp]),
         "h2g_xform_t": (i32, [vp, vp, i32, i32, i32, vp]),
-        "h2g_xform_n": (i32, [vp, vp, i32, i32, i32, vp]),
+        "h2g_xform_n": (i32, [vp, vp, i32, i32, i32, i32, vp]),
+        "h2g_xform_n_rows": (i32, []),
         "h2g_session_create": (i32, [vp, i32, i32, vp, i32, vp, vp, ctypes.POINTER(vp)]),
         "h2g_session_factor_async": (i32, [vp, vp]),
         "h2g_session_status": (i32, [vp, vp, vp]),

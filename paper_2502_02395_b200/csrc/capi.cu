@@ -79,7 +79,7 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_XFORM_T:
       return h2g_xform_t((const h2g_xform_desc*)s.descs, s.map, s.grid, s.arg, s.count < 0, st);
     case H2G_STEP_XFORM_N:
-      return h2g_xform_n((const h2g_xform_n_desc*)s.descs, s.map, s.grid, s.arg, s.count < 0, st);
+      return h2g_xform_n((const h2g_xform_n_desc*)s.descs, s.map, s.grid, s.arg, s.count < 0, (int)s.d0, st);
     case H2G_STEP_NOP:
       return H2G_OK;
     default:

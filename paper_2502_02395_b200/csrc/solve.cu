@@ -307,14 +307,17 @@ __global__ void __launch_bounds__(XT_THREADS) xform_t_kernel(const h2g_xform_des
 }
 
 // Basis transform of the backward sweep, full_i = q_red x_R + q_skel x_S = q_full [x_R; x_S]
-// (ulv_solve.py:178-181): a CTA owns 32 output rows of one box, [x_R; x_S] is staged in
-// shared memory, each warp takes 4 rows with the lanes across the columns (16-byte loads
-// when the rows are aligned), one shuffle reduction per row.
-constexpr int XN_ROWS = 32, XN_WARPS = 8, XN_THREADS = 32 * XN_WARPS, XN_MAXN = 4096;
+// (ulv_solve.py:178-181): a CTA owns XN_ROWS output rows of one box, [x_R; x_S] is staged
+// in shared memory, each warp takes its rows two at a time with the lanes across the
+// columns (16-byte loads when the rows are aligned), one shuffle reduction per row.
+#ifndef H2G_XN_ROWS
+#define H2G_XN_ROWS 32
+#endif
+constexpr int XN_ROWS = H2G_XN_ROWS, XN_WARPS = 8, XN_THREADS = 32 * XN_WARPS, XN_MAXN = 4096;
 template <bool VEC>
 __global__ void __launch_bounds__(XN_THREADS) xform_n_kernel(const h2g_xform_n_desc* __restrict__ descs,
                                                              const int32_t* __restrict__ tile_map, int w) {
-  __shared__ __align__(16) double xs[XN_MAXN];
+  extern __shared__ __align__(16) double xs[];   // n doubles (the launch sizes it to the largest box)
   const h2g_xform_n_desc D = descs[tile_map[blockIdx.x]];
   const int r0 = (blockIdx.x - D.tile_start) * XN_ROWS;
   const int n = D.n, r = D.r, ld = D.ldq;
@@ -323,31 +326,47 @@ __global__ void __launch_bounds__(XN_THREADS) xform_n_kernel(const h2g_xform_n_d
     for (int c = threadIdx.x; c < n; c += XN_THREADS)
       xs[c] = c < r ? D.xr[(size_t)c * w + j] : D.xs[(size_t)(c - r) * w + j];
     __syncthreads();
+    constexpr int RPW = XN_ROWS / XN_WARPS;   // rows per warp, taken two at a time (loads in flight)
 #pragma unroll
-    for (int u = 0; u < XN_ROWS / XN_WARPS; ++u) {
-      const int row = r0 + warp * (XN_ROWS / XN_WARPS) + u;
+    for (int u = 0; u < RPW; u += 2) {
+      const int row = r0 + warp * RPW + u;
       if (row >= n) break;
+      const bool two = row + 1 < n;
       const double* q = D.Q + (size_t)row * ld;
-      double s0 = 0.0, s1 = 0.0;
+      const double* q2 = two ? q + ld : q;
+      double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
       if (VEC) {
 #pragma unroll 4
         for (int c = 2 * lane; c < n; c += 64) {
           if (c + 1 < n) {
             const double2 a = __ldg(reinterpret_cast<const double2*>(q + c));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(q2 + c));
             s0 = fma(a.x, xs[c], s0);
             s1 = fma(a.y, xs[c + 1], s1);
+            t0 = fma(b.x, xs[c], t0);
+            t1 = fma(b.y, xs[c + 1], t1);
           } else {
             s0 = fma(__ldg(q + c), xs[c], s0);
+            t0 = fma(__ldg(q2 + c), xs[c], t0);
           }
         }
       } else {
 #pragma unroll 4
-        for (int c = lane; c < n; c += 32) s0 = fma(__ldg(q + c), xs[c], s0);
+        for (int c = lane; c < n; c += 32) {
+          s0 = fma(__ldg(q + c), xs[c], s0);
+          t0 = fma(__ldg(q2 + c), xs[c], t0);
+        }
       }
-      double v = s0 + s1;
+      double v = s0 + s1, v2 = t0 + t1;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) D.out[(size_t)row * w + j] = v;
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      if (lane == 0) {
+        D.out[(size_t)row * w + j] = v;
+        if (two) D.out[(size_t)(row + 1) * w + j] = v2;
+      }
     }
     __syncthreads();
   }
@@ -355,14 +374,18 @@ __global__ void __launch_bounds__(XN_THREADS) xform_n_kernel(const h2g_xform_n_d
 
 }  // namespace h2g
 
+extern "C" int h2g_xform_n_rows(void) { return h2g::XN_ROWS; }
+
 extern "C" int h2g_xform_n(const h2g_xform_n_desc* d_descs, const int32_t* d_tile_map, int total_tiles, int w,
-                           int vec16, void* stream) {
+                           int vec16, int max_n, void* stream) {
   if (total_tiles <= 0) return H2G_OK;
-  if (!d_descs || !d_tile_map || w <= 0) return h2g_set_error(H2G_EINVAL, "h2g_xform_n: bad argument");
+  if (!d_descs || !d_tile_map || w <= 0 || max_n <= 0 || max_n > h2g::XN_MAXN)
+    return h2g_set_error(H2G_EINVAL, "h2g_xform_n: bad argument (max_n %d)", max_n);
+  const size_t smem = (size_t)max_n * sizeof(double);
   if (vec16)
-    h2g::xform_n_kernel<true><<<total_tiles, h2g::XN_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+    h2g::xform_n_kernel<true><<<total_tiles, h2g::XN_THREADS, smem, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
   else
-    h2g::xform_n_kernel<false><<<total_tiles, h2g::XN_THREADS, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
+    h2g::xform_n_kernel<false><<<total_tiles, h2g::XN_THREADS, smem, (cudaStream_t)stream>>>(d_descs, d_tile_map, w);
   return h2g_check_launch("xform_n");
 }
 

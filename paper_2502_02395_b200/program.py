@@ -384,7 +384,7 @@ class Program:
             oarr[q] = (y, y2, init, m, split, len(tl), len(tl) + len(tms), flags, chunks)
             chunks += -(-int(m) // nat.GEMV_CHUNK)
             tl.extend(tms)
-            nbytes += 8 * int(m) * sum(int(t[4]) for t in tms)
+            nbytes += 8 * int(m) * sum(int(t[4]) for t in tms if t[0])   # matrix bytes (identity terms: none)
         tarr = np.zeros(max(len(tl), 1), dtype=nat.GEMV_TERM_DT)
         for q, (a, x, lda, trans, k) in enumerate(tl):
             tarr[q] = (a, x, lda, trans, k, 0)
@@ -423,14 +423,15 @@ class Program:
         arr = np.zeros(len(descs), dtype=nat.XFORMN_DT)
         for name, col in zip(("Q", "xr", "xs", "out", "n", "r", "ldq"), zip(*descs)):
             arr[name] = col
-        tiles = -(-arr["n"].astype(np.int64) // 32)
+        rows = nat.lib().h2g_xform_n_rows()
+        tiles = -(-arr["n"].astype(np.int64) // rows)
         arr["tile_start"] = np.concatenate([[0], np.cumsum(tiles)[:-1]])
         tmap = np.repeat(np.arange(len(descs), dtype=np.int32), tiles)
         vec = bool(((arr["Q"] % 16) == 0).all() and ((arr["ldq"] % 2) == 0).all())
         n64 = arr["n"].astype(np.int64)
         nbytes = 8 * int((n64 * n64).sum()) + 16 * int(n64.sum()) * w
         self._add(nat.STEP["XFORM_N"], -len(descs) if vec else len(descs), int(tiles.sum()), self._blob(arr),
-                  self._blob(tmap), arg=w, nbytes=nbytes)
+                  self._blob(tmap), arg=w, nbytes=nbytes, d0=float(n64.max()))
         return int(tiles.sum())
 
     def trsv(self, descs, trans, w):
