@@ -124,7 +124,7 @@ class SolvePlan:
         W = nat.PANEL_WIDTH
         prog = Program(dev)
         self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
-        self.linv, self.loff, self.wt = {}, {}, {}
+        self.linv, self.loff, self.wt, self.mblk = {}, {}, {}, {}
         for l in range(fp.depth, 0, -1):
             B = fp.bufs[l]
             lay = B.lay
@@ -145,6 +145,19 @@ class SolvePlan:
                                  lt.data_ptr() + 8 * int(loff[i]) * W * W, int(lay.r[i]), int(lay.r[i]), 0,
                                  int(nblk[i]), int(lay.n[i]), int(lay.r[i]))
                                 for i in range(lay.nb) if mine[i] and lay.r[i] > 0])
+                if not self.dist:
+                    # M_ij = L_ii^-1 L(r)_ij (i > j near): P2+P3 become y_i = z_i - sum_j M_ij z_j
+                    # and B2' x_R-terms t_i = y_i - sum_j M_ji^T y_j — one GEMV each, no TRSV
+                    pairs = [(i, j) for (i, j) in lay.off_pairs if lay.r[i] > 0 and lay.r[j] > 0]
+                    moff, acc = {}, 0
+                    for (i, j) in pairs:
+                        moff[(i, j)] = acc
+                        acc += int(lay.r[i]) * int(lay.r[j])
+                    mt = torch.zeros(max(acc, 1), dtype=F64, device=dev)
+                    self.mblk[l] = (mt, moff)
+                    prog.gemm(1, 0, [(wt.data_ptr() + 8 * int(roff[i]), B.T.ptr(B.toff[(i, j)]),
+                                      mt.data_ptr() + 8 * moff[(i, j)], int(lay.r[i]), int(lay.r[j]), int(lay.r[i]),
+                                      int(lay.r[i]), int(lay.n[j]), int(lay.r[j]), 0, 1.0, 0.0) for (i, j) in pairs])
             if self.use_v:
                 # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
                 q = fp.dh2.q[l]
@@ -401,6 +414,15 @@ class SolvePlan:
         mine = self._mine(l)
         if self.dist:
             prog = self._cut(prog, ("Z", l, "offR"))
+        if l in self.mblk:
+            # y_i = z_i - sum_{j<i near} M_ij z_j  (M_ij = L_ii^-1 L(r)_ij from the prepare step)
+            mt, moff = self.mblk[l]
+            prog.gemv([(self._p(V["Y"], offR[i]), 0, self._p(V["Z"], offR[i]), int(r[i]), 0, 0,
+                        [(mt.data_ptr() + 8 * moff[(i, j)], self._p(V["Z"], offR[j]), int(r[j]), 0, int(r[j]))
+                         for j in below[i] if r[j] > 0]) for i in range(nb) if mine[i] and r[i] > 0], w,
+                      balance=GEMV_BALANCE)
+            self._ls_update_forward(prog, l, V, lay, owned=mine)     # P4
+            return prog
         prog.memcpy(V["Y"].data_ptr(), V["Z"].data_ptr(), 8 * int(r.sum()) * w)
         nbr = [i for i in range(nb) if mine[i] and any(r[j] > 0 for j in below[i])]
         if nbr:
@@ -495,7 +517,15 @@ class SolvePlan:
                      [tm for _, tm in sorted(src.get(i, []), key=lambda x: x[0])])
                     for i in range(nb) if mine[i]]
             prog.gemv(outs, w, balance=GEMV_BALANCE)
-            if self.mode == "parallel":
+            if self.mode == "parallel" and l in self.mblk:
+                # t_i = y_i - sum_{j>i near} L(r)_ji^T L_jj^-T y_j = y_i - sum_j M_ji^T y_j
+                _, above = _near_sets(lay)
+                mt, moff = self.mblk[l]
+                prog.gemv([(self._p(V["XR"], offR[i]), 0, self._p(V["YB"], offR[i]), int(r[i]), 0, 0,
+                            [(mt.data_ptr() + 8 * moff[(j, i)], self._p(V["YB"], offR[j]), int(r[i]), 1, int(r[j]))
+                             for j in above[i] if r[j] > 0]) for i in range(nb) if mine[i] and r[i] > 0], w,
+                          balance=GEMV_BALANCE)
+            elif self.mode == "parallel":
                 _, above = _near_sets(lay)
                 if self.winv[l]:      # z2_i = L_ii^-T y_i = Wt_i y_i
                     wt, roff = self.wt[l]
