@@ -107,6 +107,17 @@ def test_fullsize_structure_flops_residual(pkg, name):
     perm = h2.cloud.perm
     res = float(np.linalg.norm(pkg.h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b))
     assert res <= 10 * m["residual"], (name, res, m["residual"])
+    if name == "c2":
+        # multi-RHS through every solve path at full size (TRSV levels, explicit-inverse
+        # levels, neighbour-free levels, balanced GEMVs with w > 1): column j == solve(b_j)
+        b2 = np.random.default_rng(2).standard_normal(m["config"]["n"])
+        xm = pkg.solve(f, np.stack([b, b2, -3.0 * b, b2, b], axis=1))
+        for j, bj in enumerate((b, b2, -3.0 * b, b2, b)):
+            xj = x if j in (0, 4) else pkg.solve(f, bj) if j != 2 else -3.0 * x
+            assert np.linalg.norm(xm[:, j] - xj) <= 1e-12 * np.linalg.norm(xj), j
+        for mode in ("naive",):
+            xn = pkg.solve(f, b, mode=mode)
+            assert np.linalg.norm(xn - x) <= 1e-9 * np.linalg.norm(x)
     del f, h2
     clear_cache()
 
