@@ -90,7 +90,10 @@ class SolvePlan:
         # of a cube tree, the N = 1M leaf among them) forward P1 z_i = V_i^T b_i = y_i too, so
         # such a level has no TRSV at all.  The prepare step puts q_skel next to V_i in R.
         self.use_v = mode == "parallel" and fplan.has_v
-        self.fused = {l: self.use_v and not fplan.bufs[l].lay.off_pairs for l in range(depth, 0, -1)}
+        # (neighbour-free levels are the same computation in both modes — there is no chain to
+        # order — so naive and parallel share the fused form and agree bit for bit, e.g. on
+        # HSS trees, test_ulv_solve.py:90-96)
+        self.fused = {l: fplan.has_v and not fplan.bufs[l].lay.off_pairs for l in range(depth, 0, -1)}
         # levels with few boxes: a one-CTA-per-box TRSV is a long serial chain on a few SMs, so
         # they get explicit Wt_i = L_ii^-T (from the stored L, in the prepare step) and every
         # triangular solve becomes a balanced GEMV
@@ -158,7 +161,7 @@ class SolvePlan:
                     prog.gemm(1, 0, [(wt.data_ptr() + 8 * int(roff[i]), B.T.ptr(B.toff[(i, j)]),
                                       mt.data_ptr() + 8 * moff[(i, j)], int(lay.r[i]), int(lay.r[j]), int(lay.r[i]),
                                       int(lay.r[i]), int(lay.n[j]), int(lay.r[j]), 0, 1.0, 0.0) for (i, j) in pairs])
-            if self.use_v:
+            if self.use_v or self.fused[l]:
                 # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
                 q = fp.dh2.q[l]
                 prog.copy([(q.data_ptr() + 8 * int(lay.qoff[i] + lay.r[i]), B.R.ptr(int(lay.qoff[i] + lay.r[i])),

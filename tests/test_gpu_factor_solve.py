@@ -183,3 +183,17 @@ def test_fused_box_with_v_matches_reference(pkg, name, monkeypatch):
             assert np.allclose(v @ lr.T, b.q_red, atol=1e-10), (l, i)
     assert _rel(pkg.solve(f, ref["b"]), ref["x"]) < RTOL_X
     ulv_factor.clear_cache()
+
+
+def test_hss_modes_bitwise_identical(pkg):
+    """eta = 0 (HSS: no near pair off the diagonal on any level): the chain terms vanish,
+    so naive and parallel substitution are the same computation and agree bit for bit
+    (the reference's test_ulv_solve.py:90-96)."""
+    cloud = pkg.gen_uniform_cube(2048, seed=1)
+    tree = pkg.build_tree(cloud, 64)
+    lists = pkg.build_interaction_lists(tree, 0.0)
+    cfg = pkg.BuildConfig(eta=0.0, leaf_max=64, rank=16, s_far=128, s_near=128)
+    h2 = pkg.construct(pkg.KernelSpec(family="laplace", diagonal_shift=1e3), tree, lists, cfg, cloud)
+    f = pkg.factorize(h2)
+    b = np.random.default_rng(3).standard_normal(cloud.count)
+    assert np.array_equal(pkg.solve(f, b, mode="naive"), pkg.solve(f, b, mode="parallel"))
