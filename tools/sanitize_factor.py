@@ -41,3 +41,18 @@ x = np.empty_like(b)
 x[cloud.perm] = sp.output[:cloud.count].cpu().numpy()
 from oracle import h2ulv_oracle as orc  # noqa: E402  (checker only)
 print("residual", orc.residual(h2, x, b))
+# the other solve paths: w = 3 (the 4-column GEMV kernel), naive mode, and the exact-kernel direct sum
+for w, mode in ((3, "parallel"), (1, "naive")):
+    spw = SolvePlan(plan, w, mode)
+    bw = np.random.default_rng(2).standard_normal((cloud.count, w))
+    spw.xin[:cloud.count * w].copy_(torch.from_numpy(bw[cloud.perm].reshape(-1)))
+    spw.prepare.run()
+    for seg in spw.fwd_segments + spw.bwd_segments:
+        if isinstance(seg, Program):
+            seg.run()
+    torch.cuda.synchronize()
+    xw = np.empty_like(bw)
+    xw[cloud.perm] = spw.output[:cloud.count * w].view(-1, w).cpu().numpy()
+    print(mode, w, "residual", max(orc.residual(h2, xw[:, j], bw[:, j]) for j in range(w)))
+from paper_2502_02395_b200.direct_sum import exact_residual  # noqa: E402
+print("exact residual", exact_residual(h2.kernel, cloud, x, b))
