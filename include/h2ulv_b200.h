@@ -67,6 +67,26 @@ typedef struct h2g_gemm_problem {
 } h2g_gemm_problem;
 
 int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg); /* tiles one problem needs */
+
+/* Per-problem extension of a grouped GEMM (h2g_gemm_grouped_ext, NN or NT):
+ *   Cin (ld ldcin), when not NULL, is the beta term's source instead of C;
+ *   remap_k >= 0 stores a LOWER problem's tile through the compact-WY relabel of
+ *   the diag transform (diag_mul1/2, ulv_factor.py:189-200; id_basis's column
+ *   order and signs, dense_core.py:140-148): the product is H' = Q^T A Q in
+ *   Householder column order (skeleton columns 0..k-1 first, k = remap_k);
+ *   entry (a, b), a >= b, goes to H[x][y] (or H[y][x] when x < y) with
+ *   x = a - k (a >= k) or a + M - k (a < k), sign-flipped by sgn[a] (a < k)
+ *   and sgn[b] (b < k).  Only a >= b is stored, so each lower entry of H has
+ *   exactly one writer.  A step carries the ext array in `aux`. */
+typedef struct h2g_gemm_ext {
+  const double* Cin;
+  const double* sgn;
+  int32_t ldcin;
+  int32_t remap_k;  /* < 0: plain store */
+} h2g_gemm_ext;
+
+int h2g_gemm_grouped_ext(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
+                         const h2g_gemm_ext* d_ext, const int32_t* d_tile_map, int total_tiles, void* stream);
 int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
                      const int32_t* d_tile_map, int total_tiles, void* stream);
 

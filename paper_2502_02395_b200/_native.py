@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("H2G_LIB_PATH") or os.path.join(HERE, "libh2ulv_b200.s
 GEMM_DT = np.dtype([("A", "<u8"), ("B", "<u8"), ("C", "<u8"), ("M", "<i4"), ("N", "<i4"), ("K", "<i4"),
                     ("lda", "<i4"), ("ldb", "<i4"), ("ldc", "<i4"), ("tile_start", "<i4"), ("flags", "<i4"),
                     ("alpha", "<f8"), ("beta", "<f8")])
+GEMM_EXT_DT = np.dtype([("Cin", "<u8"), ("sgn", "<u8"), ("ldcin", "<i4"), ("remap_k", "<i4")])
 CHOLP_DT = np.dtype([("H", "<u8"), ("Linv", "<u8"), ("ldh", "<i4"), ("ldl", "<i4"), ("n", "<i4"), ("p", "<i4"),
                      ("b", "<i4"), ("npd_slot", "<i4"), ("tile_start", "<i4"), ("pad_", "<i4")])
 ROWS_DT = np.dtype([("Lb", "<u8"), ("Xin", "<u8"), ("Xout", "<u8"), ("Linv", "<u8"), ("pad0_", "<u8"),
@@ -51,7 +52,7 @@ STEP_DT = np.dtype([("kind", "<i4"), ("count", "<i4"), ("grid", "<i4"), ("arg", 
                     ("map", "<u8"), ("npd", "<u8"), ("aux", "<u8"), ("d0", "<f8"), ("d1", "<f8"),
                     ("lane", "<i4"), ("wait_ev", "<i4"), ("rec_ev", "<i4"), ("pad_", "<i4")])
 
-assert GEMM_DT.itemsize == 72 and COPY_DT.itemsize == 40 and CHOLP_DT.itemsize == 48 and ROWS_DT.itemsize == 72
+assert GEMM_DT.itemsize == 72 and GEMM_EXT_DT.itemsize == 24 and COPY_DT.itemsize == 40 and CHOLP_DT.itemsize == 48 and ROWS_DT.itemsize == 72
 assert GEMV_TERM_DT.itemsize == 32 and GEMV_OUT_DT.itemsize == 48 and TRSV_DT.itemsize == 32
 assert SYMCHECK_DT.itemsize == 16 and TRIINV_DT.itemsize == 32 and CHOLBOX_DT.itemsize == 48 and XFORM_DT.itemsize == 48 and XFORMN_DT.itemsize == 48
 assert QRP_DT.itemsize == 48 and BASIS_DT.itemsize == 48 and KBLOCK_DT.itemsize == 40 and STEP_DT.itemsize == 80
@@ -70,7 +71,7 @@ PANEL_WIDTH = 64
 GEMV_CHUNK = 64    # output rows per CTA of h2g_gemv_grouped (csrc/solve.cu GV_CHUNK)
 QR_PANEL_WIDTH = 32
 
-EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_chol_panel_tiles", "h2g_chol_panel", "h2g_chol_panel_sync", "h2g_chol_panel_fused_max", "h2g_trsm_rows", "h2g_copy_tiles", "h2g_block_copy",
+EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_gemm_grouped_ext", "h2g_chol_panel_tiles", "h2g_chol_panel", "h2g_chol_panel_sync", "h2g_chol_panel_fused_max", "h2g_trsm_rows", "h2g_copy_tiles", "h2g_block_copy",
            "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
@@ -94,6 +95,7 @@ def load_library(path=LIB_PATH):
     sig = {
         "h2g_gemm_tiles": (i32, [i32, i32, i32, i32]),
         "h2g_gemm_grouped": (i32, [i32, i32, i32, vp, vp, i32, vp]),
+        "h2g_gemm_grouped_ext": (i32, [i32, i32, i32, vp, vp, vp, i32, vp]),
         "h2g_chol_panel_tiles": (i32, [i32, i32, i32]),
         "h2g_chol_panel": (i32, [vp, i32, vp, i32, vp, vp]),
         "h2g_chol_panel_sync": (i32, [vp, i32, vp, i32, vp, vp, vp]),

@@ -110,6 +110,79 @@ class LevelQR:
                    for i in range(nb) if k[i] == 0])
 
 
+def wy_profitable(n, k, ratio=None):
+    """Whether the compact-WY diag transform beats the dense one on a level: its
+    GEMMs (W = A V~: 2n^2k, the relabelled rank-2k update: ~2n^2k, X and U: 4nk^2)
+    against Q^T (A Q) with the lower-only second product (3n^3), summed over the
+    boxes.  Every box needs k > 0 (k = 0 means q_full = I)."""
+    n = np.asarray(n, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    if not n.size or (k <= 0).any():
+        return False
+    ratio = WY_RATIO if ratio is None else ratio
+    return float((4 * n * n * k + 4 * n * k * k).sum()) < ratio * float((3 * n ** 3).sum())
+
+
+WY_RATIO = float(__import__("os").environ.get("H2G_WY_RATIO", "0.5"))
+
+
+def build_wy(lq, prog):
+    """Compact-WY form of every box's Q (Q = I - V T V^T, k reflectors), stored with
+    the basis for the diag transform (ulv_factor.FactorPlan): Vt = V T, the operand
+    buffers P = [. | V] and Qm = [V | .] (n x 2k; the free halves receive W = A Vt and
+    U = W - V (Vt^T W) per factorization), a k x k scratch X and id_basis's column
+    signs s = sign(diag R) (0 -> +1; dense_core.py:140-144).  T is never formed:
+    with the panel factors T_p of h2g_qr_panel, panel by panel (c = 32 p)
+        Vt[:, c:c+b] = V_p T_p - Vt[:, :c] (V[:, :c]^T (V_p T_p))
+    (the forward accumulation of the block reflectors, Q_0 ... Q_p = I - [V_a V_p]
+    [[T_a, -T_a V_a^T V_p T_p], [0, T_p]] [V_a V_p]^T)."""
+    n, k, nb = lq.n, lq.k, lq.nb
+    dev = lq.device
+    lq.wy_vt = torch.zeros_like(lq.V)
+    lq.wy_poff = 2 * lq.zoff
+    lq.wy_p = torch.zeros(max(int(2 * (n * k).sum()), 1), dtype=F64, device=dev)
+    lq.wy_q = torch.zeros_like(lq.wy_p)
+    lq.wy_x = torch.zeros(max(int((k * k).sum()), 1), dtype=F64, device=dev)
+    kmax = int(k.max()) if nb else 0
+    for c in range(0, kmax, QB):
+        g0, g1, g2 = [], [], []
+        for i in range(nb):
+            ni, ki = int(n[i]), int(k[i])
+            if ki <= c:
+                continue
+            b = min(QB, ki - c)
+            v, vt = lq.ptr(lq.V, lq.zoff[i]), lq.ptr(lq.wy_vt, lq.zoff[i])
+            tp = lq.ptr(lq.T, lq.toff[i] + (c // QB) * QB * QB)
+            g0.append((v + 8 * c, tp, vt + 8 * c, ni, b, b, ki, QB, ki, 0, 1.0, 0.0))          # V_p T_p
+            if c:
+                w = lq.ptr(lq.W, lq.woff[i])
+                g1.append((v, vt + 8 * c, w, c, b, ni, ki, ki, b, 0, 1.0, 0.0))             # X = V_a^T (V_p T_p)
+                g2.append((vt, w, vt + 8 * c, ni, b, c, ki, b, ki, 0, -1.0, 1.0))           # -= Vt_a X
+        prog.gemm(0, 0, g0)
+        prog.gemm(1, 0, g1)
+        prog.gemm(0, 0, g2)
+    cp = []
+    for i in range(nb):
+        ni, ki = int(n[i]), int(k[i])
+        if ki == 0:
+            continue
+        v = lq.ptr(lq.V, lq.zoff[i])
+        cp.append((v, lq.ptr(lq.wy_p, lq.wy_poff[i]) + 8 * ki, ni, ki, ki, 2 * ki, 0))
+        cp.append((v, lq.ptr(lq.wy_q, lq.wy_poff[i]), ni, ki, ki, 2 * ki, 0))
+    prog.copy(cp)
+
+
+def wy_signs(lq):
+    """id_basis's signs s_j = sign(R_jj) (0 -> +1) of every box, from the R left in Z
+    by the QR (one +-1 double per skeleton column, laid out like tau)."""
+    idx = np.concatenate([lq.zoff[i] + np.arange(int(lq.k[i])) * (int(lq.k[i]) + 1) for i in range(lq.nb)]
+                         + [np.zeros(0, dtype=np.int64)]).astype(np.int64)
+    d = lq.Z[torch.from_numpy(idx).to(lq.device)] if idx.size else lq.Z[:0]
+    lq.wy_sgn = torch.where(d < 0, -1.0, 1.0).to(F64)
+    if not idx.size:
+        lq.wy_sgn = torch.ones(1, dtype=F64, device=lq.device)
+
+
 def complete_qr_host(zs, device=None):
     """Complete QR of host matrices Z_i on the GPU; returns [(q_full, frame)]."""
     nat.lib()

@@ -43,9 +43,12 @@ using Cfg64b = GemmCfg<64, 64, 2, 2, 4, H2G_GEMM_STAGES>;   // cfg 2: 4 CTAs/SM,
 using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // cfg 7: 3 CTAs/SM (170 registers), 2 stages (K <= 64 updates)
 using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // cfg 9: small / ragged problems, 32x32 tiles, 6 CTAs/SM
 
-template <class C, bool TA, bool TB>
+// EXT: per-problem extension (h2g_gemm_ext): the beta term read from a separate Cin and, with
+// remap_k >= 0, the compact-WY relabel epilogue of the diag transform (see h2g_gemm_grouped_ext).
+template <class C, bool TA, bool TB, bool EXT = false>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
-                                                                  const int32_t* __restrict__ tile_map) {
+                                                                  const int32_t* __restrict__ tile_map,
+                                                                  const h2g_gemm_ext* __restrict__ ext = nullptr) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + C::STAGES * C::A_DBL;
@@ -84,6 +87,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   double* Cp = P.C;  // may alias A (in-place TRSM with N <= 64)
   const int ldc = P.ldc;
   const double alpha = P.alpha, beta = P.beta;
+  const double* Cin = Cp;   // the beta term's source
+  int ldcin = ldc;
+  if constexpr (EXT) {
+    if (ext[pi].Cin) {
+      Cin = ext[pi].Cin;
+      ldcin = ext[pi].ldcin;
+    }
+  }
   // preload beta/alpha * C so the epilogue is a pure store
   // C preload scale beta/alpha: the common +-1 cases stay off the FP64 pipe (it is the DMMA pipe)
   const int cmode = (beta == 0.0 || alpha == 0.0) ? 0 : beta == alpha ? 1 : beta == -alpha ? 2 : 3;
@@ -95,7 +106,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       const int row = m0 + wm * C::WM + i * 8 + g;
       const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) acc[i][j][e] = (cmode && row < M && col + e < N) ? Cp[(size_t)row * ldc + col + e] : 0.0;
+      for (int e = 0; e < 2; ++e)
+        acc[i][j][e] = (cmode && row < M && col + e < N) ? Cin[(size_t)row * ldcin + col + e] : 0.0;
     }
   if (cmode == 2) {
 #pragma unroll
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
         double* cp = Cp + (size_t)row * ldc + col;
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (col + e < N) cp[e] = beta * cp[e];
+          if (col + e < N) cp[e] = beta * Cin[(size_t)row * ldcin + col + e];
       }
     }
     return;
@@ -225,6 +237,39 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
         acc[i][j][1] *= alpha;
       }
   }
+  if constexpr (EXT) {
+    const int rk = ext[pi].remap_k;
+    if (rk >= 0) {
+      // compact-WY relabel (diag transform, ulv_factor.py:189-200): the tile holds H' = Q^T A Q in
+      // Householder column order (skeleton columns 0..k-1 first); H = q_full^T A q_full puts the
+      // redundant columns first: index a -> a - k (a >= k) or a + (M - k) (a < k), and id_basis's
+      // signs s (dense_core.py:140-144) scale the skeleton rows / columns.  Only a >= b is stored:
+      // every lower entry of H is the image of exactly one lower entry of H' (the SR block lands
+      // transposed), so no entry has two writers.
+      const double* __restrict__ sg = ext[pi].sgn;
+      const int rr = M - rk;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const int a = m0 + wm * C::WM + i * 8 + g;
+        if (a >= M) continue;
+        const int x = a >= rk ? a - rk : a + rr;
+        const bool fa = a < rk && sg[a] < 0.0;
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int b = n0 + wn * C::WN + j * 8 + 2 * tq + e;
+            if (b >= N || b > a) continue;
+            const int y = b >= rk ? b - rk : b + rr;
+            const bool fb = b < rk && sg[b] < 0.0;
+            const double v = (fa != fb) ? neg_int(acc[i][j][e]) : acc[i][j][e];
+            if (x >= y) Cp[(size_t)x * ldc + y] = v;
+            else Cp[(size_t)y * ldc + x] = v;
+          }
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < C::MI; ++i) {
     const int row = m0 + wm * C::WM + i * 8 + g;
@@ -243,16 +288,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
 }
 
-template <class C, bool TA, bool TB>
-static int launch_gemm(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s) {
+template <class C, bool TA, bool TB, bool EXT = false>
+static int launch_gemm(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s,
+                       const h2g_gemm_ext* d_ext = nullptr) {
   static int attr_dev = -1;   // cudaFuncSetAttribute is per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(gemm_grouped_kernel<C, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_grouped_kernel<C, TA, TB, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_dev = dev;
   }
-  gemm_grouped_kernel<C, TA, TB><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map);
+  gemm_grouped_kernel<C, TA, TB, EXT><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map, d_ext);
   return h2g_check_launch("gemm_grouped");
 }
 
@@ -265,7 +311,28 @@ static int dispatch(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, c
   return launch_gemm<C, true, true>(d_probs, d_map, tiles, s);
 }
 
+// EXT variants: NN (the separate-Cin update) and NT (the relabelled symmetric rank-2k update)
+template <class C>
+static int dispatch_ext(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, const h2g_gemm_ext* d_ext,
+                        const int32_t* d_map, int tiles, cudaStream_t s) {
+  if (!trans_a && !trans_b) return launch_gemm<C, false, false, true>(d_probs, d_map, tiles, s, d_ext);
+  if (!trans_a && trans_b) return launch_gemm<C, false, true, true>(d_probs, d_map, tiles, s, d_ext);
+  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: NN or NT only");
+}
+
 }  // namespace h2g
+
+extern "C" int h2g_gemm_grouped_ext(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
+                                    const h2g_gemm_ext* d_ext, const int32_t* d_tile_map, int total_tiles,
+                                    void* stream) {
+  if (total_tiles <= 0) return H2G_OK;
+  if (!d_probs || !d_tile_map || !d_ext) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: null descriptor");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (tile_cfg == 2) return h2g::dispatch_ext<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
+  if (tile_cfg == 7) return h2g::dispatch_ext<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
+  if (tile_cfg == 9) return h2g::dispatch_ext<h2g::Cfg32>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
+  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: unknown tile config %d (2, 7, 9)", tile_cfg);
+}
 
 extern "C" int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg) {
   if (M <= 0 || N <= 0) return 0;

@@ -31,11 +31,13 @@ import torch
 from .trace import ranged
 from . import _native as nat
 from . import dense_core, kernels
-from .basis_qr import LevelQR
+from .basis_qr import LevelQR, build_wy, wy_profitable, wy_signs
 from .dense_core import BasisDecomposition, skeleton_selection, solve_triangular
 from .errors import CoincidentPointsError, SingularTriangularError, StructureError
 from .h2_device import DeviceH2, LevelLayout
 from .program import Program
+
+WY_ENABLED = os.environ.get("H2G_WY", "1") != "0"   # compact-WY diag transform (A/B switch)
 
 F64 = torch.float64
 
@@ -346,6 +348,8 @@ def _construct(kernel, tree, lists, cfg, cloud, device, workers):
                                  z0 + 8 * ka * k[i], kb, k[i], kb, kb, k[i], k[i], 0, 1.0, 0.0))
             prog.gemm(0, 0, prob)
         lq.build(prog)
+        if WY_ENABLED and wy_profitable(n, k):
+            build_wy(lq, prog)          # compact-WY form for the diag transform (FactorPlan)
         q[l] = lq.qfull
         # couplings S_ij = F_i G(SK_i, SK_j) F_j^T for far pairs i > j
         sbuf = torch.empty(max(lay.ssize, 1), dtype=F64, device=device)
@@ -385,6 +389,11 @@ def _construct(kernel, tree, lists, cfg, cloud, device, workers):
     _check_coincident(flag, kernel, cloud, [(eff[(depth, i)], eff[(depth, j)]) for (i, j) in aoff])
 
     dh2 = DeviceH2(device, depth, cloud.count, levels, q, s, leaf_a, aoff)
+    dh2.wy = {}
+    for l, lq in lqs.items():
+        if hasattr(lq, "wy_vt"):
+            wy_signs(lq)
+            dh2.wy[l] = lq
     h2._device = dh2
     h2._build_keep = (lqs, keep)
     h2._choice = choice

@@ -145,7 +145,9 @@ class Program:
 
     # -- step constructors ------------------------------------------------------------
     def gemm(self, trans_a, trans_b, problems, tile_cfg=None):
-        """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta)."""
+        """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta[, ext]) with
+        ext = (Cin, sgn, ldcin, remap_k) (h2g_gemm_ext: a separate beta source and / or the
+        compact-WY relabel store); a launch with any ext carries the array for all its problems."""
         rows = [p for p in problems if p[3] > 0 and p[4] > 0]
         if not rows:
             return 0
@@ -154,9 +156,17 @@ class Program:
             if big and small:
                 return self.gemm(trans_a, trans_b, big) + self.gemm(trans_a, trans_b, small, tile_cfg=9)
         arr = np.zeros(len(rows), dtype=nat.GEMM_DT)
-        cols = list(zip(*rows))
+        cols = list(zip(*[p[:12] for p in rows]))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
             arr[name] = col
+        aux = 0
+        if any(len(p) > 12 for p in rows):
+            ext = np.zeros(len(rows), dtype=nat.GEMM_EXT_DT)
+            ext["remap_k"] = -1
+            for q, p in enumerate(rows):
+                if len(p) > 12:
+                    ext[q] = p[12]
+            aux = ("blob", self._blob(ext))
         cfg = (choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b), ks=arr["K"])
                if tile_cfg is None else tile_cfg)
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
@@ -173,7 +183,8 @@ class Program:
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
         t = nat.GEMM_TILE[cfg]
         ex = int((tiles * 2 * t * t * (-(-k64 // 16) * 16)).sum())   # whole t x t tiles, K padded to 16
-        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex)
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex,
+                  aux=aux)
         return total
 
     def chol_panel(self, descs, npd_ptr):

@@ -56,6 +56,7 @@ F64 = torch.float64
 CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 CHOL_BOX_V = os.environ.get("H2G_CHOL_BOX_V", "0") == "1"
+WY_TRANSFORM = os.environ.get("H2G_WY", "1") != "0"   # compact-WY diag transform where the bases carry it
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -425,21 +426,25 @@ class FactorPlan:
                 prog.record(ev_ss)
                 # ---- diagonal phase (lane 0 = the critical chain)
                 prog.lane = 0
-                prob = []
-                for i in range(nb):
-                    if not mine[i]:
-                        continue
-                    ni = int(n[i])
-                    prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
-                                 0, 1.0, 0.0))
-                prog.gemm(0, 0, prob)
-                # H = Q^T (A Q) is symmetric and only its lower half is ever read
-                # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
-                prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
-                         int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
-                prog.role = "transform"
-                prog.gemm(1, 0, prob)
-                prog.role = None
+                wy = getattr(dh2, "wy", {}).get(l) if WY_TRANSFORM and not self.dist else None
+                if wy is not None:
+                    self._wy_transform(prog, wy, lay, ap, a_off, Hp)
+                else:
+                    prob = []
+                    for i in range(nb):
+                        if not mine[i]:
+                            continue
+                        ni = int(n[i])
+                        prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
+                                     0, 1.0, 0.0))
+                    prog.gemm(0, 0, prob)
+                    # H = Q^T (A Q) is symmetric and only its lower half is ever read
+                    # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
+                    prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
+                             int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
+                    prog.role = "transform"
+                    prog.gemm(1, 0, prob)
+                    prog.role = None
                 B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
                                                                     Qp=qp)
                 if self.dist and self._cross(l, lay):
@@ -528,6 +533,38 @@ class FactorPlan:
         return self._new_program()
 
     # ------------------------------------------------------------------ steps
+    @staticmethod
+    def _wy_transform(prog, lq, lay, ap, a_off, Hp):
+        """diag_mul1/2 (ulv_factor.py:189-200) through the compact-WY form of the
+        bases (basis_qr.build_wy): Q = I - V Vt^T (Vt = V T), so
+            H' = Q^T A Q = A - W V^T - V U^T,  W = A Vt,  U = W - V (Vt^T W)
+        — 2n^2k + 2n^2k + 4nk^2 flops instead of 3n^3 (n = 256, k ~ 43 at the N = 1M
+        leaf: ~4x fewer).  Four grouped GEMMs: W into P[:, :k]; X = Vt^T W; U = W - V X
+        into Qm[:, k:] (beta term from W: a separate Cin); then ONE lower NT GEMM with
+        K = 2k, H = relabel(A - [W | V] [V | U]^T), whose epilogue writes H' entry
+        (a, b) to H in q_full = [q_red | q_skel s] order with id_basis's signs (the
+        relabel store of h2g_gemm_grouped_ext).  Same matrix as Q^T (A Q) up to rounding."""
+        n, k, qo = lay.n, lay.k, lay.qoff
+        boxes = range(lay.nb)
+        P = {i: lq.ptr(lq.wy_p, lq.wy_poff[i]) for i in boxes}
+        Qm = {i: lq.ptr(lq.wy_q, lq.wy_poff[i]) for i in boxes}
+        Vt = {i: lq.ptr(lq.wy_vt, lq.zoff[i]) for i in boxes}
+        X = {i: lq.ptr(lq.wy_x, lq.foff[i]) for i in boxes}
+        A = {i: ap + 8 * a_off[(i, i)] for i in boxes}
+        ni = {i: int(n[i]) for i in boxes}
+        ki = {i: int(k[i]) for i in boxes}
+        prog.gemm(0, 0, [(A[i], Vt[i], P[i], ni[i], ki[i], ni[i], ni[i], ki[i], 2 * ki[i], 0, 1.0, 0.0)
+                         for i in boxes])                                                   # W = A Vt
+        prog.gemm(1, 0, [(Vt[i], P[i], X[i], ki[i], ki[i], ni[i], ki[i], 2 * ki[i], ki[i], 0, 1.0, 0.0)
+                         for i in boxes])                                                   # X = Vt^T W
+        prog.gemm(0, 0, [(Qm[i], X[i], Qm[i] + 8 * ki[i], ni[i], ki[i], ki[i], 2 * ki[i], ki[i], 2 * ki[i], 0,
+                          -1.0, 1.0, (P[i], 0, 2 * ki[i], -1)) for i in boxes])             # U = W - V X
+        prog.role = "transform"
+        sg = {i: lq.ptr(lq.wy_sgn, lq.tauoff[i]) for i in boxes}
+        prog.gemm(0, 1, [(P[i], Qm[i], Hp + 8 * int(qo[i]), ni[i], ni[i], 2 * ki[i], 2 * ki[i], 2 * ki[i], ni[i],
+                          nat.GEMM_LOWER, -1.0, 1.0, (A[i], sg[i], ni[i], ki[i])) for i in boxes], tile_cfg=7)
+        prog.role = None
+
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):
         return partial_cholesky_steps(prog, self.device, self.npd.data_ptr(), Hp, Rp, qo, n, r, slot0, mine, Qp)
 

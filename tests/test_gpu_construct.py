@@ -181,3 +181,62 @@ def test_c2_full_size_flops_and_residual(pkg):
     perm = h2.cloud.perm
     res = np.linalg.norm(pkg.h2_matvec(h2, x[perm]) - b[perm]) / np.linalg.norm(b)
     assert res <= 10 * m["residual"], res
+
+
+def _blocks(f):
+    out = {}
+    for l, lv in f.levels.items():
+        for i in lv.lr_diag:
+            out[("lr", l, i)] = np.array(lv.lr_diag[i])
+            out[("v", l, i)] = np.array(lv.v[i])
+        for key in lv.ls:
+            out[("ls", l) + tuple(key)] = np.array(lv.ls[key])
+        for key in lv.lr_off:
+            out[("lo", l) + tuple(key)] = np.array(lv.lr_off[key])
+    out["root"] = np.array(f.root)
+    return out
+
+
+@pytest.mark.parametrize("shape,n,leaf,family,shift", [("sphere", 16384, 256, "yukawa", 1e5),
+                                                       ("cube", 8192, 64, "laplace", 1e4)])
+def test_compact_wy_transform_equals_dense(pkg, shape, n, leaf, family, shift):
+    """The compact-WY diag transform (bases from the device QR, basis_qr.build_wy;
+    FactorPlan._wy_transform: W = A Vt, X = Vt^T W, U = W - V X, relabelled rank-2k
+    update) gives the same factors as the dense Q^T (A Q) path on the same H2, and
+    the solve matches the CPU oracle."""
+    from paper_2502_02395_b200 import basis_qr, ulv_factor
+
+    ratio = basis_qr.WY_RATIO
+    basis_qr.WY_RATIO = 100.0      # every level with k > 0 everywhere takes it (upper levels too)
+    try:
+        h2 = _build(pkg, shape, n, leaf, family, shift, tol=1e-8, s_far=256, s_near=256)
+    finally:
+        basis_qr.WY_RATIO = ratio
+    dh2 = h2._device
+    assert dh2.depth in dh2.wy and len(dh2.wy) >= 2
+    ks = np.concatenate([dh2.levels[l].k for l in dh2.wy])
+    assert int(np.max(ks)) > 32 and int(np.min(ks)) > 0      # several reflector panels, no k = 0
+    f_wy = pkg.factorize(h2)
+    a = _blocks(f_wy)
+    b = np.random.default_rng(1).standard_normal(h2.count)
+    x_wy = pkg.solve(f_wy, b)
+    del f_wy
+    ulv_factor.clear_cache()
+    old = ulv_factor.WY_TRANSFORM
+    ulv_factor.WY_TRANSFORM = False
+    try:
+        f_dense = pkg.factorize(h2)
+        d = _blocks(f_dense)
+        x_dense = pkg.solve(f_dense, b)
+    finally:
+        ulv_factor.WY_TRANSFORM = old
+        ulv_factor.clear_cache()
+    assert a.keys() == d.keys()
+    # relative 1e-11 per block, with an absolute floor at 1e-14 of the largest factor block
+    # (blocks of near pairs far below the shift's scale carry cancellation from both paths)
+    floor = 1e-14 * max(np.linalg.norm(v) for v in d.values())
+    for key in d:
+        assert np.linalg.norm(a[key] - d[key]) <= 1e-11 * np.linalg.norm(d[key]) + floor, key
+    assert np.linalg.norm(x_wy - x_dense) <= 1e-11 * np.linalg.norm(x_dense)
+    xo = orc.solve(orc.factorize(h2), b)
+    assert np.linalg.norm(x_wy - xo) / np.linalg.norm(xo) < 1e-9
