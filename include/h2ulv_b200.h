@@ -25,6 +25,7 @@
 #ifndef H2ULV_B200_H
 #define H2ULV_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -84,6 +85,18 @@ typedef struct h2g_gemm_ext {
   int32_t ldcin;
   int32_t remap_k;  /* < 0: plain store */
 } h2g_gemm_ext;
+
+/* Deterministic split-K for grouped launches under one wave (few-box upper
+ * levels): every tile is nsplit consecutive CTAs (the tile map lists each
+ * problem's tiles x nsplit CTAs), CTA s accumulates the s-th BK-aligned K
+ * range into d_ws, the last CTA of the tile (per-tile counter) sums the
+ * partials in the order 0..nsplit-1 and applies alpha / beta — independent of
+ * the arrival order.  d_ws: h2g_gemm_split_workspace(tiles, nsplit) bytes,
+ * zeroed once (the counters return to zero after every launch).  As a program
+ * step: GEMM kind, arg = tile_cfg | nsplit << 8, npd = d_ws.  tile_cfg 2. */
+size_t h2g_gemm_split_workspace(int tiles, int nsplit);
+int h2g_gemm_grouped_split(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
+                           const int32_t* d_tile_map, int total_ctas, int nsplit, void* d_ws, void* stream);
 
 int h2g_gemm_grouped_ext(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
                          const h2g_gemm_ext* d_ext, const int32_t* d_tile_map, int total_tiles, void* stream);

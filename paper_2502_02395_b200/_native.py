@@ -71,7 +71,7 @@ PANEL_WIDTH = 64
 GEMV_CHUNK = 64    # output rows per CTA of h2g_gemv_grouped (csrc/solve.cu GV_CHUNK)
 QR_PANEL_WIDTH = 32
 
-EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_gemm_grouped_ext", "h2g_chol_panel_tiles", "h2g_chol_panel", "h2g_chol_panel_sync", "h2g_chol_panel_fused_max", "h2g_trsm_rows", "h2g_copy_tiles", "h2g_block_copy",
+EXPORTS = ["h2g_gemm_tiles", "h2g_gemm_grouped", "h2g_gemm_grouped_ext", "h2g_gemm_grouped_split", "h2g_gemm_split_workspace", "h2g_chol_panel_tiles", "h2g_chol_panel", "h2g_chol_panel_sync", "h2g_chol_panel_fused_max", "h2g_trsm_rows", "h2g_copy_tiles", "h2g_block_copy",
            "h2g_gemv_grouped", "h2g_trsv_batched", "h2g_qr_panel", "h2g_basis_finish", "h2g_kernel_blocks",
            "h2g_run_program", "h2g_run_program_timed", "h2g_exec_ctx_create", "h2g_exec_ctx_destroy",
            "h2g_graph_capture", "h2g_graph_launch", "h2g_graph_destroy", "h2g_abi_version",
@@ -96,6 +96,8 @@ def load_library(path=LIB_PATH):
         "h2g_gemm_tiles": (i32, [i32, i32, i32, i32]),
         "h2g_gemm_grouped": (i32, [i32, i32, i32, vp, vp, i32, vp]),
         "h2g_gemm_grouped_ext": (i32, [i32, i32, i32, vp, vp, vp, i32, vp]),
+        "h2g_gemm_grouped_split": (i32, [i32, i32, i32, vp, vp, i32, i32, vp, vp]),
+        "h2g_gemm_split_workspace": (ctypes.c_size_t, [i32, i32]),
         "h2g_chol_panel_tiles": (i32, [i32, i32, i32]),
         "h2g_chol_panel": (i32, [vp, i32, vp, i32, vp, vp]),
         "h2g_chol_panel_sync": (i32, [vp, i32, vp, i32, vp, vp, vp]),

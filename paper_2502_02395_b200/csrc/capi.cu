@@ -43,6 +43,9 @@ static int run_step(const h2g_step& s, cudaStream_t st) {
     case H2G_STEP_GEMM_TN:
     case H2G_STEP_GEMM_TT: {
       int k = s.kind - H2G_STEP_GEMM_NN;
+      if (s.npd)   /* deterministic split-K: arg = tile_cfg | nsplit << 8, npd = the workspace */
+        return h2g_gemm_grouped_split(k >> 1, k & 1, s.arg & 0xff, (const h2g_gemm_problem*)s.descs, s.map, s.grid,
+                                      s.arg >> 8, (void*)s.npd, st);
       if (s.aux)   /* per-problem extension (separate Cin / compact-WY relabel) */
         return h2g_gemm_grouped_ext(k >> 1, k & 1, s.arg, (const h2g_gemm_problem*)s.descs,
                                     (const h2g_gemm_ext*)s.aux, s.map, s.grid, st);

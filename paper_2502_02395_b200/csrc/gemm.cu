@@ -45,10 +45,17 @@ using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // cfg 9: small / ragged problem
 
 // EXT: per-problem extension (h2g_gemm_ext): the beta term read from a separate Cin and, with
 // remap_k >= 0, the compact-WY relabel epilogue of the diag transform (see h2g_gemm_grouped_ext).
-template <class C, bool TA, bool TB, bool EXT = false>
+// SPLIT: deterministic split-K for launches under one wave (few-box upper levels): every tile
+// is nsplit consecutive CTAs, CTA s of a tile accumulates K range s (BK-aligned), writes its
+// partial tile to ws, and the last CTA to arrive (per-tile counter) sums the partials in the
+// fixed order 0..nsplit-1, adds the beta term and stores C — the same result whatever the
+// arrival order.  ws = [tiles int32 counters, zero between launches | 256 B align | partials].
+template <class C, bool TA, bool TB, bool EXT = false, bool SPLIT = false>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel(const h2g_gemm_problem* __restrict__ probs,
                                                                   const int32_t* __restrict__ tile_map,
-                                                                  const h2g_gemm_ext* __restrict__ ext = nullptr) {
+                                                                  const h2g_gemm_ext* __restrict__ ext = nullptr,
+                                                                  double* __restrict__ ws = nullptr,
+                                                                  int nsplit = 1, int ntiles = 0) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + C::STAGES * C::A_DBL;
@@ -58,6 +65,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   const int pi = tile_map[tile];
   const h2g_gemm_problem P = probs[pi];
   int t = tile - P.tile_start;
+  int split = 0;
+  if constexpr (SPLIT) {
+    split = t % nsplit;
+    t /= nsplit;
+  }
   int tm, tn;
   if (P.flags & H2G_GEMM_LOWER) {
     const int i = tri_row(t);
@@ -70,6 +82,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
   const int m0 = tm * tBM, n0 = tn * tBN;
   const int M = P.M, N = P.N, K = P.K;
+  int kbeg = 0, kend = K;
+  if constexpr (SPLIT) {
+    const int ks = ((K + nsplit - 1) / nsplit + BK - 1) / BK * BK;
+    kbeg = min(K, split * ks);
+    kend = min(K, kbeg + ks);
+  }
   const double* __restrict__ A = P.A;
   const double* __restrict__ B = P.B;
   const int lda = P.lda, ldb = P.ldb;
@@ -107,9 +125,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        acc[i][j][e] = (cmode && row < M && col + e < N) ? Cin[(size_t)row * ldcin + col + e] : 0.0;
+        acc[i][j][e] = (!SPLIT && cmode && row < M && col + e < N) ? Cin[(size_t)row * ldcin + col + e] : 0.0;
     }
-  if (cmode == 2) {
+  if (!SPLIT && cmode == 2) {
 #pragma unroll
     for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -117,7 +135,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
         acc[i][j][0] = neg_int(acc[i][j][0]);
         acc[i][j][1] = neg_int(acc[i][j][1]);
       }
-  } else if (cmode == 3) {
+  } else if (!SPLIT && cmode == 3) {
 #pragma unroll
     for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -135,13 +153,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       int idx = tid + jj * C::THREADS;
       if (!TA) {  // A[m][k] contiguous in k -> As[m][k]
         int m = idx / BK, k = idx % BK;
-        int gm = m0 + m, gk = k0 + k;
-        bool v = gm < M && gk < K;
+        int gm = m0 + m, gk = kbeg + k0 + k;
+        bool v = gm < M && gk < kend;
         cp_async8(as + m * C::S_MK + k, v ? A + (size_t)gm * lda + gk : A, v);
       } else {    // A stored K x M, contiguous in m -> As[k][m]
         int k = idx / tBM, m = idx % tBM;
-        int gm = m0 + m, gk = k0 + k;
-        bool v = gm < M && gk < K;
+        int gm = m0 + m, gk = kbeg + k0 + k;
+        bool v = gm < M && gk < kend;
         cp_async8(as + k * C::SA_KM + m, v ? A + (size_t)gk * lda + gm : A, v);
       }
     }
@@ -150,19 +168,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
       int idx = tid + jj * C::THREADS;
       if (!TB) {  // B[k][n] contiguous in n -> Bs[k][n]
         int k = idx / tBN, n = idx % tBN;
-        int gn = n0 + n, gk = k0 + k;
-        bool v = gn < N && gk < K;
+        int gn = n0 + n, gk = kbeg + k0 + k;
+        bool v = gn < N && gk < kend;
         cp_async8(bs + k * C::SB_KN + n, v ? B + (size_t)gk * ldb + gn : B, v);
       } else {    // B stored N x K, contiguous in k -> Bs[n][k]
         int n = idx / BK, k = idx % BK;
-        int gn = n0 + n, gk = k0 + k;
-        bool v = gn < N && gk < K;
+        int gn = n0 + n, gk = kbeg + k0 + k;
+        bool v = gn < N && gk < kend;
         cp_async8(bs + n * C::S_MK + k, v ? B + (size_t)gn * ldb + gk : B, v);
       }
     }
   };
 
-  const int KT = (K + BK - 1) / BK;
+  const int KT = (kend - kbeg + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
     if (s < KT) load_stage(s, s * BK);
@@ -201,6 +219,59 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
     }
   }
   cp_async_wait<0>();
+
+  if constexpr (SPLIT) {
+    // partial tile -> ws (thread-private fragment order), the last CTA of the tile reduces
+    constexpr int FR = C::MI * C::NI * 2;
+    const int gtile = tile / nsplit;
+    int32_t* counters = reinterpret_cast<int32_t*>(ws);
+    double* parts = ws + ((size_t)ntiles * 4 + 255) / 256 * 32;   // 256-byte aligned after the counters
+    double2* mine = reinterpret_cast<double2*>(parts + ((size_t)tile * C::THREADS + tid) * FR);
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) mine[i * C::NI + j] = make_double2(acc[i][j][0], acc[i][j][1]);
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (tid == 0) last = atomicAdd(&counters[gtile], 1) == nsplit - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const double2* src =
+          reinterpret_cast<const double2*>(parts + ((size_t)(gtile * nsplit + s2) * C::THREADS + tid) * FR);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const double2 v = __ldcg(src + i * C::NI + j);
+          acc[i][j][0] += v.x;
+          acc[i][j][1] += v.y;
+        }
+    }
+    if (tid == 0) counters[gtile] = 0;   // ready for the next launch (graph replay)
+    // the beta term (the unsplit kernel preloads it): acc += beta/alpha * C
+    if (cmode) {
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int row = m0 + wm * C::WM + i * 8 + g;
+          const int col = n0 + wn * C::WN + j * 8 + 2 * tq;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (row >= M || col + e >= N) continue;
+            const double c = Cin[(size_t)row * ldcin + col + e];
+            acc[i][j][e] += cmode == 1 ? c : cmode == 2 ? neg_int(c) : cscale * c;
+          }
+        }
+    }
+  }
 
   // epilogue: C = alpha * acc   (acc already holds beta/alpha * C_old); alpha = +-1 stays off the FP64 pipe
   if (idle_warp) return;
@@ -288,17 +359,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
 }
 
-template <class C, bool TA, bool TB, bool EXT = false>
+template <class C, bool TA, bool TB, bool EXT = false, bool SPLIT = false>
 static int launch_gemm(const h2g_gemm_problem* d_probs, const int32_t* d_map, int tiles, cudaStream_t s,
-                       const h2g_gemm_ext* d_ext = nullptr) {
+                       const h2g_gemm_ext* d_ext = nullptr, double* ws = nullptr, int nsplit = 1) {
   static int attr_dev = -1;   // cudaFuncSetAttribute is per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(gemm_grouped_kernel<C, TA, TB, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_grouped_kernel<C, TA, TB, EXT, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
     attr_dev = dev;
   }
-  gemm_grouped_kernel<C, TA, TB, EXT><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map, d_ext);
+  gemm_grouped_kernel<C, TA, TB, EXT, SPLIT><<<tiles, C::THREADS, C::SMEM, s>>>(d_probs, d_map, d_ext, ws, nsplit,
+                                                                                 tiles / nsplit);
   return h2g_check_launch("gemm_grouped");
 }
 
@@ -320,7 +393,32 @@ static int dispatch_ext(int trans_a, int trans_b, const h2g_gemm_problem* d_prob
   return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: NN or NT only");
 }
 
+template <class C>
+static int dispatch_split(int trans_a, int trans_b, const h2g_gemm_problem* d_probs, const int32_t* d_map,
+                          int ctas, double* ws, int nsplit, cudaStream_t s) {
+  if (!trans_a && !trans_b) return launch_gemm<C, false, false, false, true>(d_probs, d_map, ctas, s, nullptr, ws, nsplit);
+  if (!trans_a && trans_b) return launch_gemm<C, false, true, false, true>(d_probs, d_map, ctas, s, nullptr, ws, nsplit);
+  if (trans_a && !trans_b) return launch_gemm<C, true, false, false, true>(d_probs, d_map, ctas, s, nullptr, ws, nsplit);
+  return launch_gemm<C, true, true, false, true>(d_probs, d_map, ctas, s, nullptr, ws, nsplit);
+}
+
 }  // namespace h2g
+
+extern "C" size_t h2g_gemm_split_workspace(int tiles, int nsplit) {
+  return ((size_t)tiles * 4 + 255) / 256 * 256 + (size_t)tiles * nsplit * 64 * 64 * sizeof(double);
+}
+
+extern "C" int h2g_gemm_grouped_split(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
+                                      const int32_t* d_tile_map, int total_ctas, int nsplit, void* d_ws,
+                                      void* stream) {
+  if (total_ctas <= 0) return H2G_OK;
+  if (!d_probs || !d_tile_map || !d_ws) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_split: null argument");
+  if (nsplit < 1 || total_ctas % nsplit)
+    return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_split: %d CTAs not a multiple of nsplit %d", total_ctas, nsplit);
+  if (tile_cfg != 2) return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_split: tile config %d (2 only)", tile_cfg);
+  return h2g::dispatch_split<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_ctas, (double*)d_ws, nsplit,
+                                          (cudaStream_t)stream);
+}
 
 extern "C" int h2g_gemm_grouped_ext(int trans_a, int trans_b, int tile_cfg, const h2g_gemm_problem* d_probs,
                                     const h2g_gemm_ext* d_ext, const int32_t* d_tile_map, int total_tiles,

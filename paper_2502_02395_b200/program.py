@@ -64,6 +64,29 @@ _TILE32_ALL = float(os.environ.get("H2G_TILE32_ALL", "1.5"))
 _SPLIT_RATIO = float(os.environ.get("H2G_GEMM_SPLIT", "1.5"))
 
 
+_SPLITK = int(os.environ.get("H2G_SPLITK", "1"))   # largest split-K factor (1: off; measured slower in place)
+_SPLITK_OVERHEAD = 48                              # partial write + reduction, in units of K
+
+
+def choose_split(tiles, ks, sms=148, per_sm=4):
+    """Split-K factor of a 64x64-tile launch (h2g_gemm_grouped_split): the S in {1, 2, 4, 8}
+    minimising waves(S) x (K_max / S + overhead), waves(S) = ceil(tiles S / (sms x 4 CTAs)).
+    Only launches under ~2 waves with long K gain (the few-box upper levels)."""
+    if _SPLITK <= 1 or tiles <= 0 or not len(ks):
+        return 1
+    kmax = int(np.max(ks))
+    slots = sms * per_sm
+    best, best_cost = 1, -(-tiles // slots) * kmax
+    s = 2
+    while s <= _SPLITK:
+        if kmax // s >= 64:
+            cost = -(-tiles * s // slots) * (kmax / s + _SPLITK_OVERHEAD)
+            if cost < 0.9 * best_cost:
+                best, best_cost = s, cost
+        s *= 2
+    return best
+
+
 def split_by_tile(problems):
     """(problems for 64x64 tiles, problems for 32x32 tiles): a problem goes to the 32x32
     launch when its 64x64 tiles would execute more than _SPLIT_RATIO x the 32x32 tiles'
@@ -109,6 +132,17 @@ class Program:
         self.n_events = 0
         self.ctx = None
 
+    @property
+    def sms(self):
+        v = self.__dict__.get("_sms")
+        if v is None:
+            try:
+                v = torch.cuda.get_device_properties(self.device).multi_processor_count
+            except (RuntimeError, AssertionError, AttributeError):
+                v = 148
+            self._sms = v
+        return v
+
     # -- blob bookkeeping -------------------------------------------------------------
     def _blob(self, arr):
         if arr is None:
@@ -144,7 +178,7 @@ class Program:
         self._add(nat.STEP["NOP"], 0, 0, wait=ev)
 
     # -- step constructors ------------------------------------------------------------
-    def gemm(self, trans_a, trans_b, problems, tile_cfg=None):
+    def gemm(self, trans_a, trans_b, problems, tile_cfg=None, split=False):
         """problems: iterable of (A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta[, ext]) with
         ext = (Cin, sgn, ldcin, remap_k) (h2g_gemm_ext: a separate beta source and / or the
         compact-WY relabel store); a launch with any ext carries the array for all its problems."""
@@ -154,7 +188,8 @@ class Program:
         if tile_cfg is None and _SPLIT_RATIO > 0 and len(rows) > 1:
             big, small = split_by_tile(rows)
             if big and small:
-                return self.gemm(trans_a, trans_b, big) + self.gemm(trans_a, trans_b, small, tile_cfg=9)
+                return (self.gemm(trans_a, trans_b, big, split=split)
+                        + self.gemm(trans_a, trans_b, small, tile_cfg=9))
         arr = np.zeros(len(rows), dtype=nat.GEMM_DT)
         cols = list(zip(*[p[:12] for p in rows]))
         for name, col in zip(("A", "B", "C", "M", "N", "K", "lda", "ldb", "ldc", "flags", "alpha", "beta"), cols):
@@ -171,10 +206,19 @@ class Program:
                if tile_cfg is None else tile_cfg)
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
                          dtype=np.int64)
-        starts = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+        nsplit = choose_split(int(tiles.sum()), arr["K"], self.sms) if (split and cfg == 2 and not aux) else 1
+        ctas = tiles * nsplit
+        starts = np.concatenate([[0], np.cumsum(ctas)[:-1]])
         arr["tile_start"] = starts
-        total = int(tiles.sum())
-        tmap = np.repeat(np.arange(len(rows), dtype=np.int32), tiles)
+        total = int(ctas.sum())
+        tmap = np.repeat(np.arange(len(rows), dtype=np.int32), ctas)
+        ws = 0
+        if nsplit > 1:
+            wsb = int(nat.lib().h2g_gemm_split_workspace(int(tiles.sum()), nsplit))
+            wst = torch.zeros((wsb + 7) // 8, dtype=torch.float64, device=self.device)
+            self._keep.append(wst)
+            ws = wst.data_ptr()
+            cfg_arg = cfg | (nsplit << 8)
         # K == 0 problems still need their beta*C epilogue; keep them (tiles > 0)
         kind = nat.STEP["GEMM_NN"] + 2 * int(bool(trans_a)) + int(bool(trans_b))
         self._writes((p[2], p[3], p[4], p[8], p[9] & nat.GEMM_LOWER) for p in rows)
@@ -183,8 +227,8 @@ class Program:
         fl = np.where(lower, m64 * (m64 + 1) * k64, 2 * m64 * n64 * k64).sum()
         t = nat.GEMM_TILE[cfg]
         ex = int((tiles * 2 * t * t * (-(-k64 // 16) * 16)).sum())   # whole t x t tiles, K padded to 16
-        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl, arg=cfg, exec_flops=ex,
-                  aux=aux)
+        self._add(kind, len(rows), total, self._blob(arr), self._blob(tmap), flops=fl,
+                  arg=cfg_arg if nsplit > 1 else cfg, exec_flops=ex, aux=aux, npd=ws)
         return total
 
     def chol_panel(self, descs, npd_ptr):

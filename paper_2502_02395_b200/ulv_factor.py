@@ -57,6 +57,8 @@ CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 CHOL_BOX_V = os.environ.get("H2G_CHOL_BOX_V", "0") == "1"
 WY_TRANSFORM = os.environ.get("H2G_WY", "1") != "0"   # compact-WY diag transform where the bases carry it
+# tile configs of the WY launches (A/B knobs; "" = the planner's choice): W = A Vt, X, U, the relabelled update
+_WY_CFG = [int(c) if c else None for c in os.environ.get("H2G_WY_CFG", ",,,7").split(",")]
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -415,12 +417,12 @@ class FactorPlan:
                     prog.wait(merge_ev)
                 prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], qp + 8 * (qo[j] + r[j]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   int(n[i]), int(k[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off])
+                                 for (i, j) in own_off], split=True)
                 prog.role = "transform"
                 prog.gemm(1, 0, [(qp + 8 * (qo[i] + r[i]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   Tp + 8 * (B.toff[(i, j)] + r[i] * n[j] + r[j]),
                                   int(k[i]), int(k[j]), int(n[i]), int(n[i]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off])
+                                 for (i, j) in own_off], split=True)
                 prog.role = None
                 ev_ss = prog.event()
                 prog.record(ev_ss)
@@ -437,13 +439,13 @@ class FactorPlan:
                         ni = int(n[i])
                         prob.append((ap + 8 * a_off[(i, i)], qp + 8 * qo[i], Mp + 8 * qo[i], ni, ni, ni, ni, ni, ni,
                                      0, 1.0, 0.0))
-                    prog.gemm(0, 0, prob)
+                    prog.gemm(0, 0, prob, split=True)
                     # H = Q^T (A Q) is symmetric and only its lower half is ever read
                     # (partial Cholesky, L(s)_ii, the SS merge): lower tiles only
                     prob = [(qp + 8 * qo[i], Mp + 8 * qo[i], Hp + 8 * qo[i], int(n[i]), int(n[i]), int(n[i]),
                              int(n[i]), int(n[i]), int(n[i]), nat.GEMM_LOWER, 1.0, 0.0) for i in range(nb) if mine[i]]
                     prog.role = "transform"
-                    prog.gemm(1, 0, prob)
+                    prog.gemm(1, 0, prob, split=True)
                     prog.role = None
                 B.linv, B.loff, ev_v = self._partial_cholesky_steps(prog, Hp, Rp, qo, n, r, self.slot_base[l], mine,
                                                                     Qp=qp)
@@ -461,7 +463,7 @@ class FactorPlan:
                         prog.wait(ev)
                 prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], B.R.ptr(qo[j]), MOp + 8 * B.toff[(i, j)],
                                   int(n[i]), int(r[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off])
+                                 for (i, j) in own_off], split=True)
                 prob = []
                 for (i, j) in own_off:
                     ni, nj, ri, rj, kj = int(n[i]), int(n[j]), int(r[i]), int(r[j]), int(k[j])
@@ -470,7 +472,7 @@ class FactorPlan:
                     prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
                                  0, 1.0, 0.0))
                 prog.role = "transform"
-                prog.gemm(1, 0, prob)
+                prog.gemm(1, 0, prob, split=True)
                 prog.role = None
                 prog.lane = 0
                 # ---- merge into the parent level (or the root)
@@ -554,15 +556,16 @@ class FactorPlan:
         ni = {i: int(n[i]) for i in boxes}
         ki = {i: int(k[i]) for i in boxes}
         prog.gemm(0, 0, [(A[i], Vt[i], P[i], ni[i], ki[i], ni[i], ni[i], ki[i], 2 * ki[i], 0, 1.0, 0.0)
-                         for i in boxes])                                                   # W = A Vt
+                         for i in boxes], tile_cfg=_WY_CFG[0])                              # W = A Vt
         prog.gemm(1, 0, [(Vt[i], P[i], X[i], ki[i], ki[i], ni[i], ki[i], 2 * ki[i], ki[i], 0, 1.0, 0.0)
-                         for i in boxes])                                                   # X = Vt^T W
+                         for i in boxes], tile_cfg=_WY_CFG[1])                              # X = Vt^T W
         prog.gemm(0, 0, [(Qm[i], X[i], Qm[i] + 8 * ki[i], ni[i], ki[i], ki[i], 2 * ki[i], ki[i], 2 * ki[i], 0,
-                          -1.0, 1.0, (P[i], 0, 2 * ki[i], -1)) for i in boxes])             # U = W - V X
+                          -1.0, 1.0, (P[i], 0, 2 * ki[i], -1)) for i in boxes], tile_cfg=_WY_CFG[2])   # U = W - V X
         prog.role = "transform"
         sg = {i: lq.ptr(lq.wy_sgn, lq.tauoff[i]) for i in boxes}
         prog.gemm(0, 1, [(P[i], Qm[i], Hp + 8 * int(qo[i]), ni[i], ni[i], 2 * ki[i], 2 * ki[i], 2 * ki[i], ni[i],
-                          nat.GEMM_LOWER, -1.0, 1.0, (A[i], sg[i], ni[i], ki[i])) for i in boxes], tile_cfg=7)
+                          nat.GEMM_LOWER, -1.0, 1.0, (A[i], sg[i], ni[i], ki[i])) for i in boxes],
+                  tile_cfg=_WY_CFG[3])
         prog.role = None
 
     def _partial_cholesky_steps(self, prog, Hp, Rp, qo, n, r, slot0, mine=None, Qp=0):

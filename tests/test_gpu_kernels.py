@@ -206,3 +206,50 @@ def test_block_copy_modes(env, rows, cols):
     torch.cuda.synchronize()
     for d, ref in zip(outs, refs):
         np.testing.assert_array_equal(d.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("alpha,beta", [(1.0, 0.0), (-1.0, 1.0), (0.5, -2.0)])
+def test_gemm_split_k(env, ta, tb, alpha, beta):
+    """Deterministic split-K (h2g_gemm_grouped_split, picked by Program.gemm(split=True) for
+    launches under one wave with long K): every split factor against numpy, the LOWER
+    flag, alpha / beta, and bit-identical results on a replay (fixed reduction order)."""
+    import paper_2502_02395_b200.program as pm
+
+    torch, nat, Program = env
+    rng = np.random.default_rng(7 + 4 * ta + 2 * tb)
+    shapes = [(150, 150, 700, True), (70, 130, 517, False), (64, 64, 1000, False), (33, 9, 300, False)]
+    for nsplit in (2, 4, 8):
+        hold, probs, refs = [], [], []
+        for (m, n, k, lower) in shapes:
+            a = rng.standard_normal((k, m) if ta else (m, k))
+            b = rng.standard_normal((n, k) if tb else (k, n))
+            c = rng.standard_normal((m, n))
+            ref = alpha * (a.T if ta else a) @ (b.T if tb else b) + beta * c
+            t = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (a, b, c)]
+            hold.append((t, c.copy()))
+            probs.append((t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), m, n, k, a.shape[1], b.shape[1], n,
+                          nat.GEMM_LOWER if lower else 0, alpha, beta))
+            refs.append(ref)
+        old = pm.choose_split
+        pm.choose_split = lambda tiles, ks, sms=148, per_sm=4: nsplit
+        try:
+            prog = Program(torch.device("cuda"))
+            prog.gemm(ta, tb, probs, tile_cfg=2, split=True)
+        finally:
+            pm.choose_split = old
+        assert prog._steps[-1]["arg"] >> 8 == nsplit and prog._steps[-1]["npd"]
+        prog.finalize()
+        outs = []
+        for rep in range(2):
+            for (t, c0) in hold:
+                t[2].copy_(torch.from_numpy(c0))
+            prog.run()
+            torch.cuda.synchronize()
+            outs.append([t[2].cpu().numpy() for (t, _) in hold])
+        for got, again, ref, (m, n, k, lower) in zip(outs[0], outs[1], refs, shapes):
+            assert np.array_equal(got, again)
+            if lower:
+                keep = np.tril(np.ones((m, n), dtype=bool))
+                got, ref = np.where(keep, got, 0.0), np.where(keep, ref, 0.0)
+            np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))

@@ -10,7 +10,7 @@ HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))
 
 def test_header_symbols_exported():
     text = open(HEADER).read()
-    declared = sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(h2g_\w+)\s*\(", text, re.M)))
+    declared = sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(h2g_\w+)\s*\(", text, re.M)))
     assert declared, "no declarations parsed"
     lib = _native.load_library()
     missing = [s for s in declared if not hasattr(lib, s)]
