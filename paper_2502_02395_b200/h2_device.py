@@ -128,6 +128,17 @@ def _q_interleave(levels, q, device):
     return qsplit, progs
 
 
+_FIX_STREAM = {}
+
+
+def _fix_stream(device):
+    st = _FIX_STREAM.get(device)
+    if st is None:
+        st = torch.cuda.Stream(device=device, priority=-1)
+        _FIX_STREAM[device] = st
+    return st
+
+
 class DeviceH2:
     """Device copy of everything factorize/solve read from an H2Matrix."""
 
@@ -205,21 +216,39 @@ class DeviceH2:
         q, s, leaf_a, qsplit, qprog = into.q, into.s, into.leaf_a, into._qsplit, into._qprog
         regions, off = into.staging_regions()
         st = stream if stream is not None else torch.cuda.current_stream(device)
+        # the q interleave kernels run on their own high-priority stream: on the copy stream they
+        # would hold back the next DMA until they got SMs away from the factorization
+        fix = _fix_stream(device)
+        st.wait_stream(fix)                   # an earlier upload's interleave still reading qsplit
+
+        def level_done(l):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            fix.wait_event(ev)
+            if on_level is not None:
+                ev2 = torch.cuda.Event()
+                ev2.record(fix)
+                on_level(l, ev2)
+
+        def interleave(l):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            fix.wait_event(ev)
+            qprog[l].run(fix)
+
         arena = getattr(h2, "_arena", None)
         if arena is not None and arena.signature == into.signature() and arena.intact(h2):
             # the blocks already sit in one pinned buffer in staging layout (to_pinned_host):
-            # one DMA per region, no host gather
+            # one DMA per region back to back, no host gather
             with torch.cuda.stream(st):
                 for kind, l, base, size in regions:
                     dst = qsplit[l] if kind == "q" else s[l] if kind == "s" else leaf_a
                     dst[:size].copy_(arena.tensor[base:base + size], non_blocking=True)
                     if kind == "q":
-                        qprog[l].run(st)
+                        interleave(l)
                     if (kind == "s" and l != depth) or kind == "a":   # level l complete
-                        if on_level is not None:
-                            ev = torch.cuda.Event()
-                            ev.record(st)
-                            on_level(l, ev)
+                        level_done(l)
+            st.wait_stream(fix)
             if stream is None:
                 st.synchronize()
             return into
@@ -262,11 +291,9 @@ class DeviceH2:
                 fu.result()
                 dst[c0:c1].copy_(host_t[base + c0:base + c1], non_blocking=True)
                 if last_of.get(l) == idx:
-                    qprog[l].run(st)             # [q_red | q_skel] rows of level l, on the device
-                    if on_level is not None:
-                        ev = torch.cuda.Event()
-                        ev.record(st)
-                        on_level(l, ev)
+                    interleave(l)                # [q_red | q_skel] rows of level l, on the device
+                    level_done(l)
+        st.wait_stream(fix)
         done = torch.cuda.Event()
         done.record(st)
         _STAGING["done"] = done
