@@ -396,7 +396,7 @@ int h2g_direct_matvec(const double* d_points, const double* d_x, double* d_y, in
  * Linv + 4096 q, ld 64, identity beyond n), so h2g_trsm_rows can solve
  * against any triangular factor; the first zero diagonal entry j records
  * atomicMin(&d_status[status_slot], j) (SingularTriangularError,
- * dense_core.py:75-76).  One CTA per diagonal block: d_tile_map[t] =
+ * dense_core.py:75-76); Linv == NULL: that check only.  One CTA per diagonal block: d_tile_map[t] =
  * descriptor of block CTA t, tile_start = its first block CTA.
  */
 typedef struct h2g_symcheck_desc {

@@ -10,7 +10,8 @@
 //                      L: the block's inverse (the Linv layout the Cholesky
 //                      panels write, so h2g_trsm_rows can solve against any
 //                      triangular factor) and the first zero diagonal entry
-//                      (SingularTriangularError, dense_core.py:75-76).
+//                      (SingularTriangularError, dense_core.py:75-76); with
+//                      Linv == NULL only the diagonal check.
 #include <climits>
 
 #include "common.cuh"
@@ -18,7 +19,6 @@
 namespace h2g {
 
 constexpr int BO_PB = 64;
-constexpr int BO_SD = 65;   // smem stride of the inverse (column-per-thread access)
 
 __global__ void __launch_bounds__(256) sym_check_kernel(const h2g_symcheck_desc* __restrict__ descs,
                                                         unsigned long long* __restrict__ out) {
@@ -54,32 +54,45 @@ __global__ void __launch_bounds__(256) sym_check_kernel(const h2g_symcheck_desc*
 }
 
 // Block q of matrix P: rows/cols p = 64q .. p+b-1.  Thread j < 64 solves
-// L_qq x = e_j by forward substitution down its column (the rows of L are
-// broadcast from shared memory); rows/cols >= b hold the identity.
+// L_qq x = e_j down its column, right-looking: the column's 64 partial sums
+// live in registers and step i, once x_i = s_i / L_ii is known, updates the
+// rows below with independent FMAs (the rows of L are broadcast from shared
+// memory).  Every element gets the same FMA sequence (m = j .. i-1 in order)
+// and the same division as a left-looking dot product, so the bits are those
+// of the plain forward substitution; only the dependency chain is 64x shorter.
+// Rows/cols >= b hold the identity.
 __global__ void __launch_bounds__(BO_PB) tri_inv_kernel(const h2g_triinv_desc* __restrict__ descs,
                                                         const int32_t* __restrict__ tile_map,
                                                         int32_t* __restrict__ status) {
-  extern __shared__ __align__(16) double bsm[];
-  double (*Ls)[BO_PB + 1] = reinterpret_cast<double (*)[BO_PB + 1]>(bsm);
-  double (*X)[BO_SD] = reinterpret_cast<double (*)[BO_SD]>(bsm + BO_PB * (BO_PB + 1));
+  __shared__ double Ls[BO_PB][BO_PB + 1];
   const int pi = tile_map[blockIdx.x];
   const h2g_triinv_desc P = descs[pi];
   const int q = blockIdx.x - P.tile_start;
   const int p = BO_PB * q, b = min(BO_PB, P.n - p);
   const int j = threadIdx.x;
+  if (P.Linv == nullptr) {   // check only: the first zero diagonal entry (SingularTriangularError)
+    if (j < b && P.L[(size_t)(p + j) * P.ldl + p + j] == 0.0) atomicMin(&status[P.status_slot], p + j);
+    return;
+  }
   for (int i = 0; i < BO_PB; ++i) Ls[i][j] = (i < b && j < b && j <= i) ? P.L[(size_t)(p + i) * P.ldl + p + j]
                                                                         : (i == j ? 1.0 : 0.0);
   __syncthreads();
   if (j < b && Ls[j][j] == 0.0) atomicMin(&status[P.status_slot], p + j);
+  double sc[BO_PB];
+#pragma unroll
+  for (int r = 0; r < BO_PB; ++r) sc[r] = (r == j) ? 1.0 : 0.0;
+#pragma unroll
   for (int i = 0; i < BO_PB; ++i) {
-    double s = (i == j) ? 1.0 : 0.0;
-    if (i > j) {
-      for (int m = j; m < i; ++m) s = fma(-Ls[i][m], X[m][j], s);
+    const double x = (i >= j) ? sc[i] / Ls[i][i] : 0.0;
+    sc[i] = x;
+    if (i >= j) {
+#pragma unroll
+      for (int r = i + 1; r < BO_PB; ++r) sc[r] = fma(-Ls[r][i], x, sc[r]);
     }
-    X[i][j] = (i >= j) ? s / Ls[i][i] : 0.0;
   }
   double* out = P.Linv + (size_t)q * BO_PB * BO_PB;
-  for (int i = 0; i < BO_PB; ++i) out[(size_t)i * BO_PB + j] = X[i][j];
+#pragma unroll
+  for (int i = 0; i < BO_PB; ++i) out[(size_t)i * BO_PB + j] = sc[i];
 }
 
 }  // namespace h2g
@@ -95,14 +108,6 @@ extern "C" int h2g_tri_inv(const h2g_triinv_desc* d_descs, const int32_t* d_tile
                            int32_t* d_status, void* stream) {
   if (total_tiles <= 0) return H2G_OK;
   if (!d_descs || !d_tile_map || !d_status) return h2g_set_error(H2G_EINVAL, "h2g_tri_inv: null argument");
-  constexpr int smem = (int)(sizeof(double) * h2g::BO_PB * (h2g::BO_PB + 1 + h2g::BO_SD));
-  static int attr_dev = -1;   // per-process, re-applied when the current device changes
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaFuncSetAttribute(h2g::tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_dev = dev;
-  }
-  h2g::tri_inv_kernel<<<total_tiles, h2g::BO_PB, smem, (cudaStream_t)stream>>>(d_descs, d_tile_map, d_status);
+  h2g::tri_inv_kernel<<<total_tiles, h2g::BO_PB, 0, (cudaStream_t)stream>>>(d_descs, d_tile_map, d_status);
   return h2g_check_launch("tri_inv");
 }

@@ -128,18 +128,35 @@ class SolvePlan:
         prog = Program(dev)
         self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
         self.linv, self.loff, self.wt, self.mblk = {}, {}, {}, {}
+        # levels are independent: each level's steps on one lane (in order), the levels spread
+        # over lanes 1..4, the root's latency-bound inverse chain alone on lane 0
+        d = fp.root_dim
+        nb0 = -(-d // W)
+        self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
+        self.root_w = torch.zeros(max(d * d, 1), dtype=F64, device=dev)
+        rp = fp.root_buf.data_ptr()
+        prog.lane = 0
+        prog.triinv([(rp, self.root_linv.data_ptr(), d, d, 0)], self._tri_status.data_ptr())
+        prog.trsm_rows([(rp, 0, self.root_w.data_ptr(), self.root_linv.data_ptr(), d, d, 0, nb0, d, d)])
         for l in range(fp.depth, 0, -1):
+            prog.lane = 1 + (fp.depth - l) % 4
             B = fp.bufs[l]
             lay = B.lay
             nblk = -(-np.asarray(lay.r, dtype=np.int64) // W)
             loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
-            lt = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
-            self.linv[l], self.loff[l] = lt, loff
             mine = self._mine(l)
-            # (also on fused levels: it is what detects a singular L(r)_ii, SingularTriangularError)
-            prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
-                          int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
-                        self._tri_status.data_ptr())
+            if self.fused[l]:
+                # no TRSV reads a fused level's inverses (both modes transform only): just the
+                # zero-diagonal check that raises SingularTriangularError
+                self.linv[l], self.loff[l] = None, loff
+                prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, int(lay.r[i]), int(lay.n[i]), 0)
+                             for i in range(lay.nb) if mine[i] and lay.r[i] > 0], self._tri_status.data_ptr())
+            else:
+                lt = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
+                self.linv[l], self.loff[l] = lt, loff
+                prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
+                              int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
+                            self._tri_status.data_ptr())
             if self.winv[l]:
                 roff = np.concatenate([[0], np.cumsum(np.asarray(lay.r, dtype=np.int64) ** 2)[:-1]])
                 wt = torch.zeros(max(int((np.asarray(lay.r, dtype=np.int64) ** 2).sum()), 1), dtype=F64, device=dev)
@@ -180,13 +197,7 @@ class SolvePlan:
                             gm.append((B.R.ptr(o), B.H.data_ptr() + 8 * (o + ri * ni), B.R.ptr(o + ri),
                                        ni, ki, ri, ni, ni, ni, 0, -1.0, 1.0))
                     prog.gemm(0, 1, gm)
-        d = fp.root_dim
-        nb0 = -(-d // W)
-        self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
-        self.root_w = torch.zeros(max(d * d, 1), dtype=F64, device=dev)
-        rp = fp.root_buf.data_ptr()
-        prog.triinv([(rp, self.root_linv.data_ptr(), d, d, 0)], self._tri_status.data_ptr())
-        prog.trsm_rows([(rp, 0, self.root_w.data_ptr(), self.root_linv.data_ptr(), d, d, 0, nb0, d, d)])
+        prog.lane = 0
         self.prepare = prog.finalize()
         self.prepare.capture()
         self._prepared = None
@@ -704,10 +715,17 @@ def solve(factors, b, mode="parallel"):
 
 def _solve_on(factors, sp, bm, vector):
     dev = sp.device
-    perm = factors.__dict__.get("_perm_dev")
-    if perm is None:
-        perm = torch.from_numpy(np.asarray(factors.h2.cloud.perm, dtype=np.int64)).to(dev, non_blocking=True)
-        factors._perm_dev = perm
+    # the tree permutation is structure (like the cached plans): uploaded once per cloud / device
+    cloud = factors.h2.cloud
+    cached = cloud.__dict__.get("_perm_dev")
+    if cached is not None and cached[0] is cloud.perm and cached[1].device == dev:
+        perm = cached[1]
+    else:
+        perm = torch.from_numpy(np.asarray(cloud.perm, dtype=np.int64)).to(dev, non_blocking=True)
+        try:
+            cloud._perm_dev = (cloud.perm, perm)
+        except AttributeError:   # a frozen / slotted cloud: no cache
+            pass
     b_dev = torch.from_numpy(np.ascontiguousarray(bm)).to(dev)
     sp.xin.view(-1, sp.w)[:factors.h2.count] = b_dev.index_select(0, perm)
     sp.run_forward()

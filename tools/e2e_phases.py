@@ -34,3 +34,19 @@ for rep in range(4):
     print(f"rep {rep}: intact {1e3 * (t1 - t0):.1f} ms (={ok})  factorize {1e3 * (t2 - t1):.1f} ms  "
           f"solve {1e3 * (t3 - t2):.1f} ms  total {1e3 * (t3 - t0):.1f}", flush=True)
     del f
+
+# raw H2D rate of the same pinned arena: one copy, and the per-region copies alone
+arena = hh._arena
+dev = torch.empty(arena.tensor.numel(), dtype=arena.tensor.dtype, device="cuda")
+for rep in range(2):
+    t0 = T()
+    dev.copy_(arena.tensor, non_blocking=True)
+    t1 = T()
+    print(f"one H2D copy of the arena: {arena.tensor.numel() * 8 / 1e9:.2f} GB in {1e3 * (t1 - t0):.1f} ms "
+          f"= {arena.tensor.numel() * 8 / (t1 - t0) / 1e9:.1f} GB/s", flush=True)
+f = pkg.factorize(hh)
+for rep in range(2):
+    t0 = T()
+    f = pkg.factorize(hh)
+    t1 = T()
+    print(f"factorize again: {1e3 * (t1 - t0):.1f} ms", flush=True)
