@@ -78,12 +78,15 @@ int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg); /* tiles one problem 
  *   entry (a, b), a >= b, goes to H[x][y] (or H[y][x] when x < y) with
  *   x = a - k (a >= k) or a + M - k (a < k), sign-flipped by sgn[a] (a < k)
  *   and sgn[b] (b < k).  Only a >= b is stored, so each lower entry of H has
- *   exactly one writer.  A step carries the ext array in `aux`. */
+ *   exactly one writer.  A step carries the ext array in `aux`.
+ *   remap_k <= -2 relabels columns only (k = -remap_k - 2): column b of the
+ *   product goes to column b - k (b >= k) or b + N - k (b < k), sign-flipped
+ *   by sgn[b] (b < k) — q_full = [Q[:, k:] | Q[:, :k] s] from Q = I - Yt Y^T. */
 typedef struct h2g_gemm_ext {
   const double* Cin;
   const double* sgn;
   int32_t ldcin;
-  int32_t remap_k;  /* < 0: plain store */
+  int32_t remap_k;  /* >= 0: symmetric relabel; -1: plain store; <= -2: column relabel */
 } h2g_gemm_ext;
 
 /* Deterministic split-K for grouped launches under one wave (few-box upper

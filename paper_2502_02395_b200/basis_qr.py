@@ -161,15 +161,81 @@ def build_wy(lq, prog):
         prog.gemm(0, 0, g0)
         prog.gemm(1, 0, g1)
         prog.gemm(0, 0, g2)
+    wy_operands(lq, prog)
+
+
+def wy_operands(lq, prog):
+    """The constant halves of the WY operand buffers: Y into P[:, k:] and Qm[:, :k]."""
     cp = []
-    for i in range(nb):
-        ni, ki = int(n[i]), int(k[i])
+    for i in range(lq.nb):
+        ni, ki = int(lq.n[i]), int(lq.k[i])
         if ki == 0:
             continue
         v = lq.ptr(lq.V, lq.zoff[i])
         cp.append((v, lq.ptr(lq.wy_p, lq.wy_poff[i]) + 8 * ki, ni, ki, ki, 2 * ki, 0))
         cp.append((v, lq.ptr(lq.wy_q, lq.wy_poff[i]), ni, ki, ki, 2 * ki, 0))
     prog.copy(cp)
+
+
+_IDENT = {}
+
+
+def _identity(device, n):
+    t = _IDENT.get(device)
+    if t is None or t.shape[0] < n:
+        t = torch.eye(max(n, 1), dtype=F64, device=device)
+        _IDENT[device] = t
+    return t
+
+
+def rebuild_qfull(lq, prog, q_ptr):
+    """q_full_i = [Q[:, k:] | Q[:, :k] s] from the compact-WY form, Q = I - Yt Y^T: one NT
+    GEMM per box (beta term from a shared identity) whose column-relabel store writes the
+    [q_red | q_skel s] order with id_basis's signs (dense_core.py:140-148).  Used at
+    construct (so the device q_full IS this product) and after a compact upload of a
+    pinned-host H2 (DeviceH2.from_host), which therefore rebuilds the same bits."""
+    nmax = int(lq.n.max()) if lq.nb else 1
+    ident = _identity(lq.device, nmax)
+    lq._ident = ident                  # keeps the buffer the program points into alive
+    ldi = int(ident.shape[0])          # the shared identity may be larger than this level's n
+    prob = []
+    for i in range(lq.nb):
+        ni, ki = int(lq.n[i]), int(lq.k[i])
+        yt, y = lq.ptr(lq.wy_vt, lq.zoff[i]), lq.ptr(lq.V, lq.zoff[i])
+        prob.append((yt, y, q_ptr(i), ni, ni, ki, ki, ki, ni, 0, -1.0, 1.0,
+                     (ident.data_ptr(), lq.ptr(lq.wy_sgn, lq.tauoff[i]), ldi, -(ki + 2))))
+    prog.gemm(0, 1, prob, tile_cfg=2)
+
+
+class WYLevel:
+    """Device buffers of the compact-WY form of one level's bases uploaded from a
+    pinned-host H2 (the fields FactorPlan._wy_transform and rebuild_qfull read; the
+    construct keeps them on its LevelQR instead)."""
+
+    def __init__(self, device, n, k):
+        self.device = device
+        self.n = np.asarray(n, dtype=np.int64)
+        self.k = np.asarray(k, dtype=np.int64)
+        self.nb = len(self.n)
+        self.zoff = np.concatenate([[0], np.cumsum(self.n * self.k)[:-1]]).astype(np.int64)
+        self.foff = np.concatenate([[0], np.cumsum(self.k * self.k)[:-1]]).astype(np.int64)
+        self.tauoff = np.concatenate([[0], np.cumsum(self.k)[:-1]]).astype(np.int64)
+        self.wy_poff = 2 * self.zoff
+        nk = max(int((self.n * self.k).sum()), 1)
+        self.V = torch.zeros(nk, dtype=F64, device=device)
+        self.wy_vt = torch.zeros(nk, dtype=F64, device=device)
+        self.wy_sgn = torch.ones(max(int(self.k.sum()), 1), dtype=F64, device=device)
+        self.wy_p = torch.zeros(2 * nk, dtype=F64, device=device)
+        self.wy_q = torch.zeros(2 * nk, dtype=F64, device=device)
+        self.wy_x = torch.zeros(max(int((self.k * self.k).sum()), 1), dtype=F64, device=device)
+
+    def ptr(self, t, off):
+        return t.data_ptr() + 8 * int(off)
+
+    def sizes(self):
+        """(Y, Yt, signs) element counts: the layout of a pinned arena's "w" region."""
+        nk = int((self.n * self.k).sum())
+        return nk, nk, int(self.k.sum())
 
 
 def wy_signs(lq):

@@ -310,6 +310,28 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) gemm_grouped_kernel
   }
   if constexpr (EXT) {
     const int rk = ext[pi].remap_k;
+    if (rk <= -2) {
+      // column relabel (q_full = [Q[:, k:] | Q[:, :k] s] from Q = I - Yt Y^T, k = -remap_k - 2;
+      // dense_core.py:140-148): column b -> b - k (b >= k) or b + (N - k) (b < k), signed by s_b
+      const double* __restrict__ sg = ext[pi].sgn;
+      const int kc = -rk - 2, rr = N - kc;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const int a = m0 + wm * C::WM + i * 8 + g;
+        if (a >= M) continue;
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int b = n0 + wn * C::WN + j * 8 + 2 * tq + e;
+            if (b >= N) continue;
+            const int y = b >= kc ? b - kc : b + rr;
+            const double v = (b < kc && sg[b] < 0.0) ? neg_int(acc[i][j][e]) : acc[i][j][e];
+            Cp[(size_t)a * ldc + y] = v;
+          }
+      }
+      return;
+    }
     if (rk >= 0) {
       // compact-WY relabel (diag transform, ulv_factor.py:189-200): the tile holds H' = Q^T A Q in
       // Householder column order (skeleton columns 0..k-1 first); H = q_full^T A q_full puts the

@@ -31,7 +31,7 @@ import torch
 from .trace import ranged
 from . import _native as nat
 from . import dense_core, kernels
-from .basis_qr import LevelQR, build_wy, wy_profitable, wy_signs
+from .basis_qr import LevelQR, build_wy, rebuild_qfull, wy_profitable, wy_signs
 from .dense_core import BasisDecomposition, skeleton_selection, solve_triangular
 from .errors import CoincidentPointsError, SingularTriangularError, StructureError
 from .h2_device import DeviceH2, LevelLayout
@@ -394,6 +394,14 @@ def _construct(kernel, tree, lists, cfg, cloud, device, workers):
         if hasattr(lq, "wy_vt"):
             wy_signs(lq)
             dh2.wy[l] = lq
+    if dh2.wy:
+        # q_full of a compact-WY level IS relabel(I - Yt Y^T) (the product a compact upload of
+        # to_pinned_host(h2) rebuilds on the device, so both paths hold the same bits)
+        p2 = Program(device)
+        for l, lq in dh2.wy.items():
+            rebuild_qfull(lq, p2, lambda i, lq=lq: lq.ptr(lq.qfull, lq.qoff[i]))
+        p2.finalize().run()
+        torch.cuda.synchronize(device)
     h2._device = dh2
     h2._build_keep = (lqs, keep)
     h2._choice = choice
@@ -482,6 +490,14 @@ def to_pinned_host(h2):
         prog.copy(descs)
     prog.finalize().run()
     for kind, l, base, size in regions:
+        if kind == "w":   # compact-WY level: Y, Yt, signs (uploaded instead of q_full)
+            lq = lqs[l]
+            nk, k = int((lq.n * lq.k).sum()), int(lq.k.sum())
+            o = base
+            for t, m in ((lq.V, nk), (lq.wy_vt, nk), (lq.wy_sgn, k)):
+                arena_t[o:o + m].copy_(t[:m])
+                o += m
+            continue
         src = split[l] if kind == "q" else dh2.s[l] if kind == "s" else dh2.leaf_a
         arena_t[base:base + size].copy_(src[:size])
     torch.cuda.synchronize(dev)
@@ -499,8 +515,14 @@ def to_pinned_host(h2):
             r, o = n - k, b0 + int(lay.qoff[i])
             c = h2._choice[(l, i)]
             fr = fr_all[lq.foff[i]:lq.foff[i] + k * k].reshape(k, k)
-            bd = _TrackedBasis(q_skel=arena[o + n * r:o + n * n].reshape(n, k),
-                               q_red=arena[o:o + n * r].reshape(n, r), rank=k, frame=fr,
+            qs, qr = arena[o + n * r:o + n * n].reshape(n, k), arena[o:o + n * r].reshape(n, r)
+            if l in dh2.wy:
+                # the device rebuilds this level's q_full from the arena's Y / Yt: in-place edits
+                # of these views could not reach it, so they are read-only (rebinding still works
+                # and sends factorize back to the full upload)
+                qs.flags.writeable = False
+                qr.flags.writeable = False
+            bd = _TrackedBasis(q_skel=qs, q_red=qr, rank=k, frame=fr,
                                skeleton=c.skeleton if c is not None else np.zeros(0, dtype=np.int64))
             object.__setattr__(bd, "_flag", flag)
             dict.__setitem__(bases, (l, i), bd)
@@ -517,6 +539,7 @@ def to_pinned_host(h2):
     out.bases, out.near_blocks, out.couplings = bases, near, cpl
     out._arena = PinnedArena(arena_t, dh2.signature(),
                              {"bases": bases, "near_blocks": near, "couplings": cpl}, flag)
+    out._arena.wy_levels = tuple(sorted(dh2.wy))
     return out
 
 
@@ -572,6 +595,7 @@ class PinnedArena:
     of a block's values write through to the buffer, so they stay intact."""
 
     def __init__(self, tensor, signature, containers, flag):
+        self.wy_levels = ()               # levels shipped in compact-WY form (to_pinned_host)
         self.tensor = tensor
         self.signature = signature
         self.containers = containers      # attribute name -> _TrackedDict handed out

@@ -152,6 +152,7 @@ class DeviceH2:
         self.leaf_a = leaf_a    # tensor (depth >= 1)
         self.aoff = aoff        # (i, j) -> offset in leaf_a
         self.root_a = root_a    # tensor d x d (depth == 0)
+        self.wy = {}            # l -> compact-WY form of the level's bases (LevelQR / basis_qr.WYLevel)
 
     # -------------------------------------------------------------------------------
     @staticmethod
@@ -169,7 +170,10 @@ class DeviceH2:
         """Structure key: equal signatures -> identical layouts and programs."""
         sig = self.__dict__.get("_sig")
         if sig is None:
-            sig = self._sig = _signature(self.depth, self.count, self.levels)
+            sig = _signature(self.depth, self.count, self.levels)
+            if self.wy:   # compact-WY levels change the staging layout and the program
+                sig += ":wy" + ",".join(str(l) for l in sorted(self.wy))
+            self._sig = sig
         return sig
 
     @classmethod
@@ -189,6 +193,22 @@ class DeviceH2:
         leaf_a = torch.empty(max(asize, 1), dtype=F64, device=device)
         out = cls(device, depth, h2.count, levels, q, s, leaf_a, aoff)
         out._qsplit, out._qprog = _q_interleave(levels, q, device)
+        # a to_pinned_host matrix whose levels carry the compact-WY form: those levels upload
+        # Y, Yt and the signs instead of q_full, and q_full is rebuilt on the device
+        arena = getattr(h2, "_arena", None)
+        if arena is not None and getattr(arena, "wy_levels", ()) and arena.intact(h2):
+            from .basis_qr import WYLevel, rebuild_qfull, wy_operands
+            from .program import Program
+
+            out._wyprog = {}
+            for l in arena.wy_levels:
+                lay = levels[l]
+                wyl = WYLevel(device, lay.n, lay.k)
+                out.wy[l] = wyl
+                pg = Program(device)
+                rebuild_qfull(wyl, pg, lambda i, l=l, lay=lay: q[l].data_ptr() + 8 * int(lay.qoff[i]))
+                wy_operands(wyl, pg)
+                out._wyprog[l] = pg.finalize()
         return out
 
     @classmethod
@@ -242,6 +262,21 @@ class DeviceH2:
             # one DMA per region back to back, no host gather
             with torch.cuda.stream(st):
                 for kind, l, base, size in regions:
+                    if kind == "w":
+                        # compact-WY level: Y, Yt, signs; q_full is rebuilt from them (its q
+                        # region stays in the arena for the numpy views but is not copied)
+                        wyl = into.wy[l]
+                        o = base
+                        for t, m in zip((wyl.V, wyl.wy_vt, wyl.wy_sgn), wyl.sizes()):
+                            t[:m].copy_(arena.tensor[o:o + m], non_blocking=True)
+                            o += m
+                        ev = torch.cuda.Event()
+                        ev.record(st)
+                        fix.wait_event(ev)
+                        into._wyprog[l].run(fix)
+                        continue
+                    if kind == "q" and l in into.wy:
+                        continue
                     dst = qsplit[l] if kind == "q" else s[l] if kind == "s" else leaf_a
                     dst[:size].copy_(arena.tensor[base:base + size], non_blocking=True)
                     if kind == "q":
@@ -252,6 +287,8 @@ class DeviceH2:
             if stream is None:
                 st.synchronize()
             return into
+        if into.wy:
+            raise RuntimeError("a compact-WY device layout uploads only from its intact pinned arena")
         prev = _STAGING.get("done")
         if prev is not None:
             prev.synchronize()                 # the staging buffer is still being read by the last upload
@@ -303,11 +340,16 @@ class DeviceH2:
 
     def staging_regions(self):
         """[(kind, level, offset, size)] of the host staging layout, leaves first:
-        [q_L][s_L][a][q_L-1][s_L-1] ... [q_1][s_1] (q: q_red then q_skel per box)."""
+        [q_L][s_L][a][q_L-1][s_L-1] ... [q_1][s_1] (q: q_red then q_skel per box);
+        a compact-WY level puts [Y | Yt | signs] ("w") before its q region."""
         regions, off = [], 0
         asize = int(self.leaf_a.numel())
         for l in range(self.depth, 0, -1):
             lay = self.levels[l]
+            if l in self.wy:   # [Y | Yt | signs] of a compact-WY level, first
+                nk, k = int((lay.n * lay.k).sum()), int(lay.k.sum())
+                regions.append(("w", l, off, 2 * nk + k))
+                off += 2 * nk + k
             regions.append(("q", l, off, lay.qsize))
             off += lay.qsize
             regions.append(("s", l, off, max(lay.ssize, 1)))

@@ -1076,7 +1076,9 @@ def _cached_plan(h2):
     levels = DeviceH2.layouts_from_host(h2)
     from .h2_device import _signature
 
-    key = ("host", _signature(h2.tree.depth, h2.count, levels))
+    arena = getattr(h2, "_arena", None)
+    wy = tuple(getattr(arena, "wy_levels", ())) if arena is not None and arena.intact(h2) else ()
+    key = ("host", _signature(h2.tree.depth, h2.count, levels), wy)
     ent = _PLAN_CACHE.get(key)
     if ent is not None and (ent[2] is None or ent[2]() is None):
         dh2 = DeviceH2.from_host(h2, into=ent[0])

@@ -154,18 +154,22 @@ def test_pinned_host_arena_tracks_rebinds(pkg):
     key = next(iter(host.near_blocks))
     host.near_blocks[key][0, 0] += 0.0                      # in place: still the arena
     assert host._arena.intact(host)
+    # the gather path uploads q_full and runs the dense transform: the same bits unless a
+    # level took the compact-WY transform (then equal to rounding)
+    same = (lambda x: np.array_equal(x, x0)) if not h2._device.wy else \
+        (lambda x: np.linalg.norm(x - x0) <= 1e-11 * np.linalg.norm(x0))
     host.near_blocks[key] = host.near_blocks[key].copy()     # rebound entry
     assert not host._arena.intact(host)
-    assert np.array_equal(pkg.solve(pkg.factorize(host), b), x0)
+    assert same(pkg.solve(pkg.factorize(host), b))
     host2 = to_pinned_host(h2)
     bd = next(iter(host2.bases.values()))
     bd.q_red = bd.q_red.copy()                               # rebound basis factor
     assert not host2._arena.intact(host2)
-    assert np.array_equal(pkg.solve(pkg.factorize(host2), b), x0)
+    assert same(pkg.solve(pkg.factorize(host2), b))
     host3 = to_pinned_host(h2)
     host3.couplings = dict(host3.couplings)                  # replaced container
     assert not host3._arena.intact(host3)
-    assert np.array_equal(pkg.solve(pkg.factorize(host3), b), x0)
+    assert same(pkg.solve(pkg.factorize(host3), b))
 
 
 def test_c2_full_size_flops_and_residual(pkg):
@@ -240,3 +244,47 @@ def test_compact_wy_transform_equals_dense(pkg, shape, n, leaf, family, shift):
     assert np.linalg.norm(x_wy - x_dense) <= 1e-11 * np.linalg.norm(x_dense)
     xo = orc.solve(orc.factorize(h2), b)
     assert np.linalg.norm(x_wy - xo) / np.linalg.norm(xo) < 1e-9
+
+
+def test_pinned_host_compact_wy_upload(pkg):
+    """to_pinned_host of an H2 whose leaf bases carry the compact-WY form ships Y, Yt and
+    the signs instead of q_full and rebuilds q_full on the device (the construct forms q_full
+    by the same product, so the bits agree): same q_full, same factors / solution as the
+    device-resident H2; the WY levels' q views are read-only; a rebound basis falls back
+    to the full upload and the dense transform (equal to rounding)."""
+    from paper_2502_02395_b200 import basis_qr
+    from paper_2502_02395_b200.h2_build import to_pinned_host
+    from paper_2502_02395_b200.h2_device import DeviceH2
+
+    h2 = _build(pkg, "sphere", 16384, 256, "yukawa", 1e5, tol=1e-8, s_far=256, s_near=256)
+    dh2 = h2._device
+    if not dh2.wy:   # keep the test meaningful whatever the gate decides for this geometry
+        pytest.skip("no compact-WY level at this configuration")
+    b = np.random.default_rng(3).standard_normal(h2.count)
+    x0 = pkg.solve(pkg.factorize(h2), b)
+    host = to_pinned_host(h2)
+    assert host._arena.wy_levels == tuple(sorted(dh2.wy))
+    l = max(dh2.wy)
+    bd = host.bases[(l, 0)]
+    with pytest.raises(ValueError):
+        bd.q_red[0, 0] = 1.0
+    up = DeviceH2.from_host(host)
+    assert set(up.wy) == set(dh2.wy)
+    for lv in dh2.wy:
+        assert torch_equal(up.q[lv], dh2.q[lv])
+    assert np.array_equal(pkg.solve(pkg.factorize(host), b), x0)
+    host.bases[(l, 0)] = basis_qr_copy(bd)          # rebound: full upload, dense transform
+    assert not host._arena.intact(host)
+    x1 = pkg.solve(pkg.factorize(host), b)
+    assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a[:b.numel()], b[:a.numel()]))
+
+
+def basis_qr_copy(bd):
+    from paper_2502_02395_b200.dense_core import BasisDecomposition
+    return BasisDecomposition(q_skel=bd.q_skel.copy(), q_red=bd.q_red.copy(), rank=bd.rank, frame=bd.frame,
+                              skeleton=bd.skeleton)
