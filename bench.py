@@ -165,8 +165,18 @@ def host_copy(pkg, h2):
 
 
 def h2d_bytes(h2):
+    """Bytes one factorize(h2) copies host -> device: bases (q_red / q_skel, or for the
+    levels a pinned arena ships in compact-WY form Y, Yt and the signs), leaf near blocks,
+    couplings."""
     depth = h2.tree.depth
-    nb = sum(b.q_red.nbytes + b.q_skel.nbytes for b in h2.bases.values())
+    arena = getattr(h2, "_arena", None)
+    wy = set(arena.wy_levels) if arena is not None and arena.intact(h2) else set()
+    nb = 0
+    for (l, i), b in h2.bases.items():
+        if l in wy:
+            nb += 8 * (2 * b.q_skel.shape[0] * b.rank + b.rank)
+        else:
+            nb += b.q_red.nbytes + b.q_skel.nbytes
     nb += sum(v.nbytes for k, v in h2.near_blocks.items() if k[0] == depth)
     nb += sum(v.nbytes for v in h2.couplings.values())
     return nb
@@ -545,17 +555,20 @@ def main():
                          "forward + backward CUDA graphs replayed back to back, CUDA events"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        smp = OracleSampler(host_copy(pkg, h2))
+    # the CPU baseline runs AFTER the e2e leg (its BLAS threads and multi-GB host copies would
+    # otherwise still compete for the host while the e2e upload runs); its input is copied now
+    smp = OracleSampler(host_copy(pkg, h2)) if rank == 0 and world == 1 and not args.no_cpu_baseline else None
+
+    def cpu_baseline():
         best = None
         for th in thread_candidates():   # same candidates as --impl reference
             dt, fl = smp.run(0, th)
             if best is None or fl / dt > best[1] / best[0]:
                 best = (dt, fl, th)
         dt, fl, th = best
-        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": th, "kind": "port",
-               "sample": smp.describe(args.config) + f" (box 0 here); oracle/h2ulv_oracle.py, fastest of "
-                         f"{thread_candidates()} BLAS threads: {th} threads, {dt:.2f} s for {fl:.3e} flops"}
+        return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": th, "kind": "port",
+                "sample": smp.describe(args.config) + f" (box 0 here); oracle/h2ulv_oracle.py, fastest of "
+                          f"{thread_candidates()} BLAS threads: {th} threads, {dt:.2f} s for {fl:.3e} flops"}
 
     # ---- e2e through the public API with host buffers (the H² blocks in pinned host memory)
     from paper_2502_02395_b200.h2_build import to_pinned_host
@@ -598,9 +611,15 @@ def main():
            "includes": "factorize(h2): the reference's numpy H2Matrix data model, its blocks in one pinned host "
                        "buffer (to_pinned_host); H2D of bases / leaf near blocks / couplings level by level on a "
                        "copy stream, each level's factorization graph queued behind its level's copies (upload "
-                       "and factorization overlap), pivot-status D2H; solve(b): H2D b, forward/backward graphs, "
-                       "D2H x. The symbolic part (layout, descriptors, CUDA graphs) is cached per structure, the "
-                       "numeric upload is redone every step"}
+                       "and factorization overlap); bases of compact-WY levels travel as their Householder form "
+                       "(Y, Yt, signs) and q_full is rebuilt on the device; pivot-status D2H; solve(b): H2D b, "
+                       "the per-factorization solve prepare, forward/backward graphs, D2H x. The symbolic part "
+                       "(layout, descriptors, CUDA graphs) is cached per structure, the numeric upload is redone "
+                       "every step"}
+
+    if smp is not None:
+        cpu = cpu_baseline()
+        smp = None
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,

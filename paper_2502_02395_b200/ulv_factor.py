@@ -57,8 +57,10 @@ CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
 CHOL_BOX_MAX_N = int(os.environ.get("H2G_CHOL_BOX_MAX_N", "512"))
 CHOL_BOX_V = os.environ.get("H2G_CHOL_BOX_V", "0") == "1"
 WY_TRANSFORM = os.environ.get("H2G_WY", "1") != "0"   # compact-WY diag transform where the bases carry it
-# tile configs of the WY launches (A/B knobs; "" = the planner's choice): W = A Vt, X, U, the relabelled update
-_WY_CFG = [int(c) if c else None for c in os.environ.get("H2G_WY_CFG", ",,,7").split(",")]
+def _wy_cfg():
+    """Tile configs of the WY launches (A/B knob, read when a plan is built; "" = the
+    planner's choice): W = A Yt, X, U, the relabelled update."""
+    return [int(c) if c else None for c in os.environ.get("H2G_WY_CFG", ",,,7").split(",")]
 PANEL_ROWS_PER_CTA = 128
 
 
@@ -555,6 +557,7 @@ class FactorPlan:
         A = {i: ap + 8 * a_off[(i, i)] for i in boxes}
         ni = {i: int(n[i]) for i in boxes}
         ki = {i: int(k[i]) for i in boxes}
+        _WY_CFG = _wy_cfg()
         prog.gemm(0, 0, [(A[i], Vt[i], P[i], ni[i], ki[i], ni[i], ni[i], ki[i], 2 * ki[i], 0, 1.0, 0.0)
                          for i in boxes], tile_cfg=_WY_CFG[0])                              # W = A Vt
         prog.gemm(1, 0, [(Vt[i], P[i], X[i], ki[i], ki[i], ni[i], ki[i], 2 * ki[i], ki[i], 0, 1.0, 0.0)
