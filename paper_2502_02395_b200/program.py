@@ -87,6 +87,36 @@ def choose_split(tiles, ks, sms=148, per_sm=4):
     return best
 
 
+_CARVE = os.environ.get("H2G_GEMM_CARVE", "1") != "0"
+
+
+def carve_edges(p, trans_a, trans_b):
+    """(interior, [edge strips]) of a plain (non-LOWER, no ext) problem whose M or N ends
+    in a remainder of 1..32 past a multiple of 64: the interior keeps the 64x64 tiles, the
+    bottom / right strips go to the 32x32-tile launch (sub-problems are pointer offsets of
+    the same operands, disjoint parts of C).  None when nothing is carved."""
+    A, B, C, M, N, K, lda, ldb, ldc, flags, alpha, beta = p[:12]
+    if len(p) > 12 or flags & nat.GEMM_LOWER or M < 64 or N < 64:
+        return None
+    rm, rn = M % 64, N % 64
+    mi = M - rm if 0 < rm <= 32 else M
+    ni = N - rn if 0 < rn <= 32 else N
+    if mi == M and ni == N:
+        return None
+
+    def sub(m0, n0, m, n):
+        a = A + 8 * (m0 if trans_a else m0 * lda)
+        b = B + 8 * (n0 * ldb if trans_b else n0)
+        return (a, b, C + 8 * (m0 * ldc + n0), m, n, K, lda, ldb, ldc, flags, alpha, beta)
+
+    edges = []
+    if mi < M:
+        edges.append(sub(mi, 0, M - mi, N))
+    if ni < N:
+        edges.append(sub(0, ni, mi, N - ni))
+    return sub(0, 0, mi, ni), edges
+
+
 def split_by_tile(problems):
     """(problems for 64x64 tiles, problems for 32x32 tiles): a problem goes to the 32x32
     launch when its 64x64 tiles would execute more than _SPLIT_RATIO x the 32x32 tiles'
@@ -187,6 +217,16 @@ class Program:
             return 0
         if tile_cfg is None and _SPLIT_RATIO > 0 and len(rows) > 1:
             big, small = split_by_tile(rows)
+            if big and _CARVE:
+                carved = []
+                for p in big:
+                    c = carve_edges(p, trans_a, trans_b)
+                    if c is None:
+                        carved.append(p)
+                    else:
+                        carved.append(c[0])
+                        small.extend(c[1])
+                big = carved
             if big and small:
                 return (self.gemm(trans_a, trans_b, big, split=split)
                         + self.gemm(trans_a, trans_b, small, tile_cfg=9))

@@ -939,21 +939,32 @@ def audit_writes(regions, writes):
     regions = sorted(regions)
     starts = [g[0] for g in regions]
     hits = {}                                   # (region index, slab) -> list of roles
+    pieces = {}                                 # (region index, slab) -> transform rectangles
 
-    def hit(g, slab, role):
+    def hit(g, slab, role, box=None):
         hits.setdefault((g, slab), []).append(role)
+        if role == "transform" and box is not None:
+            pieces.setdefault((g, slab), []).append(box)
 
     def rect(g, r0, c0, rows, cols, role):
         _, nr, nc, rs, cs, _ = regions[g]
         r1, c1 = min(r0 + rows, nr), min(c0 + cols, nc)
         if r0 < rs and c0 < cs:
-            hit(g, "rr", role)
+            hit(g, "rr", role, (r0, c0, min(r1, rs), min(c1, cs)))
         if r0 < rs and c1 > cs:
-            hit(g, "rs", role)
+            hit(g, "rs", role, (r0, max(c0, cs), min(r1, rs), c1))
         if r1 > rs and c0 < cs:
-            hit(g, "sr", role)
+            hit(g, "sr", role, (max(r0, rs), c0, r1, min(c1, cs)))
         if r1 > rs and c1 > cs:
-            hit(g, "ss", role)
+            hit(g, "ss", role, (max(r0, rs), max(c0, cs), r1, c1))
+
+    def overlapping(boxes):
+        for a in range(len(boxes)):
+            for b in range(a + 1, len(boxes)):
+                p, q = boxes[a], boxes[b]
+                if p[0] < q[2] and q[0] < p[2] and p[1] < q[3] and q[1] < p[3]:
+                    return True
+        return False
 
     for (_, role, ptr, rows, cols, ld, lower) in writes:
         if rows <= 0 or cols <= 0:
@@ -987,6 +998,8 @@ def audit_writes(regions, writes):
         for slab in ("rr", "rs", "sr", "ss", "mismatched_ld"):
             roles = hits.get((g, slab), [])
             init = sum(1 for x in roles if x == "transform")
+            if init > 1 and not overlapping(pieces.get((g, slab), [])):
+                init = 1       # one transform stored in disjoint pieces (edge-carved GEMM launches)
             post = [x for x in roles if x != "transform"]
             area = {"rr": rs * cs, "rs": rs * (nc - cs), "sr": (nr - rs) * cs, "ss": (nr - rs) * (nc - cs)}.get(slab, 1)
             if slab == "mismatched_ld":

@@ -48,3 +48,16 @@ def test_vacuous_schur_of_full_rank_box_counts_once():
     regions = [(H0, 8, 8, 0, 0, ("diag", 1, 0, 0))]                  # r = 0: nothing to eliminate
     a = audit_writes(regions, [(0, "transform", H0, 8, 8, 8, True)])
     assert a["diag_ss_update_counts"] == [1]
+
+
+def test_edge_carved_transform_counts_once():
+    """A transform stored by disjoint pieces (Program.gemm carves the ragged edge strips
+    of a plain problem into the 32x32-tile launch) initializes each slab once; pieces
+    that overlap are still an initialization twice."""
+    w = [x for x in good_program() if x[0] != 5]
+    carved = w + [(5, "transform", T, 4, 5, 8, False),                    # rows 0..3 of T[:, :r_j]
+                  (9, "transform", T + 8 * (4 * 8), 4, 5, 8, False)]      # rows 4..7: the edge strip
+    a = audit_writes(REGIONS, carved)
+    assert a["initialized_twice"] == 0 and a["uninitialized_slabs"] == 0
+    overlap = w + [(5, "transform", T, 5, 5, 8, False), (9, "transform", T + 8 * (4 * 8), 4, 5, 8, False)]
+    assert audit_writes(REGIONS, overlap)["initialized_twice"] == 1
