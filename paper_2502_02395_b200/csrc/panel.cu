@@ -137,21 +137,28 @@ __device__ __forceinline__ void tile8_nt16(double (&c)[2], const double* A, cons
 }
 
 // NW warps (4 or 8).  D, Li: 64 x SD smem; pv: 64 doubles smem.
+// b < 64 (a partial last panel): rows / cols >= b hold the identity, so the 16x16 blocks
+// past ceil(b/16) are skipped — they would factor to the identity with zero coupling
+// (their Li diagonal blocks are set to I, the off-diagonal blocks stay 0).
 template <int NW>
-__device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs) {
+__device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs, int b = PB) {
   constexpr int NU = (16 + NW - 1) / NW;   // 8x8 output tiles per warp (<= 12 / 16 tiles per phase)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  for (int t = tid; t < PB * PB; t += blockDim.x) Li[(t / PB) * SD + t % PB] = 0.0;
+  const int nb = b >= PB ? PB / DB : max(1, (b + DB - 1) / DB);   // 16x16 blocks with real pivots
+  for (int t = tid; t < PB * PB; t += blockDim.x) {
+    const int i = t / PB, x = t % PB;
+    Li[i * SD + x] = (i == x && i >= nb * DB) ? 1.0 : 0.0;
+  }
   __syncthreads();
   PTRACE(16);
 #pragma unroll 1
-  for (int kb = 0; kb < PB / DB; ++kb) {
+  for (int kb = 0; kb < nb; ++kb) {
     const int c = kb * DB;
     if (warp == 0) chol16_warp(D + c * SD + c, Li + c * SD + c, pv + c, cs);
     __syncthreads();
     PTRACE(17 + 2 * kb);
-    const int R = PB - c - DB;                 // rows below the block
+    const int R = nb * DB - c - DB;            // rows below the block (padding rows stay the identity)
     if (R == 0) break;
     // TRSM: X = D[c+16:, c:c+16] <- X Linv_kk^T; 8x8 output tiles (R/8) x 2
     const int nt = (R / 8) * 2;
@@ -194,8 +201,8 @@ __device__ void diag_blocked(double* D, double* Li, double* pv, Chol16Shared& cs
   // off-diagonal 16x16 blocks of L^-1, by block diagonals dd = 1..3:
   //   Linv_IJ = -Linv_II * (sum_{K=J}^{I-1} L_IK Linv_KJ),  I = J + dd
 #pragma unroll 1
-  for (int dd = 1; dd < PB / DB; ++dd) {
-    const int nblk = PB / DB - dd;             // blocks on this block diagonal
+  for (int dd = 1; dd < nb; ++dd) {
+    const int nblk = nb - dd;                  // blocks on this block diagonal
     // phase 1: W_J = sum_K L_IK Linv_KJ (16x16 each, 4 8x8 tiles) -> registers, then smem scratch
     double w[NU][2];
     int tt[NU];
@@ -361,7 +368,7 @@ __device__ __forceinline__ void chol_diag_body(const h2g_chol_panel_desc& P, dou
     for (int x = 0; x < PB; ++x) S[r * SD + x] = (x == r) ? 1.0 : 0.0;
   }
   __syncthreads();
-  diag_blocked<NW>(S, Li, sh.pv, sh.cs);
+  diag_blocked<NW>(S, Li, sh.pv, sh.cs, b);
   if (tid < 32) record_npd(sh, b, p, npd, P.npd_slot);
   for (int t = tid; t < PB * PB; t += NT) {
     const int i = t / PB, x = t % PB;
@@ -840,7 +847,7 @@ __global__ void __launch_bounds__(RW_THREADS, 3) chol_box_kernel(const h2g_cholb
     }
     __syncthreads();
     double* pv = R0 + CB_PV;
-    diag_blocked<8>(R0, R1, pv, *reinterpret_cast<Chol16Shared*>(R0 + CB_CS));
+    diag_blocked<8>(R0, R1, pv, *reinterpret_cast<Chol16Shared*>(R0 + CB_CS), b);
     if (warp == 0) {
       const unsigned lo = __ballot_sync(0xffffffffu, lane < b && !(pv[lane] > 0.0));
       const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < b && !(pv[lane + 32] > 0.0));
