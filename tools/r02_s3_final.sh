@@ -13,5 +13,4 @@ tail -3 gpurun_out/${T}_pytest.log
 NCU="ncu --clock-control none --profile-from-start off"
 timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file gpurun_out/${T}_launches_m1.csv python tools/profile_factor.py m1 1 > gpurun_out/${T}_pf.log 2>&1
 python tools/launch_summary.py gpurun_out/${T}_launches_m1.csv > gpurun_out/${T}_launches_m1.txt 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/${T}_launches_bench.csv python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-exact-residual > gpurun_out/${T}_ncu_bench.log 2>&1
-python tools/launch_summary.py gpurun_out/${T}_launches_bench.csv > gpurun_out/${T}_launches_bench.txt 2>&1
+timeout 900 python tools/ablate_once.py m1 > gpurun_out/${T}_ablate.txt 2>&1
