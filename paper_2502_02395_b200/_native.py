@@ -65,7 +65,7 @@ STEP = {"GEMM_NN": 0, "GEMM_NT": 1, "GEMM_TN": 2, "GEMM_TT": 3, "COPY": 5, "MEMC
 GEMM_LOWER = 1
 GEMV_PLUS = 1
 GEMV_SPLIT = 2
-GEMM_TILE = {2: 64, 7: 64, 9: 32}  # tile edge per tile_cfg (gemm.cu: Cfg64b, Cfg64m3, Cfg32)
+GEMM_TILE = {2: 64, 7: 64, 9: 32, 11: 64}  # tile edge per tile_cfg (gemm.cu: Cfg64b, Cfg64m3, Cfg32, Cfg64w8)
 COPY_TILE = 64
 PANEL_WIDTH = 64
 GEMV_CHUNK = 64    # output rows per CTA of h2g_gemv_grouped (csrc/solve.cu GV_CHUNK)

@@ -42,6 +42,7 @@ struct GemmCfg {
 using Cfg64b = GemmCfg<64, 64, 2, 2, 4, H2G_GEMM_STAGES>;   // cfg 2: 4 CTAs/SM, <= 128 registers (transforms)
 using Cfg64m3 = GemmCfg<64, 64, 2, 2, 3, 2>;    // cfg 7: 3 CTAs/SM (170 registers), 2 stages (K <= 64 updates)
 using Cfg32 = GemmCfg<32, 32, 2, 2, 6, 2>;      // cfg 9: small / ragged problems, 32x32 tiles, 6 CTAs/SM
+using Cfg64w8 = GemmCfg<64, 64, 2, 4, 3, 2>;    // cfg 11: 8 warps (32x16 warp tiles), EXT launches only (A/B)
 
 // EXT: per-problem extension (h2g_gemm_ext): the beta term read from a separate Cin and, with
 // remap_k >= 0, the compact-WY relabel epilogue of the diag transform (see h2g_gemm_grouped_ext).
@@ -451,12 +452,13 @@ extern "C" int h2g_gemm_grouped_ext(int trans_a, int trans_b, int tile_cfg, cons
   if (tile_cfg == 2) return h2g::dispatch_ext<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
   if (tile_cfg == 7) return h2g::dispatch_ext<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
   if (tile_cfg == 9) return h2g::dispatch_ext<h2g::Cfg32>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
-  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: unknown tile config %d (2, 7, 9)", tile_cfg);
+  if (tile_cfg == 11) return h2g::dispatch_ext<h2g::Cfg64w8>(trans_a, trans_b, d_probs, d_ext, d_tile_map, total_tiles, s);
+  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped_ext: unknown tile config %d (2, 7, 9, 11)", tile_cfg);
 }
 
 extern "C" int h2g_gemm_tiles(int M, int N, int flags, int tile_cfg) {
   if (M <= 0 || N <= 0) return 0;
-  const int T = tile_cfg == 9 ? 32 : 64;   // cfg 9: 32x32 tiles, cfg 2 / 7: 64x64
+  const int T = tile_cfg == 9 ? 32 : 64;   // cfg 9: 32x32 tiles, cfg 2 / 7 / 11: 64x64
   if (flags & H2G_GEMM_LOWER) {
     int t = (M + T - 1) / T;
     return t * (t + 1) / 2;

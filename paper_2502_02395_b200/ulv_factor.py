@@ -60,7 +60,7 @@ WY_TRANSFORM = os.environ.get("H2G_WY", "1") != "0"   # compact-WY diag transfor
 def _wy_cfg():
     """Tile configs of the WY launches (A/B knob, read when a plan is built; "" = the
     planner's choice): W = A Yt, X, U, the relabelled update."""
-    return [int(c) if c else None for c in os.environ.get("H2G_WY_CFG", ",,,7").split(",")]
+    return [int(c) if c else None for c in os.environ.get("H2G_WY_CFG", ",,,11").split(",")]
 PANEL_ROWS_PER_CTA = 128
 
 
