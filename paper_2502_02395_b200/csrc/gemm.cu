@@ -474,5 +474,6 @@ extern "C" int h2g_gemm_grouped(int trans_a, int trans_b, int tile_cfg, const h2
   if (tile_cfg == 2) return h2g::dispatch<h2g::Cfg64b>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 7) return h2g::dispatch<h2g::Cfg64m3>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
   if (tile_cfg == 9) return h2g::dispatch<h2g::Cfg32>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
-  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d (2, 7, 9)", tile_cfg);
+  if (tile_cfg == 11) return h2g::dispatch<h2g::Cfg64w8>(trans_a, trans_b, d_probs, d_tile_map, total_tiles, s);
+  return h2g_set_error(H2G_EINVAL, "h2g_gemm_grouped: unknown tile config %d (2, 7, 9, 11)", tile_cfg);
 }

@@ -88,6 +88,7 @@ def choose_split(tiles, ks, sms=148, per_sm=4):
 
 
 _CARVE = os.environ.get("H2G_GEMM_CARVE", "1") != "0"
+_BIG_CFG = int(os.environ.get("H2G_BIG_CFG", "2"))   # tile config of the large plain launches (A/B: 2 or 11)
 
 
 def carve_edges(p, trans_a, trans_b):
@@ -244,6 +245,8 @@ class Program:
             aux = ("blob", self._blob(ext))
         cfg = (choose_tile_cfg(arr["M"], arr["N"], arr["flags"], trans_b=bool(trans_b), ks=arr["K"])
                if tile_cfg is None else tile_cfg)
+        if tile_cfg is None and cfg == 2 and _BIG_CFG != 2 and not (split and _SPLITK > 1):
+            cfg = _BIG_CFG
         tiles = np.array([gemm_tiles(m, n, f, cfg) for m, n, f in zip(arr["M"], arr["N"], arr["flags"])],
                          dtype=np.int64)
         nsplit = choose_split(int(tiles.sum()), arr["K"], self.sms) if (split and cfg == 2 and not aux) else 1

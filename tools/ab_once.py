@@ -33,6 +33,7 @@ for rep in range(2):
         pm._SPLIT_RATIO = float(os.environ.get("H2G_GEMM_SPLIT", "1.5"))
         pm._SPLITK = int(os.environ.get("H2G_SPLITK", "1"))
         pm._CARVE = os.environ.get("H2G_GEMM_CARVE", "1") != "0"
+        pm._BIG_CFG = int(os.environ.get("H2G_BIG_CFG", "2"))
         from paper_2502_02395_b200 import ulv_factor as uf
         uf.CHOL_BOX_MIN = int(os.environ.get("H2G_CHOL_BOX_MIN", "4096"))
         plan = FactorPlan(h2._device, lists)
