@@ -482,6 +482,10 @@ def main():
                 "peak_source": "measured FP64 DMMA issue peak (profiles/r01_fp64_peak.txt); "
                                "cuBLAS DGEMM 8192^3 = 35.5 TFLOP/s",
                 "gemm_share_of_step": g_ms / eager_ms if eager_ms else None,
+                "note": ("achieved = useful flops of ALL grouped-GEMM launches / their CUDA-event time. Levels "
+                         "whose bases carry the compact-WY form (the N = 1M leaf) replace the 3n^3 of Q^T (A Q) "
+                         "by thin K <= 2k GEMMs (4n^2k + 4nk^2 flops): fewer flops at a lower DMMA rate, so this "
+                         "fraction is lower than with the dense transform while the step is faster"),
                 "per_kind": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
                                  "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["flops"] and v["ms"] else None,
                                  "gbs": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["bytes"] and v["ms"] else None}
