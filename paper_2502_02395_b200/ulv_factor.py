@@ -685,23 +685,34 @@ class FactorPlan:
 
         run_segments(self, stream)
 
-    def launch_streamed(self):
+    def launch_streamed(self, post=None):
         """Incremental launcher for a plan built with level_cuts: returns
         (on_level, finish).  on_level(l, event) — called by DeviceH2.from_host
         when level l's operands are on their way — queues every segment up to
         and including level l's after a wait on `event`; finish() queues the
-        rest (the root)."""
+        rest (the root).  post(l), when given, is called right after level l's
+        segment is queued (its factor blocks are final once it ran); post(0)
+        after the root."""
         stream = torch.cuda.current_stream(self.device)
         segs = self.segments
-        state = {"i": 0}
+        state = {"i": 0, "level": None}
+
+        def launched(seg):
+            seg.launch(stream)
+            if post is not None and state["level"] is not None:
+                post(state["level"])
+                if state["level"] == 1:
+                    post(0)
+                state["level"] = None
 
         def on_level(level, event):
             waited = False
             while state["i"] < len(segs):
                 seg = segs[state["i"]]
                 if isinstance(seg, Program):
-                    seg.launch(stream)
+                    launched(seg)
                 elif seg[0] == "upload" and seg[1] == level and not waited:
+                    state["level"] = level
                     stream.wait_event(event)
                     waited = True
                 elif seg[0] == "upload":
@@ -715,7 +726,7 @@ class FactorPlan:
                 seg = segs[state["i"]]
                 if not isinstance(seg, Program):
                     raise RuntimeError(f"streamed launch: level {seg} was never uploaded")
-                seg.launch(stream)
+                launched(seg)
                 state["i"] += 1
 
         self.generation += 1
@@ -1143,11 +1154,40 @@ def _factorize_streamed(h2):
         plan = FactorPlan(dh2, h2.lists, level_cuts=True)
         plan.capture()
         _remember(key, dh2, plan)
-    torch.cuda.current_stream(dh2.device).wait_stream(_upload_stream(dh2.device))
-    on_level, finish = plan.launch_streamed()
+    cur = torch.cuda.current_stream(dh2.device)
+    cur.wait_stream(_upload_stream(dh2.device))
+    # a cached solve plan of this structure (w = 1, parallel: what solve(f, b) uses): its
+    # per-factorization prepare runs level by level right behind the factorization, on a side
+    # stream, hidden under the upload of the levels above
+    sp = plan.__dict__.get("_solve_plans", {}).get((1, "parallel"))
+    post = None
+    if sp is not None:
+        side = _prepare_stream(dh2.device)
+        side.wait_stream(cur)
+
+        def post(l):
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            side.wait_event(ev)
+            sp.prepare_level[l].launch(side)
+    on_level, finish = plan.launch_streamed(post)
     DeviceH2.from_host(h2, into=dh2, on_level=on_level, stream=_upload_stream(dh2.device))
     finish()
+    if sp is not None:
+        cur.wait_stream(side)
+        sp._prepared = plan.generation
     return dh2, plan
+
+
+_PREPARE_STREAM = {}
+
+
+def _prepare_stream(device):
+    st = _PREPARE_STREAM.get(device)
+    if st is None:
+        st = torch.cuda.Stream(device=device)
+        _PREPARE_STREAM[device] = st
+    return st
 
 
 @ranged("h2ulv.factorize")

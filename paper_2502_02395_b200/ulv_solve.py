@@ -121,86 +121,111 @@ class SolvePlan:
         by-products.  The solve is then a pure function of the factor blocks
         (lr_diag, lr_off, ls, v, root; ulv_factor.py:27-43) — like the
         reference's — so factors read back from storage solve to the same bits
-        (test_storage.py:90-98)."""
+        (test_storage.py:90-98).
+
+        One program with the levels on separate lanes (they are independent; the
+        root's latency-bound inverse chain alone on lane 0), plus the same steps
+        as one program per level (`prepare_level[l]`, l = 0 the root) that a
+        streamed factorization queues right behind each level (ulv_factor.
+        _factorize_streamed), hidden under the upload of the levels above."""
+        dev = self.device
+        self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        self.linv, self.loff, self.wt, self.mblk = {}, {}, {}, {}
+        prog = Program(dev)
+        levels = [0] + list(range(self.fp.depth, 0, -1))
+        for l in levels:
+            prog.lane = 0 if l == 0 else 1 + (self.fp.depth - l) % 4
+            self._emit_prepare(prog, l, alloc=True)
+        prog.lane = 0
+        self.prepare = prog.finalize()
+        self.prepare.capture()
+        self.prepare_level = {}
+        for l in levels:
+            pl = Program(dev)
+            self._emit_prepare(pl, l, alloc=False)
+            self.prepare_level[l] = pl.finalize()
+        self._prepared = None
+
+    def _emit_prepare(self, prog, l, alloc):
+        """The prepare steps of level l (l = 0: the root) into `prog`; `alloc` creates the
+        buffers they write, otherwise the ones a first call created are reused."""
         fp = self.fp
         dev = self.device
         W = nat.PANEL_WIDTH
-        prog = Program(dev)
-        self._tri_status = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
-        self.linv, self.loff, self.wt, self.mblk = {}, {}, {}, {}
-        # levels are independent: each level's steps on one lane (in order), the levels spread
-        # over lanes 1..4, the root's latency-bound inverse chain alone on lane 0
-        d = fp.root_dim
-        nb0 = -(-d // W)
-        self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
-        self.root_w = torch.zeros(max(d * d, 1), dtype=F64, device=dev)
-        rp = fp.root_buf.data_ptr()
-        prog.lane = 0
-        prog.triinv([(rp, self.root_linv.data_ptr(), d, d, 0)], self._tri_status.data_ptr())
-        prog.trsm_rows([(rp, 0, self.root_w.data_ptr(), self.root_linv.data_ptr(), d, d, 0, nb0, d, d)])
-        for l in range(fp.depth, 0, -1):
-            prog.lane = 1 + (fp.depth - l) % 4
-            B = fp.bufs[l]
-            lay = B.lay
-            nblk = -(-np.asarray(lay.r, dtype=np.int64) // W)
-            loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
-            mine = self._mine(l)
-            if self.fused[l]:
-                # no TRSV reads a fused level's inverses (both modes transform only): just the
-                # zero-diagonal check that raises SingularTriangularError
+        if l == 0:
+            d = fp.root_dim
+            nb0 = -(-d // W)
+            if alloc:
+                self.root_linv = torch.zeros(max(nb0, 1) * W * W, dtype=F64, device=dev)
+                self.root_w = torch.zeros(max(d * d, 1), dtype=F64, device=dev)
+            rp = fp.root_buf.data_ptr()
+            prog.triinv([(rp, self.root_linv.data_ptr(), d, d, 0)], self._tri_status.data_ptr())
+            prog.trsm_rows([(rp, 0, self.root_w.data_ptr(), self.root_linv.data_ptr(), d, d, 0, nb0, d, d)])
+            return
+        B = fp.bufs[l]
+        lay = B.lay
+        nblk = -(-np.asarray(lay.r, dtype=np.int64) // W)
+        loff = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
+        mine = self._mine(l)
+        lt = None
+        if self.fused[l]:
+            # no TRSV reads a fused level's inverses (both modes transform only): just the
+            # zero-diagonal check that raises SingularTriangularError
+            if alloc:
                 self.linv[l], self.loff[l] = None, loff
-                prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, int(lay.r[i]), int(lay.n[i]), 0)
-                             for i in range(lay.nb) if mine[i] and lay.r[i] > 0], self._tri_status.data_ptr())
-            else:
-                lt = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
-                self.linv[l], self.loff[l] = lt, loff
-                prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
-                              int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
-                            self._tri_status.data_ptr())
-            if self.winv[l]:
-                roff = np.concatenate([[0], np.cumsum(np.asarray(lay.r, dtype=np.int64) ** 2)[:-1]])
-                wt = torch.zeros(max(int((np.asarray(lay.r, dtype=np.int64) ** 2).sum()), 1), dtype=F64, device=dev)
-                self.wt[l] = (wt, roff)
-                prog.trsm_rows([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, wt.data_ptr() + 8 * int(roff[i]),
-                                 lt.data_ptr() + 8 * int(loff[i]) * W * W, int(lay.r[i]), int(lay.r[i]), 0,
-                                 int(nblk[i]), int(lay.n[i]), int(lay.r[i]))
-                                for i in range(lay.nb) if mine[i] and lay.r[i] > 0])
-                if not self.dist:
-                    # M_ij = L_ii^-1 L(r)_ij (i > j near): P2+P3 become y_i = z_i - sum_j M_ij z_j
-                    # and B2' x_R-terms t_i = y_i - sum_j M_ji^T y_j — one GEMV each, no TRSV
-                    pairs = [(i, j) for (i, j) in lay.off_pairs if lay.r[i] > 0 and lay.r[j] > 0]
+            prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, int(lay.r[i]), int(lay.n[i]), 0)
+                         for i in range(lay.nb) if mine[i] and lay.r[i] > 0], self._tri_status.data_ptr())
+        else:
+            if alloc:
+                self.linv[l] = torch.zeros(max(int(nblk.sum()), 1) * W * W, dtype=F64, device=dev)
+                self.loff[l] = loff
+            lt = self.linv[l]
+            prog.triinv([(B.H.data_ptr() + 8 * int(lay.qoff[i]), lt.data_ptr() + 8 * int(loff[i]) * W * W,
+                          int(lay.r[i]), int(lay.n[i]), 0) for i in range(lay.nb) if mine[i] and lay.r[i] > 0],
+                        self._tri_status.data_ptr())
+        if self.winv[l]:
+            roff = np.concatenate([[0], np.cumsum(np.asarray(lay.r, dtype=np.int64) ** 2)[:-1]])
+            if alloc:
+                wt_ = torch.zeros(max(int((np.asarray(lay.r, dtype=np.int64) ** 2).sum()), 1), dtype=F64, device=dev)
+                self.wt[l] = (wt_, roff)
+            wt = self.wt[l][0]
+            prog.trsm_rows([(B.H.data_ptr() + 8 * int(lay.qoff[i]), 0, wt.data_ptr() + 8 * int(roff[i]),
+                             lt.data_ptr() + 8 * int(loff[i]) * W * W, int(lay.r[i]), int(lay.r[i]), 0,
+                             int(nblk[i]), int(lay.n[i]), int(lay.r[i]))
+                            for i in range(lay.nb) if mine[i] and lay.r[i] > 0])
+            if not self.dist:
+                # M_ij = L_ii^-1 L(r)_ij (i > j near): P2+P3 become y_i = z_i - sum_j M_ij z_j
+                # and B2' x_R-terms t_i = y_i - sum_j M_ji^T y_j — one GEMV each, no TRSV
+                pairs = [(i, j) for (i, j) in lay.off_pairs if lay.r[i] > 0 and lay.r[j] > 0]
+                if alloc:
                     moff, acc = {}, 0
                     for (i, j) in pairs:
                         moff[(i, j)] = acc
                         acc += int(lay.r[i]) * int(lay.r[j])
-                    mt = torch.zeros(max(acc, 1), dtype=F64, device=dev)
-                    self.mblk[l] = (mt, moff)
-                    prog.gemm(1, 0, [(wt.data_ptr() + 8 * int(roff[i]), B.T.ptr(B.toff[(i, j)]),
-                                      mt.data_ptr() + 8 * moff[(i, j)], int(lay.r[i]), int(lay.r[j]), int(lay.r[i]),
-                                      int(lay.r[i]), int(lay.n[j]), int(lay.r[j]), 0, 1.0, 0.0) for (i, j) in pairs])
-            if self.use_v or self.fused[l]:
-                # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
-                q = fp.dh2.q[l]
-                prog.copy([(q.data_ptr() + 8 * int(lay.qoff[i] + lay.r[i]), B.R.ptr(int(lay.qoff[i] + lay.r[i])),
-                            int(lay.n[i]), int(lay.k[i]), int(lay.n[i]), int(lay.n[i]), 0)
-                           for i in range(lay.nb) if mine[i] and lay.k[i] > 0])
-                if self.fused[l]:
-                    # no near neighbours: L(s)_ii is the only L(s) block of box i, so P4
-                    # (b_S -= L(s)_ii y) and B1 (y_R -= L(s)_ii^T x_S) fold into the transforms
-                    # through q_skel~ = q_skel - V_i L(s)_ii^T:  b_S - L(s) V^T b = q_skel~^T b,
-                    # V (y - L(s)^T x_S) + q_skel x_S = V y + q_skel~ x_S
-                    gm = []
-                    for i in range(lay.nb):
-                        ni, ri, ki = int(lay.n[i]), int(lay.r[i]), int(lay.k[i])
-                        if mine[i] and ri > 0 and ki > 0:
-                            o = int(lay.qoff[i])
-                            gm.append((B.R.ptr(o), B.H.data_ptr() + 8 * (o + ri * ni), B.R.ptr(o + ri),
-                                       ni, ki, ri, ni, ni, ni, 0, -1.0, 1.0))
-                    prog.gemm(0, 1, gm)
-        prog.lane = 0
-        self.prepare = prog.finalize()
-        self.prepare.capture()
-        self._prepared = None
+                    self.mblk[l] = (torch.zeros(max(acc, 1), dtype=F64, device=dev), moff)
+                mt, moff = self.mblk[l]
+                prog.gemm(1, 0, [(wt.data_ptr() + 8 * int(roff[i]), B.T.ptr(B.toff[(i, j)]),
+                                  mt.data_ptr() + 8 * moff[(i, j)], int(lay.r[i]), int(lay.r[j]), int(lay.r[i]),
+                                  int(lay.r[i]), int(lay.n[j]), int(lay.r[j]), 0, 1.0, 0.0) for (i, j) in pairs])
+        if self.use_v or self.fused[l]:
+            # R_i = [V_i | q_skel_i]: the spare columns of V's n x n slot take q_skel
+            q = fp.dh2.q[l]
+            prog.copy([(q.data_ptr() + 8 * int(lay.qoff[i] + lay.r[i]), B.R.ptr(int(lay.qoff[i] + lay.r[i])),
+                        int(lay.n[i]), int(lay.k[i]), int(lay.n[i]), int(lay.n[i]), 0)
+                       for i in range(lay.nb) if mine[i] and lay.k[i] > 0])
+            if self.fused[l]:
+                # no near neighbours: L(s)_ii is the only L(s) block of box i, so P4
+                # (b_S -= L(s)_ii y) and B1 (y_R -= L(s)_ii^T x_S) fold into the transforms
+                # through q_skel~ = q_skel - V_i L(s)_ii^T:  b_S - L(s) V^T b = q_skel~^T b,
+                # V (y - L(s)^T x_S) + q_skel x_S = V y + q_skel~ x_S
+                gm = []
+                for i in range(lay.nb):
+                    ni, ri, ki = int(lay.n[i]), int(lay.r[i]), int(lay.k[i])
+                    if mine[i] and ri > 0 and ki > 0:
+                        o = int(lay.qoff[i])
+                        gm.append((B.R.ptr(o), B.H.data_ptr() + 8 * (o + ri * ni), B.R.ptr(o + ri),
+                                   ni, ki, ri, ni, ni, ni, 0, -1.0, 1.0))
+                prog.gemm(0, 1, gm)
 
     def ensure_prepared(self, stream=None):
         """Run the inverse program if the factors changed since the last solve."""
