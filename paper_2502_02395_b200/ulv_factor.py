@@ -419,12 +419,12 @@ class FactorPlan:
                     prog.wait(merge_ev)
                 prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], qp + 8 * (qo[j] + r[j]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   int(n[i]), int(k[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off], split=True)
+                                 for (i, j) in own_off])
                 prog.role = "transform"
                 prog.gemm(1, 0, [(qp + 8 * (qo[i] + r[i]), MOp + 8 * (B.toff[(i, j)] + r[j]),
                                   Tp + 8 * (B.toff[(i, j)] + r[i] * n[j] + r[j]),
                                   int(k[i]), int(k[j]), int(n[i]), int(n[i]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off], split=True)
+                                 for (i, j) in own_off])
                 prog.role = None
                 ev_ss = prog.event()
                 prog.record(ev_ss)
@@ -465,7 +465,7 @@ class FactorPlan:
                         prog.wait(ev)
                 prog.gemm(0, 0, [(ap + 8 * a_off[(i, j)], B.R.ptr(qo[j]), MOp + 8 * B.toff[(i, j)],
                                   int(n[i]), int(r[j]), int(n[j]), int(n[j]), int(n[j]), int(n[j]), 0, 1.0, 0.0)
-                                 for (i, j) in own_off], split=True)
+                                 for (i, j) in own_off])
                 prob = []
                 for (i, j) in own_off:
                     ni, nj, ri, rj, kj = int(n[i]), int(n[j]), int(r[i]), int(r[j]), int(k[j])
@@ -474,7 +474,7 @@ class FactorPlan:
                     prob.append((mo + 8 * rj, Rp + 8 * qo[i], LSp + 8 * B.lsoff[(i, j)], kj, ri, ni, nj, ni, ri,
                                  0, 1.0, 0.0))
                 prog.role = "transform"
-                prog.gemm(1, 0, prob, split=True)
+                prog.gemm(1, 0, prob)
                 prog.role = None
                 prog.lane = 0
                 # ---- merge into the parent level (or the root)
