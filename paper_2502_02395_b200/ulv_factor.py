@@ -67,9 +67,14 @@ PANEL_ROWS_PER_CTA = 128
 class _LazyBlocks(Mapping):
     """Read-only dict whose values are downloaded from HBM on first access."""
 
-    def __init__(self, keys, fetch):
-        self._keys = list(keys)
-        self._set = set(self._keys)
+    def __init__(self, keys, fetch, shared=None):
+        # shared: a (key list, key set) pair cached with the plan (never mutated), so a new
+        # factors object over the same structure costs O(1) per mapping instead of O(boxes)
+        if shared is not None:
+            self._keys, self._set = shared
+        else:
+            self._keys = list(keys)
+            self._set = set(self._keys)
         self._fetch = fetch
         self._cache = {}
 
@@ -776,13 +781,23 @@ class FactorPlan:
         n, k, r, qo = lay.n, lay.k, lay.r, lay.qoff
         nb = lay.nb
         lvl = ULVLevel()
-        lvl.dims = {i: (int(r[i]), int(k[i])) for i in range(nb)}
-        mine = self.mine(l)           # distributed: only the blocks this rank computed
-        boxes = [i for i in range(nb) if mine[i]]
-        pairs = [p for p in lay.off_pairs if mine[p[0]]]
-        lvl.lr_diag = _LazyBlocks(boxes, lambda i: np.tril(_mat(B.H, int(qo[i]), int(r[i]), int(r[i]), int(n[i]))))
-        lvl.v = _LazyBlocks(boxes, lambda i: _mat(B.R, int(qo[i]), int(n[i]), int(r[i]), int(n[i])))
-        lvl.lr_off = _LazyBlocks(pairs, lambda p: _mat(B.T, B.toff[p], int(r[p[0]]), int(r[p[1]]), int(n[p[1]])))
+        # the structure (dims, key lists) is the plan's: built once, shared by every factors object
+        st = self.__dict__.setdefault("_view_struct", {}).get(l)
+        if st is None:
+            mine = self.mine(l)           # distributed: only the blocks this rank computed
+            boxes = [i for i in range(nb) if mine[i]]
+            pairs = [p for p in lay.off_pairs if mine[p[0]]]
+            keys = [(i, i) for i in boxes] + list(pairs) + [(j, i) for (i, j) in pairs]
+            st = ({i: (int(r[i]), int(k[i])) for i in range(nb)},
+                  (boxes, set(boxes)), (pairs, set(pairs)), (keys, set(keys)))
+            self._view_struct[l] = st
+        dims, sb, sp_, sk = st
+        lvl.dims = dict(dims)
+        lvl.lr_diag = _LazyBlocks(None, lambda i: np.tril(_mat(B.H, int(qo[i]), int(r[i]), int(r[i]), int(n[i]))),
+                                  shared=sb)
+        lvl.v = _LazyBlocks(None, lambda i: _mat(B.R, int(qo[i]), int(n[i]), int(r[i]), int(n[i])), shared=sb)
+        lvl.lr_off = _LazyBlocks(None, lambda p: _mat(B.T, B.toff[p], int(r[p[0]]), int(r[p[1]]), int(n[p[1]])),
+                                 shared=sp_)
 
         def ls_fetch(key):
             a, b = key
@@ -792,8 +807,7 @@ class FactorPlan:
                 return _mat(B.T, B.toff[(a, b)], int(k[a]), int(r[b]), int(n[b]), r0=int(r[a]))
             return _mat(B.LSm, B.lsoff[(b, a)], int(k[a]), int(r[b]), int(r[b]))
 
-        keys = [(i, i) for i in boxes] + list(pairs) + [(j, i) for (i, j) in pairs]
-        lvl.ls = _LazyBlocks(keys, ls_fetch)
+        lvl.ls = _LazyBlocks(None, ls_fetch, shared=sk)
         return lvl
 
 
@@ -1269,9 +1283,12 @@ def factors_from_plan(h2, plan):
         for m in (lvl.lr_diag, lvl.lr_off, lvl.ls, lvl.v):
             m._owner = f._lease
         f.levels[l] = lvl
-    for l, parents in plan.merge_pairs.items():
-        f.merge_map[l] = {(pi, pj): [(2 * pi + a, 2 * pj + b) for a in (0, 1) for b in (0, 1)]
-                          for (pi, pj) in parents}
+    mm = plan.__dict__.get("_merge_map")
+    if mm is None:
+        mm = plan._merge_map = {l: {(pi, pj): [(2 * pi + a, 2 * pj + b) for a in (0, 1) for b in (0, 1)]
+                                    for (pi, pj) in parents} for l, parents in plan.merge_pairs.items()}
+    for l, m in mm.items():
+        f.merge_map[l] = dict(m)      # per-factors dicts; the child lists are the plan's (read-only by contract)
     return f
 
 

@@ -50,3 +50,18 @@ for rep in range(2):
     f = pkg.factorize(hh)
     t1 = T()
     print(f"factorize again: {1e3 * (t1 - t0):.1f} ms", flush=True)
+
+# host-side cost of building the factors object (lazy views) after the pivot check
+from paper_2502_02395_b200.ulv_factor import factor_plan_of, factors_from_plan  # noqa: E402
+del f
+f = pkg.factorize(hh)
+fp = factor_plan_of(f)
+for rep in range(3):
+    t0 = time.perf_counter()
+    g = factors_from_plan(hh, fp)
+    t1 = time.perf_counter()
+    print(f"factors_from_plan: {1e3 * (t1 - t0):.2f} ms", flush=True)
+    del g
+t0 = time.perf_counter()
+fp.check_pivots()
+print(f"check_pivots (idle GPU): {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
