@@ -123,7 +123,7 @@ def wy_profitable(n, k, ratio=None):
     return float((4 * n * n * k + 4 * n * k * k).sum()) < ratio * float((3 * n ** 3).sum())
 
 
-WY_RATIO = float(__import__("os").environ.get("H2G_WY_RATIO", "0.5"))
+WY_RATIO = float(__import__("os").environ.get("H2G_WY_RATIO", "0.8"))
 
 
 def build_wy(lq, prog):
