@@ -120,10 +120,14 @@ def wy_profitable(n, k, ratio=None):
     if not n.size or (k <= 0).any():
         return False
     ratio = WY_RATIO if ratio is None else ratio
-    return float((4 * n * n * k + 4 * n * k * k).sum()) < ratio * float((3 * n ** 3).sum())
+    frac = float((4 * n * n * k + 4 * n * k * k).sum()) / float((3 * n ** 3).sum())
+    # past half the dense flops the thin WY GEMMs only pay on boxes large enough to keep
+    # their tiles busy (M1 levels 9 / 6 / 3, mean n >= 221, gain; C3 level 9, mean n 90, loses)
+    return frac < min(ratio, 0.5) or (frac < ratio and float(n.mean()) >= WY_MIN_N)
 
 
 WY_RATIO = float(__import__("os").environ.get("H2G_WY_RATIO", "0.8"))
+WY_MIN_N = float(__import__("os").environ.get("H2G_WY_MIN_N", "128"))
 
 
 def build_wy(lq, prog):

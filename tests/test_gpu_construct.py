@@ -210,12 +210,12 @@ def test_compact_wy_transform_equals_dense(pkg, shape, n, leaf, family, shift):
     the solve matches the CPU oracle."""
     from paper_2502_02395_b200 import basis_qr, ulv_factor
 
-    ratio = basis_qr.WY_RATIO
-    basis_qr.WY_RATIO = 100.0      # every level with k > 0 everywhere takes it (upper levels too)
+    ratio, min_n = basis_qr.WY_RATIO, basis_qr.WY_MIN_N
+    basis_qr.WY_RATIO, basis_qr.WY_MIN_N = 100.0, 0.0   # every level with k > 0 takes it (upper levels too)
     try:
         h2 = _build(pkg, shape, n, leaf, family, shift, tol=1e-8, s_far=256, s_near=256)
     finally:
-        basis_qr.WY_RATIO = ratio
+        basis_qr.WY_RATIO, basis_qr.WY_MIN_N = ratio, min_n
     dh2 = h2._device
     assert dh2.depth in dh2.wy and len(dh2.wy) >= 2
     ks = np.concatenate([dh2.levels[l].k for l in dh2.wy])

@@ -22,7 +22,7 @@ if "box" in sys.argv[1:]:
 WY = "wy" in sys.argv[1:]
 if WY:
     from paper_2502_02395_b200 import basis_qr, program as pm
-    basis_qr.WY_RATIO = 100.0
+    basis_qr.WY_RATIO, basis_qr.WY_MIN_N = 100.0, 0.0
     pm._SPLITK = 8
 cloud = pkg.gen_uniform_cube(4096, seed=0)
 tree = pkg.build_tree(cloud, 256)
